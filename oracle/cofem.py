@@ -1,0 +1,151 @@
+"""Algorithm 1 (CovarianceFreeEM) in fp64, step by step (oracle; test infrastructure only).
+
+Paper passages followed:
+  Eq. 5   Sigma^-1 mu = beta Phi^T y: mu solves A x = b, b = beta Phi^T y
+  Eq. 6   s = (1/K) sum_k p_k o Sigma p_k, with Sigma p_k = x_k solving A x = p_k
+  Eq. 7   A X = B, A = beta Phi^T Phi + diag(alpha), B = [probes | mean]
+  Eq. 8   alpha_new = 1 / (mu o mu + s)
+  §3.2   conjugate gradient, matrix-matrix applies, at most U iterations
+  Alg. 1 the EM loop; returns alpha, mu, s
+
+Readings of silent/ambiguous passages:
+  R2  column 0 of B is the mean system b0 = beta Phi^T y, columns 1..K the probes
+  R3  "block" CG = K+1 column-independent CG recurrences batched into one
+      matrix-matrix apply per iteration (per-column step scalars), not O'Leary
+      block-CG
+  R4  X0 = 0 every E-step (no warm start)
+  R5  fixed U iterations; a column freezes (stops updating) when
+      !(gamma > 0) or !(rho > 1e-30 rho0) or gamma/rho non-finite
+  R6  Jacobi preconditioner z = r / (beta colsq + alpha) (BASELINE.json); the
+      paper's plain CG is precond=False
+  R7  M-step floor 1e-12 and clamp 1e12
+  R9  Algorithm 1 returns alpha after the last M-step and mu, s of the last E-step
+"""
+import numpy as np
+
+from .operators import gram_apply
+from .philox import rademacher_probes
+
+FREEZE_TAU = 1e-30
+DEN_FLOOR = 1e-12
+ALPHA_MAX = 1e12
+
+
+class PCGReport:
+    def __init__(self, m):
+        self.frozen_at = np.full(m, -1, dtype=np.int64)   # iteration index at which a column froze
+        self.nonfinite = np.zeros(m, dtype=bool)
+        self.iters_run = 0
+        self.rho_hist = []                                # per-iteration rho (recursive residual^2, M-norm)
+
+
+def pcg(apply_A, B, diag, U, precond=True, tau=FREEZE_TAU):
+    """Jacobi-preconditioned CG on every column of B, column-independently (R3-R6).
+
+    Per column j, the textbook PCG recurrence:
+        x = 0, r = b, z = M^-1 r, p = z, rho = r^T z, rho0 = rho
+        repeat U times (skipping frozen columns):
+            q = A p,  gamma = p^T q
+            freeze if !(gamma > 0) or !(rho > tau rho0) or non-finite
+            a = rho / gamma;  x += a p;  r -= a q
+            z = M^-1 r;  rho' = r^T z;  p = z + (rho'/rho) p;  rho = rho'
+    Every x_j is materialised (no fused estimator).  Returns (X, PCGReport).
+    """
+    B = np.asarray(B, dtype=np.float64)
+    D, m = B.shape
+    minv = 1.0 / diag if precond else np.ones(D)
+    X = np.zeros((D, m))
+    R = B.copy()
+    Z = R * minv[:, None]
+    P = Z.copy()
+    rho = np.sum(R * Z, axis=0)
+    rho0 = rho.copy()
+    active = np.ones(m, dtype=bool)
+    rep = PCGReport(m)
+    for i in range(U):
+        if not active.any():
+            break
+        rep.iters_run = i + 1
+        idx = np.nonzero(active)[0]
+        Q = apply_A(P[:, idx])
+        gamma = np.sum(P[:, idx] * Q, axis=0)
+        r_i = rho[idx]
+        finite = np.isfinite(gamma) & np.isfinite(r_i)
+        ok = finite & (gamma > 0) & (r_i > tau * rho0[idx])
+        for jj, j in enumerate(idx):
+            if not ok[jj]:
+                active[j] = False
+                rep.frozen_at[j] = i
+                rep.nonfinite[j] = not finite[jj]
+        keep = ok
+        idx, Q, gamma = idx[keep], Q[:, keep], gamma[keep]
+        if idx.size == 0:
+            continue
+        a = rho[idx] / gamma
+        X[:, idx] += a * P[:, idx]
+        R[:, idx] -= a * Q
+        Z[:, idx] = R[:, idx] * minv[:, None]
+        rho_new = np.sum(R[:, idx] * Z[:, idx], axis=0)
+        b = rho_new / rho[idx]
+        P[:, idx] = Z[:, idx] + b * P[:, idx]
+        rho[idx] = rho_new
+        rep.rho_hist.append(rho.copy())
+    return X, rep
+
+
+def mean_rhs(op, y, beta):
+    """b0 = beta Phi^T y (Eq. 5)."""
+    return beta * op.apply_T(np.asarray(y, dtype=np.float64)[:, None])[:, 0]
+
+
+def jacobi_diag(op, beta, alpha):
+    """diag(A) = beta diag(Phi^T Phi) + alpha (R6)."""
+    return beta * op.colsq() + alpha
+
+
+def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=False):
+    """Simplified E-step (Alg. 1 lines 3-7; Eq. 6-7).
+
+    B = [b0 | p_1 .. p_K]  (R2),  X = LinearSolver(A, B),
+    mu = x_0,  s = (1/K) sum_k p_k o x_k (Eq. 6; Alg. 1 line 7).
+    Raises FloatingPointError if a column met a non-finite value.
+    """
+    alpha = np.asarray(alpha, dtype=np.float64)
+    b0 = mean_rhs(op, y, beta)
+    diag = jacobi_diag(op, beta, alpha)
+    Pk = rademacher_probes(op.D, K, seed, t, k_offset)
+    B = np.concatenate([b0[:, None], Pk], axis=1)
+    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), B, diag, U, precond)
+    if rep.nonfinite.any():
+        raise FloatingPointError("numerical breakdown in column %d" % int(np.argmax(rep.nonfinite)))
+    mu = X[:, 0]
+    s = np.mean(Pk * X[:, 1:], axis=1)
+    if return_x:
+        return mu, s, rep, X
+    return mu, s, rep
+
+
+def mstep(mu, s, den_floor=DEN_FLOOR, alpha_max=ALPHA_MAX):
+    """alpha = 1 / (mu o mu + s)  (Eq. 8), floored/clamped (R7)."""
+    den = np.maximum(mu * mu + s, den_floor)
+    return np.minimum(1.0 / den, alpha_max)
+
+
+def cofem_em(op, y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True, trace=None):
+    """Algorithm 1: alpha <- 1; for t in 1..T: E-step with fresh probes
+    (probe counter t0 + t), M-step.  Returns (alpha_T, mu, s) where mu, s are
+    from the last E-step (R9)."""
+    alpha = np.ones(op.D) if alpha_init is None else np.asarray(alpha_init, dtype=np.float64).copy()
+    mu = s = None
+    for t in range(t0, t0 + T):
+        mu, s, _ = estep(op, y, beta, alpha, K, seed, t, U, precond)
+        alpha = mstep(mu, s)
+        if trace is not None:
+            trace.append((alpha.copy(), mu.copy(), s.copy()))
+    return alpha, mu, s
+
+
+def support(mu, rel=1e-3):
+    """Recovered support |mu_d| > rel * max|mu| (BASELINE.json north_star; reading R16)."""
+    mu = np.asarray(mu)
+    return np.abs(mu) > rel * np.max(np.abs(mu))
