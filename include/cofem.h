@@ -1,0 +1,154 @@
+/* cofem.h — C ABI of the B200-native covariance-free EM (CoFEM) hot path.
+ *
+ * Paper: covariance-free expectation-maximization (CoFEM) for sparse Bayesian
+ * learning, arXiv 2202.12808 (/root/reference/PAPER.md, cited as P:<line>).
+ *
+ * The library implements Algorithm 1: for each EM iteration it
+ * solves  A X = B,  A = beta Phi^T Phi + diag(alpha)  (Eq. 7) for the
+ * K+1 right-hand sides B = [b0 | p_1 .. p_K] with b0 = beta Phi^T y (Eq. 5,
+ * P:60-63) and K Rademacher probes p_k (Alg. 1 l.5) by U iterations of
+ * column-independent Jacobi-preconditioned conjugate gradient batched into
+ * matrix-matrix applies (§3.2; readings R3-R6), then
+ *     mu = x_0,   s = (1/K) sum_k p_k o x_k        (Eq. 6; Alg. 1 l.7)
+ *     alpha_new = 1 / (mu o mu + s)                 (Eq. 8; floor/clamp R7)
+ *
+ * Conventions (all entry points):
+ *  - Vector arguments (alpha, mu, s, y, Phi, obs_idx, taps) may be HOST or
+ *    DEVICE pointers; the library detects which (cudaPointerGetAttributes)
+ *    and stages host buffers through its own device workspace with
+ *    cudaMemcpyAsync on the context's stream.  Device pointers must be on the
+ *    context's device.  The caller owns every buffer it passes.
+ *  - Phi (DENSE) is copied at setup (the library owns its device copy); it is
+ *    never modified.
+ *  - Every call enqueues on the context's CUDA stream and returns after one
+ *    stream synchronisation (needed to report numerical breakdown).
+ *  - A context serves one stream and is not thread-safe.
+ *  - Invalid arguments return COFEM_ERR_INVALID and leave the context
+ *    unchanged; cofem_last_error() returns a message.
+ *  - CG that does not converge within U iterations is NOT an error;
+ *    a NaN/Inf met in a recurrence freezes that column and the call returns
+ *    COFEM_ERR_NUMERIC with the column and iteration in cofem_last_report()
+ *    (S:107).  The M-step never fails (floor/clamp).
+ *  - Layout: every D-vector is contiguous, element d = coefficient index d.
+ *    DCT2 coefficient vectors are row-major images, d = r * cols + c.
+ */
+#ifndef COFEM_H
+#define COFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cofem_ctx_s* cofem_ctx;
+
+typedef enum {
+  COFEM_OK = 0,
+  COFEM_ERR_INVALID = 1,     /* bad argument / dimension mismatch */
+  COFEM_ERR_CUDA = 2,        /* CUDA runtime error */
+  COFEM_ERR_NCCL = 3,        /* reserved (collectives are done by the caller's process group) */
+  COFEM_ERR_NUMERIC = 4,     /* NaN/Inf in the CG recurrence */
+  COFEM_ERR_OOM = 5,         /* device allocation failed */
+  COFEM_ERR_UNSUPPORTED = 6  /* valid but not implemented (e.g. DCT grid not a power of two) */
+} cofem_status;
+
+typedef enum {
+  COFEM_OP_DENSE = 0,        /* Phi: N x D matrix, row-major fp32 (§4.1) */
+  COFEM_OP_DCT2_MASKED = 1,  /* Phi = S C2^T: orthonormal 2D inverse DCT, then N masked pixels (§4.2; R11) */
+  COFEM_OP_CIRCCONV = 2      /* (Phi x)_i = sum_{j<T} h_j x_{(i-j) mod D}, N = D (R12) */
+} cofem_op_kind;
+
+typedef struct {
+  int32_t kind;              /* cofem_op_kind */
+  int64_t N, D;              /* Phi is N x D */
+  /* DENSE */
+  const float* phi;          /* N x D row-major fp32, row stride ld (>= D) elements; host or device */
+  int64_t ld;
+  /* DCT2_MASKED */
+  int32_t rows, cols;        /* grid, rows * cols == D, each a power of two in [16, 1024] */
+  const int64_t* obs_idx;    /* N pixel indices (r * cols + c), sorted, distinct, in [0, D); host or device */
+  int32_t convention;        /* 0: Phi = S C2^T (paper, default); 1: Phi = S C2 */
+  /* CIRCCONV */
+  const float* taps;         /* ntaps fp32 filter taps h_j; host or device */
+  int32_t ntaps;             /* 1 <= ntaps <= 64, ntaps <= D */
+} cofem_operator;
+
+typedef struct {
+  int32_t cg_iters;          /* U >= 1: fixed CG iteration count (BASELINE north_star; R5) */
+  int32_t precond;           /* 1: Jacobi z = r / (beta colsq + alpha) (default, R6); 0: plain CG */
+  double den_floor;          /* M-step floor on mu^2 + s (default 1e-12) */
+  double alpha_max;          /* M-step clamp (default 1e12) */
+  int32_t probe_precision;   /* 0: probe columns in fp32 (fast); 1: fp64 (parity mode). The mean column is always fp64. */
+  int32_t max_probes;        /* K capacity of the workspaces (>= any K passed later) */
+} cofem_options;
+
+/* Fill *opt with the defaults above (U = 100, precond = 1, max_probes = 32). */
+void cofem_default_options(cofem_options* opt);
+
+/* Build a context: validate, copy/derive the operator (dense Phi copy; DCT
+ * mask and twiddle tables; conv Gram stencil g = autocorr(h)), compute
+ * b0 = beta Phi^T y (fp64, Eq. 5) and colsq = diag(Phi^T Phi) (fp64), and
+ * allocate all workspaces for K <= opt->max_probes.
+ *   y:           N fp32 observations, host or device
+ *   beta:        noise precision > 0 (Alg. 1 signature)
+ *   cuda_stream: cudaStream_t to enqueue on (NULL = legacy default stream)
+ * Errors: COFEM_ERR_INVALID (dims, beta <= 0, mask unsorted, ntaps out of
+ * range), COFEM_ERR_UNSUPPORTED, COFEM_ERR_OOM, COFEM_ERR_CUDA. */
+cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* y,
+                         double beta, const cofem_options* opt, void* cuda_stream);
+
+/* One simplified E-step (Alg. 1 lines 3-7; Eq. 6-7) at precision alpha:
+ *   alpha:     D fp64, every entry > 0 and finite
+ *   K:         number of probes this call solves, 1 <= K <= max_probes
+ *   seed, t:   probe stream: p_k[d] from Philox4x32-10 with key = seed and
+ *              counter (d/128, k_offset + k, t, 0x50524F42) (R8)
+ *   k_offset:  global index of this call's first probe (probe-parallel ranks)
+ *   K_total:   the K of Eq. 6's 1/K (== K on one GPU; the global K when the
+ *              probes are split over ranks: s is then this rank's partial sum)
+ *   mu, s:     out, D fp64 each
+ * Returns COFEM_OK or COFEM_ERR_NUMERIC (mu/s still written). */
+cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
+                         int32_t k_offset, int32_t K_total, double* mu, double* s);
+
+/* M-step (Eq. 8): alpha_out_d = min(1 / max(mu_d^2 + s_d, den_floor), alpha_max). Never fails. */
+cofem_status cofem_mstep(cofem_ctx ctx, const double* mu, const double* s, double* alpha_out);
+
+/* Algorithm 1: `iters` EM iterations with fresh probes each (probe counter
+ * t = t0 + i), starting from alpha_init (NULL: all ones, Alg. 1 l.1).
+ * Outputs alpha after the last M-step and mu, s of the last E-step (R9);
+ * any output may be NULL.  cofem_em(ctx, 1, K, seed, 0, NULL, ...) equals
+ * cofem_estep(alpha = 1, t = 0) followed by cofem_mstep. */
+cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, int32_t t0,
+                      const double* alpha_init, double* alpha_out, double* mu_out, double* s_out);
+
+typedef struct {
+  int32_t cols;                   /* K + 1 columns of the last E-step (column 0 = mean, R2) */
+  int32_t cg_iters;               /* U */
+  const int32_t* frozen_at;       /* [cols] iteration at which a column froze, -1 if never (R5) */
+  const double* rho;              /* [cols] final recursive M^-1-norm residual^2 r^T z */
+  const double* rho0;             /* [cols] initial r^T z */
+  int32_t bad_col, bad_iter;      /* first column that met NaN/Inf, -1 if none */
+  double estep_ms_last;           /* device time of the last E-step (CUDA events) */
+  int64_t launches;               /* kernels launched by this context so far */
+} cofem_report;
+
+/* Report of the last E-step; the pointers stay valid until the next call on ctx. */
+cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out);
+
+/* Per-kernel-class device timing (CUDA events around each launch of the
+ * classes in `mask` on the context stream; bit i = class i, see
+ * cofem_kernel_class_name).  cofem_profile_read syncs and returns, for class
+ * i, the summed milliseconds and launch count since the last reset. */
+cofem_status cofem_profile_enable(cofem_ctx ctx, uint32_t mask);
+cofem_status cofem_profile_read(cofem_ctx ctx, int32_t cls, double* total_ms, int64_t* count, int32_t reset);
+const char* cofem_kernel_class_name(int32_t cls);   /* NULL past the last class */
+
+const char* cofem_last_error(cofem_ctx ctx);        /* message of the last failing call ("" if none); ctx may be NULL */
+const char* cofem_version(void);
+void cofem_destroy(cofem_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COFEM_H */

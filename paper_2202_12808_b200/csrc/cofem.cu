@@ -1,0 +1,751 @@
+// cofem.cu — C ABI, context, fused CG vector kernels and the E-step / EM driver.
+//
+// Paper map: Algorithm 1; Eq. 5 b0; Eq. 6 s
+// (P:74-78); Eq. 7 batched system; Eq. 8 M-step; CG §3.2
+// (P:96-98).  Readings R2-R9 are listed in DESIGN.md §3.
+//
+// Data layout in HBM: every column is a contiguous D-vector
+// padded to Dp (multiple of 2048, zero padding).  Column 0 (mean system) is
+// fp64 in its own arrays x0/r0/p0/q0; probe columns 1..K are a [K][Dp] block
+// in probe precision TP (fp32 fast / fp64 parity).  The probe x_k are never
+// stored: s accumulates (a_k/K) p_k o p_k^(i) every iteration (x_k = sum_i a_k p_k^(i)).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace cofem {
+
+static const char* kClassNames[KC_COUNT] = {
+    "probe_bits", "pcg_init", "pcg_direction", "pcg_update", "finalize_mstep",
+    "dense_phi_p", "dense_phiT_w", "dct_rows_inv", "dct_cols", "dct_rows_fwd",
+    "conv_apply", "setup"};
+
+// ------------------------------------------------------------------ bookkeeping
+static cudaEvent_t pool_get(Ctx* c) {
+  if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+  cudaEvent_t e; cudaEventCreate(&e); return e;
+}
+
+void launch_begin(Ctx* c, int cls) {
+  if (c->prof_mask & (1u << cls)) {
+    Ctx::Rec r{cls, pool_get(c), pool_get(c)};
+    cudaEventRecord(r.a, c->stream);
+    c->prof_recs.push_back(r);
+  }
+}
+
+void launch_end(Ctx* c, int cls) {
+  c->launches++;
+  if (c->prof_mask & (1u << cls)) cudaEventRecord(c->prof_recs.back().b, c->stream);
+}
+
+cudaError_t check_launch(Ctx* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e;
+}
+
+static void prof_collect(Ctx* c) {
+  if (c->prof_recs.empty()) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& r : c->prof_recs) {
+    float ms = 0; cudaEventElapsedTime(&ms, r.a, r.b);
+    c->prof_ms[r.cls] += ms; c->prof_cnt[r.cls] += 1;
+    c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b);
+  }
+  c->prof_recs.clear();
+}
+
+// ------------------------------------------------------------------ vector kernels
+template <typename TP>
+struct VecArgs {
+  int64_t D, Dp; int K; int m; int64_t wpc;
+  double beta; int precond;
+  const double* alpha; const double* colsq; const double* b0;
+  double* dinv64; TP* dinvp;
+  double *x0, *r0, *p0, *q0;
+  TP *R, *P, *Q;
+  double* s;
+  const uint32_t* bits;
+  ColState* cs; double* part; int part_stride; unsigned* counter;
+  double invK;
+};
+
+__global__ void k_probe_bits(uint32_t* __restrict__ bits, int64_t wpc, int K, int64_t nblk128,
+                             int k_offset, int t, uint2 key) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)K * nblk128) return;
+  int k = (int)(idx / nblk128);
+  int64_t b = idx - (int64_t)k * nblk128;
+  uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(k_offset + k), (uint32_t)t, PROBE_TAG), key);
+  *reinterpret_cast<uint4*>(bits + (int64_t)k * wpc + b * 4) = w;
+}
+
+template <typename T> __device__ __forceinline__ void ld8(const T* p, T (&v)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) v[e] = p[e];
+}
+template <> __device__ __forceinline__ void ld8<float>(const float* p, float (&v)[8]) {
+  float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <> __device__ __forceinline__ void ld8<double>(const double* p, double (&v)[8]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { double2 a = reinterpret_cast<const double2*>(p)[e]; v[2 * e] = a.x; v[2 * e + 1] = a.y; }
+}
+template <typename T> __device__ __forceinline__ void st8(T* p, const T (&v)[8]);
+template <> __device__ __forceinline__ void st8<float>(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <> __device__ __forceinline__ void st8<double>(double* p, const double (&v)[8]) {
+#pragma unroll
+  for (int e = 0; e < 4; ++e) reinterpret_cast<double2*>(p)[e] = make_double2(v[2 * e], v[2 * e + 1]);
+}
+
+// Per-CTA reduction scratch: red[warp][column]; only warp w writes row w (deterministic).
+struct VecShared {
+  double red[VEC_THREADS / 32][MAXM];
+  double a[MAXM];
+  int act[MAXM];
+  bool last;
+};
+
+// After the tile loop: CTA partials -> part[j][bx]; the last CTA reduces them in fixed
+// order and applies `fin(j, sum)` (one warp per column).
+template <typename Fin>
+__device__ void vec_finish(VecShared& sh, double* part, int stride, unsigned* counter, int m, Fin fin) {
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < VEC_THREADS / 32; ++w) v += sh.red[w][j];
+    part[(int64_t)j * stride + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sh.last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!sh.last) return;
+  __threadfence();
+  int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < m; j += nw) {
+    double v = reduce_partials(part + (int64_t)j * stride, gridDim.x);
+    if ((threadIdx.x & 31) == 0) fin(j, v);
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// a2: X = 0, R = B, Z = M^-1 R, P = Z, rho = R^T Z; diag(A) = beta colsq + alpha (R6); s = 0.
+template <typename TP>
+__global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
+  __shared__ VecShared sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < a.m; j += blockDim.x)
+    for (int w = 0; w < VEC_THREADS / 32; ++w) sh.red[w][j] = 0.0;
+  __syncthreads();
+  const int64_t ntiles = a.Dp / VEC_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
+    double dv[8], al[8], cq[8], bb[8];
+    ld8(a.alpha + d0, al); ld8(a.colsq + d0, cq); ld8(a.b0 + d0, bb);
+    TP dp[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      bool valid = d0 + e < a.D;
+      double diag = a.beta * cq[e] + al[e];
+      dv[e] = valid ? (a.precond ? 1.0 / diag : 1.0) : 0.0;
+      dp[e] = (TP)dv[e];
+    }
+    st8(a.dinv64 + d0, dv); st8(a.dinvp + d0, dp);
+    double z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    st8(a.s + d0, z8); st8(a.x0 + d0, z8);
+    double p8[8], acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { p8[e] = dv[e] * bb[e]; acc += bb[e] * p8[e]; }
+    st8(a.r0 + d0, bb); st8(a.p0 + d0, p8);
+    acc = warp_sum(acc);
+    if (lane == 0) sh.red[warp][0] += acc;
+    for (int k = 0; k < a.K; ++k) {
+      uint32_t w = (a.bits[(int64_t)k * a.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
+      TP r[8], p[8];
+      double acck = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        bool valid = d0 + e < a.D;
+        r[e] = valid ? (((w >> e) & 1u) ? (TP)-1 : (TP)1) : (TP)0;
+        p[e] = dp[e] * r[e];
+        acck += (double)r[e] * (double)p[e];
+      }
+      st8(a.R + (int64_t)k * a.Dp + d0, r); st8(a.P + (int64_t)k * a.Dp + d0, p);
+      acck = warp_sum(acck);
+      if (lane == 0) sh.red[warp][k + 1] += acck;
+    }
+  }
+  ColState* cs = a.cs;
+  vec_finish(sh, a.part, a.part_stride, a.counter, a.m, [cs](int j, double v) {
+    ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
+    c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+    cs[j] = c;
+  });
+}
+
+// a5: r -= a q; x0 += a0 p0; s += (a_k/K) p_k o P_k; z = M^-1 r; rho' = r^T z; then
+// (last CTA) b = rho'/rho, rho = rho'.
+template <typename TP>
+__global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
+  __shared__ VecShared sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < a.m; j += blockDim.x) {
+    ColState c = a.cs[j];
+    sh.act[j] = !c.frozen;
+    sh.a[j] = c.a;
+    for (int w = 0; w < VEC_THREADS / 32; ++w) sh.red[w][j] = 0.0;
+  }
+  __syncthreads();
+  const int64_t ntiles = a.Dp / VEC_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
+    if (sh.act[0]) {
+      const double a0 = sh.a[0];
+      double x[8], r[8], p[8], q[8], dv[8], acc = 0.0;
+      ld8(a.x0 + d0, x); ld8(a.r0 + d0, r); ld8(a.p0 + d0, p); ld8(a.q0 + d0, q); ld8(a.dinv64 + d0, dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        x[e] = fma(a0, p[e], x[e]);
+        r[e] = fma(-a0, q[e], r[e]);
+        acc += r[e] * (dv[e] * r[e]);
+      }
+      st8(a.x0 + d0, x); st8(a.r0 + d0, r);
+      acc = warp_sum(acc);
+      if (lane == 0) sh.red[warp][0] += acc;
+    }
+    TP dp[8];
+    ld8(a.dinvp + d0, dp);
+    double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool any = false;
+    for (int k = 0; k < a.K; ++k) {
+      if (!sh.act[k + 1]) continue;
+      any = true;
+      const double ak = sh.a[k + 1];
+      const TP akt = (TP)ak;
+      const double aks = ak * a.invK;
+      uint32_t w = (a.bits[(int64_t)k * a.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
+      TP r[8], q[8], p[8];
+      TP* Rk = a.R + (int64_t)k * a.Dp + d0;
+      ld8(Rk, r); ld8(a.Q + (int64_t)k * a.Dp + d0, q); ld8(a.P + (int64_t)k * a.Dp + d0, p);
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        r[e] = r[e] - akt * q[e];
+        TP z = dp[e] * r[e];
+        acc += (double)r[e] * (double)z;
+        double pe = (double)p[e];
+        sacc[e] += ((w >> e) & 1u) ? -aks * pe : aks * pe;
+      }
+      st8(Rk, r);
+      acc = warp_sum(acc);
+      if (lane == 0) sh.red[warp][k + 1] += acc;
+    }
+    if (any) {
+      double sv[8];
+      ld8(a.s + d0, sv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sv[e] += sacc[e];
+      st8(a.s + d0, sv);
+    }
+  }
+  ColState* cs = a.cs;
+  vec_finish(sh, a.part, a.part_stride, a.counter, a.m, [cs](int j, double v) {
+    ColState c = cs[j];
+    if (c.frozen) return;
+    c.b = v / c.rho;
+    c.rho = v;
+    cs[j] = c;
+  });
+}
+
+// a6: P_j = M^-1 R_j + b_j P_j  (separate kernel for dense / conv; fused into DCT pass A).
+template <typename TP>
+__global__ void __launch_bounds__(VEC_THREADS) k_dir(VecArgs<TP> a) {
+  const int j = blockIdx.y;
+  const ColState c = a.cs[j];
+  if (c.frozen) return;
+  const int64_t ntiles = a.Dp / VEC_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
+    if (j == 0) {
+      double r[8], p[8], dv[8];
+      ld8(a.r0 + d0, r); ld8(a.p0 + d0, p); ld8(a.dinv64 + d0, dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p[e] = fma(c.b, p[e], dv[e] * r[e]);
+      st8(a.p0 + d0, p);
+    } else {
+      TP r[8], p[8], dv[8];
+      TP* Pk = a.P + (int64_t)(j - 1) * a.Dp + d0;
+      ld8(a.R + (int64_t)(j - 1) * a.Dp + d0, r); ld8(Pk, p); ld8(a.dinvp + d0, dv);
+      const TP bt = (TP)c.b;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p[e] = dv[e] * r[e] + bt * p[e];
+      st8(Pk, p);
+    }
+  }
+}
+
+// a8 + a9: mu = x0, s, and (optionally) the M-step alpha = min(1/max(mu^2+s, floor), amax) (Eq. 8).
+__global__ void k_finalize(int64_t D, const double* __restrict__ x0, const double* __restrict__ s,
+                           double* __restrict__ mu_out, double* __restrict__ s_out, double* __restrict__ alpha_out,
+                           double den_floor, double alpha_max) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    double mu = x0[d], sv = s[d];
+    if (mu_out) mu_out[d] = mu;
+    if (s_out) s_out[d] = sv;
+    if (alpha_out) alpha_out[d] = fmin(1.0 / fmax(mu * mu + sv, den_floor), alpha_max);
+  }
+}
+
+__global__ void k_mstep(int64_t D, const double* __restrict__ mu, const double* __restrict__ s,
+                        double* __restrict__ alpha_out, double den_floor, double alpha_max) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    double m = mu[d];
+    alpha_out[d] = fmin(1.0 / fmax(m * m + s[d], den_floor), alpha_max);
+  }
+}
+
+__global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* __restrict__ bad) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    double v = alpha[d];
+    if (!(v > 0.0) || !isfinite(v)) atomicExch(bad, 1);
+  }
+}
+
+template <typename TP>
+static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
+  VecArgs<TP> a;
+  a.D = c->D; a.Dp = c->Dp; a.K = K; a.m = K + 1; a.wpc = c->Dp / 32;
+  a.beta = c->beta; a.precond = c->opt.precond;
+  a.alpha = c->alpha; a.colsq = c->colsq; a.b0 = c->b0;
+  a.dinv64 = c->dinv64; a.dinvp = (TP*)c->dinvp;
+  a.x0 = c->x0; a.r0 = c->r0; a.p0 = c->p0; a.q0 = c->q0;
+  a.R = (TP*)c->R; a.P = (TP*)c->P; a.Q = (TP*)c->Q;
+  a.s = c->s; a.bits = c->bits;
+  a.cs = c->cs; a.part = c->part; a.part_stride = c->part_stride; a.counter = c->counters + MAXM;
+  a.invK = invK;
+  return a;
+}
+
+
+cofem_status launch_dir(Ctx* c, int m) {
+  int K = m - 1;
+  dim3 grid((unsigned)std::min<int64_t>(c->Dp / VEC_TILE, (int64_t)c->num_sms * 4), m);
+  launch_begin(c, KC_DIR);
+  if (c->probe64) k_dir<double><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, 0));
+  else k_dir<float><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, 0));
+  launch_end(c, KC_DIR);
+  return check_launch(c, "k_dir") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
+// ------------------------------------------------------------------ helpers
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(_e);            \
+      return _e == cudaErrorMemoryAllocation ? COFEM_ERR_OOM : COFEM_ERR_CUDA; \
+    }                                                                         \
+  } while (0)
+
+template <typename T>
+static cofem_status dalloc(Ctx* c, T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) { c->err = std::string("cudaMalloc: ") + cudaGetErrorString(e); return COFEM_ERR_OOM; }
+  e = cudaMemsetAsync(*p, 0, n * sizeof(T), c->stream);
+  if (e != cudaSuccess) { c->err = cudaGetErrorString(e); return COFEM_ERR_CUDA; }
+  return COFEM_OK;
+}
+#define ALLOC(p, n) do { cofem_status _s = dalloc(c, &(p), (n)); if (_s != COFEM_OK) return _s; } while (0)
+
+// Stage a D-vector input: device pointers are used in place, host ones copied.
+static cofem_status stage_in(Ctx* c, const double* src, double* dst_ws, const double** use) {
+  if (is_device_ptr(src)) { *use = src; return COFEM_OK; }
+  CK(cudaMemcpyAsync(dst_ws, src, c->D * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  *use = dst_ws;
+  return COFEM_OK;
+}
+
+static cofem_status validate_alpha(Ctx* c, const double* alpha_dev) {
+  int* bad; CK(cudaMalloc(&bad, sizeof(int)));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+  k_check_alpha<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, alpha_dev, bad);
+  int hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  cudaFree(bad);
+  if (hb) { c->err = "alpha must be positive and finite"; return COFEM_ERR_INVALID; }
+  return COFEM_OK;
+}
+
+// ------------------------------------------------------------------ E-step driver
+// Runs Alg. 1 lines 3-7 with alpha already in c->alpha.  No host sync inside.
+static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offset, int K_total) {
+  const int m = K + 1;
+  const double invK = 1.0 / (double)K_total;
+  const int64_t nblk128 = c->Dp / 128;
+  uint2 key = make_uint2((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
+  {
+    int64_t n = (int64_t)K * nblk128;
+    launch_begin(c, KC_PROBES);
+    k_probe_bits<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->bits, c->Dp / 32, K, nblk128, k_offset, t, key);
+    launch_end(c, KC_PROBES);
+    if (check_launch(c, "k_probe_bits")) return COFEM_ERR_CUDA;
+  }
+  launch_begin(c, KC_INIT);
+  if (c->probe64) k_init<double><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
+  else k_init<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
+  launch_end(c, KC_INIT);
+  if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
+  for (int it = 0; it < c->opt.cg_iters; ++it) {
+    cofem_status st;
+    if (c->kind == COFEM_OP_DCT2_MASKED) {
+      st = dct_apply(c, m, it, it > 0);
+    } else {
+      if (it > 0 && (st = launch_dir(c, m)) != COFEM_OK) return st;
+      st = c->kind == COFEM_OP_DENSE ? dense_apply(c, m, it) : conv_apply(c, m, it);
+    }
+    if (st != COFEM_OK) return st;
+    launch_begin(c, KC_UPDATE);
+    if (c->probe64) k_update<double><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
+    else k_update<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
+    launch_end(c, KC_UPDATE);
+    if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
+  }
+  return COFEM_OK;
+}
+
+// Read the column states back (the one end-of-E-step sync) and fill the report.
+static cofem_status estep_report(Ctx* c, int m) {
+  c->cs_host.resize(m);
+  CK(cudaMemcpyAsync(c->cs_host.data(), c->cs, m * sizeof(ColState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->last_cols = m;
+  c->frozen_host.resize(m); c->rho_host.resize(m); c->rho0_host.resize(m);
+  c->bad_col = -1; c->bad_iter = -1;
+  for (int j = 0; j < m; ++j) {
+    c->frozen_host[j] = c->cs_host[j].frozen_at;
+    c->rho_host[j] = c->cs_host[j].rho;
+    c->rho0_host[j] = c->cs_host[j].rho0;
+    if (c->cs_host[j].nonfinite && c->bad_col < 0) { c->bad_col = j; c->bad_iter = c->cs_host[j].frozen_at; }
+  }
+  if (c->bad_col >= 0) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "numerical breakdown (NaN/Inf) in column %d at CG iteration %d", c->bad_col, c->bad_iter);
+    c->err = buf;
+    return COFEM_ERR_NUMERIC;
+  }
+  return COFEM_OK;
+}
+
+}  // namespace cofem
+
+using namespace cofem;
+
+// ====================================================================== C ABI
+extern "C" {
+
+struct cofem_ctx_s { Ctx c; };
+
+static thread_local std::string g_err;
+
+void cofem_default_options(cofem_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof *o);
+  o->cg_iters = 100; o->precond = 1; o->den_floor = 1e-12; o->alpha_max = 1e12;
+  o->probe_precision = 0; o->max_probes = 32;
+}
+
+const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
+
+const char* cofem_kernel_class_name(int32_t cls) {
+  return (cls >= 0 && cls < KC_COUNT) ? kClassNames[cls] : nullptr;
+}
+
+const char* cofem_last_error(cofem_ctx ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
+
+static void free_all(Ctx* c) {
+  void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
+                  c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
+                  c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
+                  c->ws1, c->ws2, c->ws1d, c->ws2d};
+  for (void* p : ptrs) if (p) cudaFree(p);
+  for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+}
+
+void cofem_destroy(cofem_ctx ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->c.stream);
+  free_all(&ctx->c);
+  delete ctx;
+}
+
+static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y, double beta, const cofem_options* opt) {
+  if (!op || !y || !opt) { c->err = "null argument"; return COFEM_ERR_INVALID; }
+  if (!(beta > 0.0) || !isfinite(beta)) { c->err = "beta must be > 0"; return COFEM_ERR_INVALID; }
+  if (op->D < 1 || op->N < 1) { c->err = "N, D must be >= 1"; return COFEM_ERR_INVALID; }
+  if (opt->cg_iters < 1) { c->err = "cg_iters must be >= 1"; return COFEM_ERR_INVALID; }
+  if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
+  if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
+  c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
+  c->probe64 = opt->probe_precision != 0;
+  c->Kcap = opt->max_probes; c->m_cap = c->Kcap + 1;
+  c->Dp = ((c->D + VEC_TILE - 1) / VEC_TILE) * VEC_TILE;
+  CK(cudaGetDevice(&c->device));
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
+
+  const size_t tp = c->probe64 ? sizeof(double) : sizeof(float);
+  const int64_t Dp = c->Dp;
+  ALLOC(c->b0, Dp); ALLOC(c->colsq, Dp); ALLOC(c->alpha, Dp); ALLOC(c->dinv64, Dp);
+  { char* p; ALLOC(p, Dp * tp); c->dinvp = p; }
+  ALLOC(c->x0, Dp); ALLOC(c->r0, Dp); ALLOC(c->p0, Dp); ALLOC(c->q0, Dp); ALLOC(c->s, Dp);
+  ALLOC(c->mu_out, Dp); ALLOC(c->s_out, Dp); ALLOC(c->alpha_out, Dp);
+  { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->R = p; }
+  { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->P = p; }
+  { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->Q = p; }
+  ALLOC(c->bits, (size_t)c->Kcap * (Dp / 32));
+  ALLOC(c->cs, c->m_cap);
+  ALLOC(c->counters, MAXM + 1);
+  c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
+  c->part_stride = std::max(c->vec_grid, 1);
+
+  // y to device
+  const float* y_dev = y;
+  float* y_tmp = nullptr;
+  if (!is_device_ptr(y)) {
+    CK(cudaMalloc(&y_tmp, c->N * sizeof(float)));
+    CK(cudaMemcpyAsync(y_tmp, y, c->N * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    y_dev = y_tmp;
+  }
+  cofem_status st = COFEM_ERR_INVALID;
+  if (op->kind == COFEM_OP_DENSE) {
+    if (op->ld < op->D || !op->phi) { c->err = "DENSE: phi NULL or ld < D"; st = COFEM_ERR_INVALID; }
+    else {
+      c->ld = op->D;
+      cudaError_t e = cudaMalloc(&c->phi, (size_t)op->N * op->D * sizeof(float));
+      if (e != cudaSuccess) { c->err = "cudaMalloc phi"; st = COFEM_ERR_OOM; }
+      else {
+        e = cudaMemcpy2DAsync(c->phi, op->D * sizeof(float), op->phi, op->ld * sizeof(float),
+                              op->D * sizeof(float), op->N, cudaMemcpyDefault, c->stream);
+        st = e == cudaSuccess ? dense_setup(c, y_dev) : COFEM_ERR_CUDA;
+        if (e != cudaSuccess) c->err = cudaGetErrorString(e);
+      }
+    }
+  } else if (op->kind == COFEM_OP_DCT2_MASKED) {
+    c->rows = op->rows; c->cols = op->cols; c->conv = op->convention;
+    auto pow2 = [](int v) { return v >= 16 && v <= 1024 && (v & (v - 1)) == 0; };
+    if ((int64_t)op->rows * op->cols != op->D || op->N > op->D || !op->obs_idx) {
+      c->err = "DCT2: rows*cols must equal D, N <= D, obs_idx non-NULL"; st = COFEM_ERR_INVALID;
+    } else if (!pow2(op->rows) || !pow2(op->cols)) {
+      c->err = "DCT2: rows and cols must be powers of two in [16, 1024]"; st = COFEM_ERR_UNSUPPORTED;
+    } else if (op->convention != 0 && op->convention != 1) {
+      c->err = "DCT2: convention must be 0 or 1"; st = COFEM_ERR_INVALID;
+    } else {
+      // validate the mask on the host (sorted, distinct, in range)
+      std::vector<int64_t> h(op->N);
+      cudaError_t e = cudaMemcpy(h.data(), op->obs_idx, op->N * sizeof(int64_t), cudaMemcpyDefault);
+      if (e != cudaSuccess) { c->err = cudaGetErrorString(e); st = COFEM_ERR_CUDA; }
+      else {
+        bool ok = h[0] >= 0 && h[op->N - 1] < op->D;
+        for (int64_t i = 1; ok && i < op->N; ++i) ok = h[i] > h[i - 1];
+        if (!ok) { c->err = "DCT2: obs_idx must be sorted, distinct, in [0, D)"; st = COFEM_ERR_INVALID; }
+        else {
+          int64_t* od = nullptr;
+          e = cudaMalloc(&od, op->N * sizeof(int64_t));
+          if (e == cudaSuccess) e = cudaMemcpyAsync(od, h.data(), op->N * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream);
+          st = e == cudaSuccess ? dct_setup(c, y_dev, od) : COFEM_ERR_CUDA;
+          cudaStreamSynchronize(c->stream);
+          if (od) cudaFree(od);
+        }
+      }
+    }
+  } else if (op->kind == COFEM_OP_CIRCCONV) {
+    if (op->N != op->D || op->ntaps < 1 || op->ntaps > 64 || op->ntaps > op->D || !op->taps) {
+      c->err = "CIRCCONV: need N == D, 1 <= ntaps <= min(64, D), taps non-NULL"; st = COFEM_ERR_INVALID;
+    } else {
+      std::vector<float> h(op->ntaps);
+      cudaError_t e = cudaMemcpy(h.data(), op->taps, op->ntaps * sizeof(float), cudaMemcpyDefault);
+      c->ntaps = op->ntaps;
+      st = e == cudaSuccess ? conv_setup(c, y_dev, h.data()) : COFEM_ERR_CUDA;
+    }
+  } else {
+    c->err = "unknown operator kind";
+  }
+  cudaStreamSynchronize(c->stream);
+  if (y_tmp) cudaFree(y_tmp);
+  if (st != COFEM_OK) return st;
+  ALLOC(c->part, (size_t)c->m_cap * c->part_stride);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaGetLastError());
+  return COFEM_OK;
+}
+
+cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* y, double beta,
+                         const cofem_options* opt, void* cuda_stream) {
+  if (!out) { g_err = "out is NULL"; return COFEM_ERR_INVALID; }
+  *out = nullptr;
+  cofem_ctx ctx = new cofem_ctx_s();
+  ctx->c.stream = (cudaStream_t)cuda_stream;
+  cofem_status st = setup_impl(&ctx->c, op, y, beta, opt);
+  if (st != COFEM_OK) {
+    g_err = ctx->c.err;
+    free_all(&ctx->c);
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return COFEM_OK;
+}
+
+static cofem_status estep_impl(Ctx* c, const double* alpha, int32_t K, uint64_t seed, int32_t t,
+                               int32_t k_offset, int32_t K_total, double* mu, double* s) {
+  if (!alpha) { c->err = "alpha is NULL"; return COFEM_ERR_INVALID; }
+  if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes] (S:148)"; return COFEM_ERR_INVALID; }
+  if (K_total < K || k_offset < 0) { c->err = "need K_total >= K and k_offset >= 0"; return COFEM_ERR_INVALID; }
+  const double* a_dev;
+  cofem_status st = stage_in(c, alpha, c->alpha, &a_dev);
+  if (st) return st;
+  if (a_dev != c->alpha) CK(cudaMemcpyAsync(c->alpha, a_dev, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if ((st = validate_alpha(c, c->alpha))) return st;
+  CK(cudaEventRecord(c->ev0, c->stream));
+  if ((st = estep_device(c, K, seed, t, k_offset, K_total))) return st;
+  const bool mu_dev = mu && is_device_ptr(mu), s_dev = s && is_device_ptr(s);
+  launch_begin(c, KC_FINAL);
+  k_finalize<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, c->x0, c->s, mu_dev ? mu : c->mu_out,
+                                                     s_dev ? s : c->s_out, nullptr, c->opt.den_floor, c->opt.alpha_max);
+  launch_end(c, KC_FINAL);
+  if (check_launch(c, "k_finalize")) return COFEM_ERR_CUDA;
+  CK(cudaEventRecord(c->ev1, c->stream));
+  if (mu && !mu_dev) CK(cudaMemcpyAsync(mu, c->mu_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (s && !s_dev) CK(cudaMemcpyAsync(s, c->s_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  st = estep_report(c, K + 1);
+  float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->estep_ms = ms;
+  prof_collect(c);
+  return st;
+}
+
+cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
+                         int32_t k_offset, int32_t K_total, double* mu, double* s) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  ctx->c.err.clear();
+  return estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, mu, s);
+}
+
+cofem_status cofem_mstep(cofem_ctx ctx, const double* mu, const double* s, double* alpha_out) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  Ctx* c = &ctx->c;
+  c->err.clear();
+  if (!mu || !s || !alpha_out) { c->err = "null argument"; return COFEM_ERR_INVALID; }
+  const double *mu_d, *s_d;
+  cofem_status st;
+  if ((st = stage_in(c, mu, c->mu_out, &mu_d))) return st;
+  if ((st = stage_in(c, s, c->s_out, &s_d))) return st;
+  const bool out_dev = is_device_ptr(alpha_out);
+  launch_begin(c, KC_FINAL);
+  k_mstep<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, mu_d, s_d, out_dev ? alpha_out : c->alpha_out,
+                                                  c->opt.den_floor, c->opt.alpha_max);
+  launch_end(c, KC_FINAL);
+  if (check_launch(c, "k_mstep")) return COFEM_ERR_CUDA;
+  if (!out_dev) CK(cudaMemcpyAsync(alpha_out, c->alpha_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return COFEM_OK;
+}
+
+cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, int32_t t0,
+                      const double* alpha_init, double* alpha_out, double* mu_out, double* s_out) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  Ctx* c = &ctx->c;
+  c->err.clear();
+  if (iters < 1) { c->err = "iters must be >= 1"; return COFEM_ERR_INVALID; }
+  if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes] (S:148)"; return COFEM_ERR_INVALID; }
+  cofem_status st;
+  if (alpha_init) {
+    const double* a_dev;
+    if ((st = stage_in(c, alpha_init, c->alpha, &a_dev))) return st;
+    if (a_dev != c->alpha) CK(cudaMemcpyAsync(c->alpha, a_dev, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if ((st = validate_alpha(c, c->alpha))) return st;
+  } else {
+    std::vector<double> ones(c->D, 1.0);   // Alg. 1 line 1
+    CK(cudaMemcpyAsync(c->alpha, ones.data(), c->D * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  const bool a_dev = alpha_out && is_device_ptr(alpha_out);
+  const bool m_dev = mu_out && is_device_ptr(mu_out);
+  const bool s_dev = s_out && is_device_ptr(s_out);
+  for (int i = 0; i < iters; ++i) {
+    CK(cudaEventRecord(c->ev0, c->stream));
+    if ((st = estep_device(c, K, seed, t0 + i, 0, K))) return st;
+    const bool lastit = i == iters - 1;
+    launch_begin(c, KC_FINAL);
+    // the M-step writes the next alpha in place (the E-step state no longer needs it)
+    k_finalize<<<c->num_sms * 4, 256, 0, c->stream>>>(
+        c->D, c->x0, c->s, lastit ? (m_dev ? mu_out : c->mu_out) : nullptr,
+        lastit ? (s_dev ? s_out : c->s_out) : nullptr, c->alpha, c->opt.den_floor, c->opt.alpha_max);
+    launch_end(c, KC_FINAL);
+    if (check_launch(c, "k_finalize")) return COFEM_ERR_CUDA;
+    CK(cudaEventRecord(c->ev1, c->stream));
+    st = estep_report(c, K + 1);
+    float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->estep_ms = ms;
+    if (st != COFEM_OK) return st;
+  }
+  if (alpha_out) CK(cudaMemcpyAsync(alpha_out, c->alpha, c->D * sizeof(double), a_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (mu_out && !m_dev) CK(cudaMemcpyAsync(mu_out, c->mu_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (s_out && !s_dev) CK(cudaMemcpyAsync(s_out, c->s_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  return COFEM_OK;
+}
+
+cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out) {
+  if (!ctx || !out) { g_err = "null argument"; return COFEM_ERR_INVALID; }
+  Ctx* c = &ctx->c;
+  out->cols = c->last_cols; out->cg_iters = c->opt.cg_iters;
+  out->frozen_at = c->frozen_host.data(); out->rho = c->rho_host.data(); out->rho0 = c->rho0_host.data();
+  out->bad_col = c->bad_col; out->bad_iter = c->bad_iter;
+  out->estep_ms_last = c->estep_ms; out->launches = c->launches;
+  return COFEM_OK;
+}
+
+cofem_status cofem_profile_enable(cofem_ctx ctx, uint32_t mask) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  ctx->c.prof_mask = mask;
+  return COFEM_OK;
+}
+
+cofem_status cofem_profile_read(cofem_ctx ctx, int32_t cls, double* total_ms, int64_t* count, int32_t reset) {
+  if (!ctx || cls < 0 || cls >= KC_COUNT) { g_err = "bad argument"; return COFEM_ERR_INVALID; }
+  Ctx* c = &ctx->c;
+  prof_collect(c);
+  if (total_ms) *total_ms = c->prof_ms[cls];
+  if (count) *count = c->prof_cnt[cls];
+  if (reset) { c->prof_ms[cls] = 0; c->prof_cnt[cls] = 0; }
+  return COFEM_OK;
+}
+
+}  // extern "C"

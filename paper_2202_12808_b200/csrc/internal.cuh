@@ -1,0 +1,202 @@
+// internal.cuh — shared declarations of the CoFEM CUDA library (sm_100a).
+// Product code: nothing here is shared with, or derived from, oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/cofem.h"
+
+namespace cofem {
+
+// ---------------------------------------------------------------- constants
+constexpr int MAXM = 129;              // max columns (K + 1) supported by the fused vector kernels
+constexpr int VEC_THREADS = 256;       // vector kernels: threads per CTA
+constexpr int VEC_ELEMS = 8;           // elements per thread per tile
+constexpr int VEC_TILE = VEC_THREADS * VEC_ELEMS;   // 2048 d per tile
+constexpr double FREEZE_TAU = 1e-30;   // reading R5
+constexpr uint32_t PROBE_TAG = 0x50524F42u;
+
+enum KernelClass : int {
+  KC_PROBES = 0, KC_INIT, KC_DIR, KC_UPDATE, KC_FINAL,
+  KC_DENSE_PHI_P, KC_DENSE_PHIT_W,
+  KC_DCT_ROWS_INV, KC_DCT_COLS, KC_DCT_ROWS_FWD,
+  KC_CONV_APPLY, KC_SETUP, KC_COUNT
+};
+
+// Per-column CG scalars (device).  Column 0 = mean system (R2).
+struct ColState {
+  double rho, rho0, gamma, a, b;
+  int frozen;       // 1 once a freeze rule fired (R5)
+  int frozen_at;    // iteration index, -1 if never
+  int nonfinite;    // the freeze was caused by NaN/Inf
+  int pad;
+};
+
+template <typename T> struct cplx { T x, y; };
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+  int kind = 0;
+  int64_t N = 0, D = 0, Dp = 0;        // Dp: D padded to a multiple of VEC_TILE (zero padding)
+  double beta = 0;
+  cofem_options opt{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  bool probe64 = false;                 // probe columns in fp64
+  int Kcap = 0, m_cap = 0;              // workspace capacity (columns = Kcap + 1)
+
+  // operator data
+  float* phi = nullptr; int64_t ld = 0; // DENSE device copy, row-major N x ld
+  int rows = 0, cols = 0, conv = 0;     // DCT2
+  uint8_t* mask_vvT = nullptr;          // DCT2: mask in v-order, transposed [cols][rows]
+  void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu
+  void* dct_tab64 = nullptr;            // (double)
+  int ntaps = 0;                        // CIRCCONV
+  float* taps = nullptr;                // fp32 h (device)
+  double* g64 = nullptr;                // Gram stencil g_l, l = -(T-1)..(T-1), fp64
+  float* g32 = nullptr;                 // same, fp32
+
+  double* b0 = nullptr;                 // beta Phi^T y (fp64, Dp)
+  double* colsq = nullptr;              // diag(Phi^T Phi) (fp64, Dp)
+
+  // E-step state
+  double* alpha = nullptr;              // fp64 Dp
+  double* dinv64 = nullptr;             // 1 / diag(A) fp64
+  void* dinvp = nullptr;                // same in probe precision
+  double *x0 = nullptr, *r0 = nullptr, *p0 = nullptr, *q0 = nullptr;  // mean column (fp64)
+  void *R = nullptr, *P = nullptr, *Q = nullptr;                       // probe block [Kcap][Dp]
+  double* s = nullptr;                  // accumulated (1/K) sum p_k o x_k  (fp64 Dp)
+  double* mu_out = nullptr;             // staging for outputs
+  double* s_out = nullptr;
+  double* alpha_out = nullptr;
+  uint32_t* bits = nullptr;             // probe signs [Kcap][Dp/32]
+  ColState* cs = nullptr;               // [m_cap]
+  double* part = nullptr;               // per-CTA partial sums [m_cap][part_stride]
+  int part_stride = 0;
+  unsigned* counters = nullptr;         // last-block counters [m_cap + 1]
+  int vec_grid = 0;                     // CTAs of the fused vector kernels
+
+  // operator scratch
+  void* ws1 = nullptr; void* ws2 = nullptr;   // probe-precision scratch (dense W partials / DCT T1,T2)
+  double* ws1d = nullptr; double* ws2d = nullptr;   // mean-column scratch
+  int dense_splits = 1;
+
+  // host mirrors for the report
+  std::vector<ColState> cs_host;
+  std::vector<int32_t> frozen_host;
+  std::vector<double> rho_host, rho0_host;
+  int last_cols = 0;
+  int bad_col = -1, bad_iter = -1;
+  double estep_ms = 0;
+  int64_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // profiling
+  uint32_t prof_mask = 0;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  double prof_ms[KC_COUNT] = {0};
+  int64_t prof_cnt[KC_COUNT] = {0};
+
+  std::string err;
+};
+
+// launch bookkeeping: call around every kernel launch
+void launch_begin(Ctx* c, int cls);
+void launch_end(Ctx* c, int cls);
+cudaError_t check_launch(Ctx* c, const char* what);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), product-side implementation.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u; k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Finish a per-column reduction of `n` CTA partials in fixed order (deterministic).
+// Called by one full warp.
+__device__ __forceinline__ double reduce_partials(const double* __restrict__ p, int n) {
+  double v = 0.0;
+  for (int i = threadIdx.x & 31; i < n; i += 32) v += __ldcg(p + i);   // L2: written by other CTAs
+  return warp_sum(v);
+}
+
+// Freeze rule + step length after gamma_j is known (R5): executed by one thread.
+__device__ __forceinline__ void finish_gamma(ColState& c, double gamma, int iter) {
+  if (c.frozen) return;
+  c.gamma = gamma;
+  bool finite = isfinite(gamma) && isfinite(c.rho);
+  bool ok = finite && (gamma > 0.0) && (c.rho > FREEZE_TAU * c.rho0);
+  if (!ok) {
+    c.frozen = 1; c.frozen_at = iter; c.nonfinite = finite ? 0 : 1; c.a = 0.0;
+  } else {
+    c.a = c.rho / gamma;
+  }
+}
+
+// Per-column reduction of one CTA value v (already CTA-reduced, valid in thread 0):
+// part[j][bx] = v; the last CTA of column j (grid.x CTAs) reduces in fixed order and
+// calls fin(sum) from one thread.  Requires blockDim.x >= 32 and all threads present.
+template <typename Fin>
+__device__ __forceinline__ void column_finish(double v, int j, double* part, int stride, unsigned* counters,
+                                              Fin fin) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    part[(int64_t)j * stride + blockIdx.x] = v;
+    __threadfence();
+    s_last = (atomicAdd(counters + j, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double tot = reduce_partials(part + (int64_t)j * stride, gridDim.x);
+    if (threadIdx.x == 0) { fin(tot); counters[j] = 0u; }
+  }
+}
+
+// CTA-wide sum of one double per thread (result valid in thread 0). blockDim.x <= 1024.
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double s_w[32];
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) s_w[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = lane < nw ? s_w[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------- operator launchers
+// every apply computes Q = A P for all active columns and finishes gamma_j / a_j.
+cofem_status dense_setup(Ctx* c, const float* y_dev);
+cofem_status dense_apply(Ctx* c, int m, int iter);
+cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev);
+cofem_status dct_apply(Ctx* c, int m, int iter, bool dir);   // direction update fused into pass A
+cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host);
+cofem_status conv_apply(Ctx* c, int m, int iter);
+
+// vector kernels (cofem.cu)
+cofem_status launch_dir(Ctx* c, int m);
+
+}  // namespace cofem

@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded inputs and the same Philox probes.  Bars (BASELINE.json north_star):
+rel. L2 error <= 1e-4 on mu and s after one E-step, <= 1e-3 on final 1/alpha and
+mu after all EM iterations, identical recovered support |mu_d| > 1e-3 max|mu|.
+Parity mode (fp64 probe columns) is held to 1e-9 / 1e-8."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import closed_forms as cf
+from oracle.cofem import cofem_em, estep, support
+from oracle.operators import CircConvOp, DCT2MaskedOp, DenseOp
+from oracle.philox import rademacher_probes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2202_12808_b200 import build
+    build.build()
+    torch.cuda.set_device(0)
+
+
+def ctx_of(w, **kw):
+    from paper_2202_12808_b200 import Context
+    return Context.from_workload(w, **kw)
+
+
+def op_of(w):
+    if w.kind == "dense":
+        return DenseOp(w.phi)
+    if w.kind == "dct2_masked":
+        return DCT2MaskedOp(w.rows, w.cols, w.obs_idx, w.convention)
+    return CircConvOp(w.taps, w.D)
+
+
+def dev(n):
+    return torch.empty(n, dtype=torch.float64, device="cuda")
+
+
+def gpu_estep(ctx, w, alpha, K, seed, t):
+    a = torch.as_tensor(alpha, dtype=torch.float64, device="cuda").contiguous()
+    mu, s = dev(w.D), dev(w.D)
+    ctx.estep(a, K, seed, t, mu, s)
+    return mu.cpu().numpy(), s.cpu().numpy()
+
+
+def gpu_em(ctx, w, T, K, seed, t0=0, alpha_init=None):
+    ao, mu, s = dev(w.D), dev(w.D), dev(w.D)
+    ai = None if alpha_init is None else torch.as_tensor(alpha_init, device="cuda").contiguous()
+    ctx.em(T, K, seed, t0, ai, ao, mu, s)
+    return ao.cpu().numpy(), mu.cpu().numpy(), s.cpu().numpy()
+
+
+SMALL = [
+    synth.preset("C1"),                                                  # dense 100 x 400 (full config 1)
+    synth.dense(250, 1000, 20, K=32, U=200, T=5, seed=1, name="dense_ragged_250x1000"),
+    synth.dct(64, 64, 1024, 41, K=32, U=200, T=5, seed=0),
+    synth.dct(32, 128, 1024, 40, K=12, U=150, T=4, seed=2),            # rows != cols
+    synth.dct(128, 128, 4096, 163, K=8, U=200, T=3, seed=3),
+    synth.circconv(4099, 64, 4, K=16, U=150, T=5, seed=0),              # ragged D
+    synth.circconv(20000, 64, 20, K=8, U=150, T=3, seed=4),
+]
+
+
+@pytest.mark.parametrize("w", SMALL, ids=lambda w: w.name)
+def test_estep1_parity(w):
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 5, 0)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 5, 0, w.U)
+    assert rel(mu, omu) <= 1e-4 and rel(s, os_) <= 1e-4, (rel(mu, omu), rel(s, os_))
+    rep = ctx.report()
+    assert rep["cols"] == w.K + 1 and rep["bad_col"] == -1
+
+
+@pytest.mark.parametrize("w", SMALL, ids=lambda w: w.name)
+def test_em_parity_and_support(w):
+    ctx = ctx_of(w)
+    T = min(w.T, 5)
+    a, mu, s = gpu_em(ctx, w, T, w.K, 11)
+    oa, omu, os_ = cofem_em(op_of(w), w.y, w.beta, T, w.K, 11, w.U)
+    assert rel(1 / a, 1 / oa) <= 1e-3 and rel(mu, omu) <= 1e-3, (rel(1 / a, 1 / oa), rel(mu, omu))
+    sg, so = support(mu), support(omu)
+    flips = np.nonzero(sg != so)[0]
+    if flips.size:   # certify: every flip sits at the threshold (SURVEY.md §8(c) fragility note)
+        mx = np.max(np.abs(omu))
+        margin = np.abs(np.abs(omu[flips]) / mx - 1e-3)
+        assert flips.size <= 2 and np.all(margin < 1e-5), (flips, margin)
+
+
+def test_full_em_c1_30_iterations():
+    w = synth.preset("C1")
+    ctx = ctx_of(w)
+    a, mu, s = gpu_em(ctx, w, w.T, w.K, 0)
+    oa, omu, os_ = cofem_em(op_of(w), w.y, w.beta, w.T, w.K, 0, w.U)
+    assert rel(1 / a, 1 / oa) <= 1e-3 and rel(mu, omu) <= 1e-3
+    assert np.array_equal(support(mu), support(omu))
+
+
+@pytest.mark.parametrize("w", [SMALL[1], SMALL[2], SMALL[5]], ids=lambda w: w.name)
+def test_parity_mode_fp64_probes(w):
+    ctx = ctx_of(w, probe_precision=1)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 3, 1, w.U)
+    assert rel(mu, omu) <= 1e-9 and rel(s, os_) <= 1e-8, (rel(mu, omu), rel(s, os_))
+    a, mu, s = gpu_em(ctx, w, 3, w.K, 3)
+    oa, omu, _ = cofem_em(op_of(w), w.y, w.beta, 3, w.K, 3, w.U)
+    assert rel(1 / a, 1 / oa) <= 1e-8 and np.array_equal(support(mu), support(omu))
+
+
+def test_probes_match_oracle_through_estimator():
+    # A = I + beta Phi^T Phi with U = 1 and no preconditioner: x_k = (p^T p / p^T A p) p_k, so
+    # s_d = (1/K) sum_k D / (p_k^T A p_k): any probe bit error changes s at O(1/K).
+    w = synth.dense(30, 256, 3, K=5, U=1, T=1, seed=2)
+    ctx = ctx_of(w, precond=0)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 123456789012345, 9)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 123456789012345, 9, 1, precond=False)
+    assert rel(s, os_) < 1e-6 and rel(mu, omu) < 1e-6
+
+
+def test_edge_cases_k1_u1_phi_zero():
+    w = synth.dense(8, 40, 2, K=1, U=1, T=1, seed=0)
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), 1, 0, 0)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), 1, 0, 0, 1)
+    assert rel(mu, omu) < 1e-6 and rel(s, os_) < 1e-5
+    z = synth.dense(8, 40, 2, K=4, U=5, T=1, seed=0)
+    z.phi = np.zeros_like(z.phi)
+    ctx = ctx_of(z)
+    mu, s = gpu_estep(ctx, z, np.ones(z.D), 4, 0, 0)
+    assert np.all(mu == 0) and np.allclose(s, 1.0, rtol=0, atol=1e-7)
+
+
+def test_invalid_arguments_rejected():
+    from paper_2202_12808_b200 import CofemError, Context, OP_DCT2_MASKED
+    w = synth.dct(32, 32, 100, 5, K=4, U=10, T=1, seed=0)
+    ctx = ctx_of(w)
+    with pytest.raises(CofemError) as e:
+        gpu_estep(ctx, w, np.ones(w.D), 0, 0, 0)                              # K = 0
+    assert e.value.status == 1
+    with pytest.raises(CofemError):
+        gpu_estep(ctx, w, np.ones(w.D), 5, 0, 0)                              # K > max_probes
+    bad = np.ones(w.D); bad[3] = -1.0
+    with pytest.raises(CofemError):
+        gpu_estep(ctx, w, bad, 2, 0, 0)                                       # alpha <= 0
+    with pytest.raises(CofemError) as e:
+        Context(OP_DCT2_MASKED, 100, w.D, w.y, w.beta, rows=32, cols=32, obs_idx=w.obs_idx[::-1].copy())
+    assert e.value.status == 1
+    with pytest.raises(CofemError) as e:
+        Context(OP_DCT2_MASKED, 100, 24 * 32, w.y, w.beta, rows=24, cols=32, obs_idx=w.obs_idx)
+    assert e.value.status == 6
+    with pytest.raises(CofemError):
+        Context(OP_DCT2_MASKED, 100, w.D, w.y, -1.0, rows=32, cols=32, obs_idx=w.obs_idx)   # beta <= 0
+
+
+def test_nan_reports_numeric_breakdown():
+    from paper_2202_12808_b200 import CofemError
+    w = synth.dense(20, 64, 2, K=2, U=5, T=1, seed=0)
+    w.phi = w.phi.copy()
+    w.phi[3, 7] = np.nan
+    ctx = ctx_of(w)
+    with pytest.raises(CofemError) as e:
+        gpu_estep(ctx, w, np.ones(w.D), 2, 0, 0)
+    assert e.value.status == 4
+    assert ctx.report()["bad_col"] >= 0
+
+
+def test_determinism_and_host_pointers():
+    w = SMALL[2]
+    ctx = ctx_of(w)
+    a1 = gpu_em(ctx, w, 2, w.K, 4)
+    a2 = gpu_em(ctx, w, 2, w.K, 4)
+    for x, y in zip(a1, a2):
+        assert np.array_equal(x, y)
+    ah, mh, sh = np.empty(w.D), np.empty(w.D), np.empty(w.D)          # host buffers through the C ABI
+    ctx.em(2, w.K, 4, 0, None, ah, mh, sh)
+    assert np.array_equal(ah, a1[0]) and np.array_equal(mh, a1[1]) and np.array_equal(sh, a1[2])
+
+
+def test_em_equals_estep_mstep_and_resume():
+    w = SMALL[5]
+    ctx = ctx_of(w)
+    a2, mu2, s2 = gpu_em(ctx, w, 2, w.K, 8)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 8, 0)
+    a1 = dev(w.D)
+    ctx.mstep(torch.as_tensor(mu, device="cuda"), torch.as_tensor(s, device="cuda"), a1)
+    mu_b, s_b = gpu_estep(ctx, w, a1.cpu().numpy(), w.K, 8, 1)
+    assert np.array_equal(mu_b, mu2) and np.array_equal(s_b, s2)
+    ar, mur, sr = gpu_em(ctx, w, 1, w.K, 8, t0=1, alpha_init=a1.cpu().numpy())
+    assert np.array_equal(ar, a2) and np.array_equal(mur, mu2)
+
+
+def test_probe_parallel_partial_s_sums_to_full():
+    # probe-parallel ranks: k_offset / K_total give partial s that sum to the single-GPU s
+    w = SMALL[2]
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 6, 2)
+    parts = []
+    for r in range(4):
+        a = torch.ones(w.D, dtype=torch.float64, device="cuda")
+        m_r, s_r = dev(w.D), dev(w.D)
+        ctx.estep(a, w.K // 4, 6, 2, m_r, s_r, k_offset=r * (w.K // 4), K_total=w.K)
+        parts.append(s_r.cpu().numpy())
+        assert np.array_equal(m_r.cpu().numpy(), mu)
+    assert rel(np.sum(parts, axis=0), s) < 1e-12
+
+
+# ------------------------------------------------------------ full-size checks (bench launch config)
+def test_c4_full_estep1_closed_form():
+    """Config 4 at full size (1024 x 1024, N = 2^18, K = 32, U = 200): E-step 1 vs the
+    closed form mu = b0/(beta+1), x_k = p_k - beta/(beta+1) P p_k (oracle/closed_forms.py)."""
+    w = synth.preset("C4")
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 0, 0)
+    P = rademacher_probes(w.D, w.K, 0, 0)
+    emu, es, _ = cf.masked_dct_estep1(w.rows, w.cols, w.obs_idx, w.y, w.beta, P)
+    assert rel(mu, emu) <= 1e-4 and rel(s, es) <= 1e-4, (rel(mu, emu), rel(s, es))
+
+
+def test_c4_full_sampled_oracle_iterations():
+    """Config 4 at full size, U = 3: the oracle's 3-iteration iterate (not converged, so
+    it checks the recurrence itself) against the GPU, every element."""
+    w = synth.preset("C4")
+    w.U = 3
+    ctx = ctx_of(w, cg_iters=3, max_probes=4)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), 4, 1, 0)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), 4, 1, 0, 3)
+    assert rel(mu, omu) <= 1e-6 and rel(s, os_) <= 1e-5, (rel(mu, omu), rel(s, os_))
+
+
+def test_c5_full_size_vs_fft_closed_form():
+    """Config 5 at full size (D = 2^24, 64 taps) with K = 4 probes solved to convergence
+    (U = 1500) against the FFT diagonalisation (oracle/closed_forms.py item 3)."""
+    w = synth.preset("C5")
+    ctx = ctx_of(w, cg_iters=1500, max_probes=4)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), 4, 2, 0)
+    P = rademacher_probes(w.D, 4, 2, 0)
+    emu, es, _ = cf.circconv_estep(w.taps, w.D, w.y, w.beta, 1.0, P)
+    assert rel(mu, emu) <= 1e-4 and rel(s, es) <= 1e-4, (rel(mu, emu), rel(s, es))
