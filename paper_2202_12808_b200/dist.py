@@ -1,0 +1,38 @@
+"""Probe-parallel CoFEM over ranks (one process per GPU; BASELINE north_star multi-GPU mode).
+
+The K probe columns of Eq. 7 are independent systems (reading R3), so rank r
+solves probes [k_offset, k_offset + K_r) with their GLOBAL indices in the Philox
+counter (reading R8) plus a replica of the deterministic mean column; the only
+exchange is one sum-allreduce of the partial s = (1/K) sum_{k in rank} p_k o x_k
+per E-step (Eq. 6), after which every rank applies the M-step (Eq. 8) itself.
+The collective is injected (torch.distributed NCCL on GPUs, gloo in the CPU
+tests); this module holds only the host-side orchestration.
+"""
+
+
+def probe_split(K, world, rank):
+    """Contiguous split of K probes over `world` ranks: (k_offset, K_local)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if K < world:
+        raise ValueError("probe-parallel needs K >= world (every rank solves >= 1 probe)")
+    base, extra = divmod(K, world)
+    K_local = base + (1 if rank < extra else 0)
+    k_offset = rank * base + min(rank, extra)
+    return k_offset, K_local
+
+
+def em_probe_parallel(estep, mstep, allreduce_sum, T, K, seed, rank, world, alpha, mu, s, t0=0):
+    """Algorithm 1 with the probes split over ranks.
+
+    estep(alpha, K_local, seed, t, mu, s, k_offset, K_total) writes mu and this
+    rank's partial s; allreduce_sum(s) sums s over ranks in place; mstep(mu, s,
+    alpha) overwrites alpha.  Returns (alpha, mu, s) of the last iteration (R9).
+    """
+    k_offset, K_local = probe_split(K, world, rank)
+    for t in range(t0, t0 + T):
+        estep(alpha, K_local, seed, t, mu, s, k_offset, K)
+        if world > 1:
+            allreduce_sum(s)
+        mstep(mu, s, alpha)
+    return alpha, mu, s
