@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""bench.py — CoFEM hot path on B200 (BASELINE.json metric: EM iters/s and CG
+RHS-operator-applies/s at D = 2^20; % of HBM roofline).
+
+A step = one EM iteration of Algorithm 1: probes, Jacobi-PCG with
+U iterations on the K+1 columns, s, M-step — every row of SURVEY.md §8(a) —
+on the synthetic workload of BASELINE config 4 (masked 1024 x 1024 DCT,
+N = 2^18, K = 32, U = 200), with alpha carried from step to step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C4]
+
+N > 1 (torchrun, one process per GPU): probe-parallel — each rank solves its
+share of the K probes plus a replica of the mean column; one NCCL all-reduce of
+s per E-step; total work fixed ("strong").  --impl reference times the CPU
+fp64 oracle (oracle/) on a bounded sample (rank 0 only).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "EM iters/s and CG RHS-operator-applies/s at D=2^20; % of HBM/compute roofline"
+UNIT = "EM iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.lines, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic bytes per launch
+def algorithmic_bytes(cls, w, K_local):
+    """Bytes the algorithm must move per launch of kernel class `cls`:
+    fp32 probe columns (4 B), fp64 mean column (8 B), D elements per column."""
+    D, K = w.D, K_local
+    if cls == "dct_rows_inv":      # read r, p; write p (direction); write T1; dinv once
+        return D * (16 * K + 32 + 4 + 8)
+    if cls == "dct_cols":          # read T1, write T2
+        return D * (8 * K + 16)
+    if cls == "dct_rows_fwd":      # read T2, p; write q; alpha once
+        return D * (12 * K + 24 + 8)
+    if cls == "pcg_update":        # probes r,q,p read + r write; mean x,r,p,q,dinv read + x,r write; s rmw; dinv; bits
+        return D * (16 * K + 56 + 16 + 4) + D * K // 8
+    if cls == "pcg_direction":     # r, p read, p write (+dinv)
+        return D * (12 * K + 24 + 12)
+    if cls == "conv_apply":        # p read, q write, alpha once
+        return D * (8 * K + 16 + 8)
+    if cls == "dense_phiT_w":      # Phi once, p read, q write, alpha
+        return w.N * D * 4 + D * (8 * K + 16 + 8)
+    if cls == "dense_phi_p":
+        return w.N * D * 4 + D * (4 * K + 8)
+    return None
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def cpu_sample(w, seed=0):
+    """Time the oracle (as it stands) on a bounded sample of one E-step of w: the
+    setup part (probes, b0, Jacobi diagonal) and one PCG iteration of all K+1
+    columns; E-step time = setup + U x iteration (the oracle's PCG cost is
+    linear in U).  Returns (EM iters/s, description, threads)."""
+    import numpy as np
+
+    from oracle.cofem import jacobi_diag, mean_rhs, pcg
+    from oracle.operators import CircConvOp, DCT2MaskedOp, DenseOp, gram_apply
+    from oracle.philox import rademacher_probes
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    if w.kind == "dense":
+        op = DenseOp(w.phi)
+    elif w.kind == "dct2_masked":
+        op = DCT2MaskedOp(w.rows, w.cols, w.obs_idx, w.convention)
+    else:
+        op = CircConvOp(w.taps, w.D)
+    alpha = np.ones(w.D)
+    t0 = time.perf_counter()
+    b0 = mean_rhs(op, w.y, w.beta)
+    diag = jacobi_diag(op, w.beta, alpha)
+    P = rademacher_probes(w.D, w.K, seed, 0)
+    B = np.concatenate([b0[:, None], P], axis=1)
+    t1 = time.perf_counter()
+    pcg(lambda V: gram_apply(op, w.beta, alpha, V), B, diag, 1)
+    t2 = time.perf_counter()
+    est = (t1 - t0) + w.U * (t2 - t1)
+    desc = ("oracle E-step setup + 1 of U=%d PCG iterations on all %d columns of %s (%.1f s measured), "
+            "E-step time extrapolated linearly in U" % (w.U, w.K + 1, w.name, t2 - t0))
+    return 1.0 / est, desc, threads, t2 - t0
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    import synth
+    w = synth.preset(args.workload, seed=args.seed)
+    for _ in range(args.warmup):
+        cpu_sample(w, args.seed)
+    vals, descs, threads = [], None, 1
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, descs, threads, _ = cpu_sample(w, args.seed)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = len(vals) / sum(1.0 / v for v in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": w.name, **w.config()},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": descs},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if args.warmup < 3:
+        raise SystemExit("timing rules: --warmup must be >= 3")
+
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_2202_12808_b200 import Context
+    from paper_2202_12808_b200.dist import probe_split
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    w = synth.preset(args.workload, seed=args.seed)
+    k_off, K_loc = probe_split(w.K, world, rank)
+    ctx = Context.from_workload(w, max_probes=K_loc)
+    D = w.D
+    alpha = torch.ones(D, dtype=torch.float64, device=dev)
+    mu = torch.empty_like(alpha)
+    s = torch.empty_like(alpha)
+    seed = args.seed
+
+    def step(t, a_in, a_out, m_out, s_out):
+        if world == 1:
+            ctx.em(1, w.K, seed, t, a_in, a_out, m_out, s_out)
+        else:
+            ctx.estep(a_in, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
+            torch.distributed.all_reduce(s)
+            ctx.mstep(mu, s, alpha)
+            if a_out is not alpha:
+                a_out.copy_(alpha)
+            if m_out is not None and m_out is not mu:
+                m_out.copy_(mu)
+            if s_out is not None and s_out is not s:
+                s_out.copy_(s)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    t = 0
+    for _ in range(args.warmup):
+        step(t, alpha, alpha, mu, s)
+        t += 1
+    # ---- device-timed region (inputs resident in HBM)
+    classes = ["dct_rows_inv", "dct_cols", "dct_rows_fwd", "pcg_update", "pcg_direction", "conv_apply",
+               "dense_phi_p", "dense_phiT_w", "pcg_init", "probe_bits", "finalize_mstep"]
+    ctx.profile_enable(classes)
+    for c in classes:
+        ctx.profile_read(c, reset=True)
+    clk = ClockSampler(local)
+    clk.start()
+    barrier()
+    launches0 = ctx.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step(t, alpha, alpha, mu, s)
+        t += 1
+    e1.record()
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    prof = {c: ctx.profile_read(c) for c in classes}
+    ctx.profile_enable([])
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = args.steps / (ms / 1000.0)
+    rhs_applies = (w.K + 1) * w.U * args.steps / (ms / 1000.0)
+
+    # ---- end-to-end through the C ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        a_h = torch.empty(D, dtype=torch.float64).pin_memory()
+        m_h = torch.empty(D, dtype=torch.float64).pin_memory()
+        s_h = torch.empty(D, dtype=torch.float64).pin_memory()
+        a_h.copy_(alpha.cpu())
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.steps):
+            if world == 1:
+                ctx.em(1, w.K, seed, t, a_h, a_h, m_h, s_h)      # h2d alpha; d2h alpha, mu, s
+            else:
+                ctx.estep(a_h, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
+                torch.distributed.all_reduce(s)
+                ctx.mstep(mu, s, a_h)
+                m_h.copy_(mu); s_h.copy_(s)
+            t += 1
+        f1.record()
+        barrier()
+        ems = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(ems, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": args.steps / (float(ems.item()) / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": D * 8, "d2h_bytes_per_step": 3 * D * 8}
+
+    # ---- roofline of the dominant kernel (live CUDA events over the timed region)
+    pk, pk_kind = peaks()
+    dom = max((c for c in classes if prof[c][1] > 0), key=lambda c: prof[c][0])
+    tot_ms, cnt = prof[dom]
+    avg_ms = tot_ms / cnt
+    byt = algorithmic_bytes(dom, w, K_loc)
+    achieved = byt / (avg_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+    share = {c: round(prof[c][0] / ms, 4) for c in classes if prof[c][1] > 0}
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_kind,
+            "algorithmic_bytes_per_launch": byt, "avg_launch_ms": avg_ms, "launches": cnt,
+            "share_of_step": share}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, desc, threads, _ = cpu_sample(w, seed)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32 (probe columns) + f64 (mean column)",
+                "data": "synthetic",
+                "config": {"workload": w.name, **w.config(), "parallelism": "probe-parallel x%d" % world,
+                           "K_per_rank": K_loc,
+                           "l2": "inputs larger than L2 (working set %.0f MB > 126 MB)" % (
+                               (w.K + 1) * D * 4 * 5 / 1e6)},
+                "rhs_applies_per_s": rhs_applies, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+                "clocks": clocks, "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
