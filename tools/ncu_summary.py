@@ -1,0 +1,54 @@
+#!/usr/bin/env python
+"""Summarise ncu outputs into markdown for profiles/ (launch list shares + full-set key metrics).
+
+    python tools/ncu_summary.py launches gpurun_out/launches.csv
+    python tools/ncu_summary.py full gpurun_out/prof.ncu-rep
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+        "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum", "launch__grid_size",
+        "launch__block_size"]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hd = rows[h]
+    ki, vi, ui = hd.index("Kernel Name"), hd.index("Metric Value"), hd.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+    tot = sum(v for _, v in agg.values())
+    out = ["| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+    for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append("| %s | %d | %.1f | %.2f | %.3f |" % (k, n, v, v / n, v / tot))
+    return "\n".join(out)
+
+
+def full(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hd, units = rows[0], rows[1]
+    idx = {k: hd.index(k) for k in KEYS if k in hd}
+    out = ["| kernel | " + " | ".join("%s (%s)" % (k, units[i]) for k, i in idx.items()) + " |",
+           "|---|" + "---|" * len(idx)]
+    for r in rows[2:]:
+        out.append("| %s | " % r[hd.index("Kernel Name")].split("(")[0] + " | ".join(r[i] for i in idx.values()) + " |")
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    print(launches(sys.argv[2]) if sys.argv[1] == "launches" else full(sys.argv[2]))
