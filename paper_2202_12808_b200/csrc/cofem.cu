@@ -24,7 +24,7 @@ namespace cofem {
 static const char* kClassNames[KC_COUNT] = {
     "probe_bits", "pcg_init", "pcg_direction", "pcg_update", "finalize_mstep",
     "dense_phi_p", "dense_phiT_w", "dct_rows_inv", "dct_cols", "dct_rows_fwd",
-    "conv_apply", "setup"};
+    "conv_apply", "mean_column", "setup"};
 
 // ------------------------------------------------------------------ bookkeeping
 static cudaEvent_t pool_get(Ctx* c) {
@@ -32,17 +32,23 @@ static cudaEvent_t pool_get(Ctx* c) {
   cudaEvent_t e; cudaEventCreate(&e); return e;
 }
 
-void launch_begin(Ctx* c, int cls) {
+void launch_begin(Ctx* c, int cls, cudaStream_t st) {
   if (c->prof_mask & (1u << cls)) {
-    Ctx::Rec r{cls, pool_get(c), pool_get(c)};
-    cudaEventRecord(r.a, c->stream);
+    if (!st) st = c->stream;
+    Ctx::Rec r{cls, pool_get(c), pool_get(c), st};
+    cudaEventRecord(r.a, st);
     c->prof_recs.push_back(r);
   }
 }
 
-void launch_end(Ctx* c, int cls) {
+void launch_end(Ctx* c, int cls, cudaStream_t st) {
   c->launches++;
-  if (c->prof_mask & (1u << cls)) cudaEventRecord(c->prof_recs.back().b, c->stream);
+  if (c->prof_mask & (1u << cls)) {
+    if (!st) st = c->stream;
+    // the matching begin is the last record of this stream
+    for (auto it = c->prof_recs.rbegin(); it != c->prof_recs.rend(); ++it)
+      if (it->st == st) { cudaEventRecord(it->b, st); break; }
+  }
 }
 
 cudaError_t check_launch(Ctx* c, const char* what) {
@@ -53,6 +59,7 @@ cudaError_t check_launch(Ctx* c, const char* what) {
 
 static void prof_collect(Ctx* c) {
   if (c->prof_recs.empty()) return;
+  if (c->side) cudaStreamSynchronize(c->side);
   cudaStreamSynchronize(c->stream);
   for (auto& r : c->prof_recs) {
     float ms = 0; cudaEventElapsedTime(&ms, r.a, r.b);
@@ -68,7 +75,8 @@ struct VecArgs {
   int64_t D, Dp; int K; int m; int64_t wpc;
   double beta; int precond;
   const double* alpha; const double* colsq; const double* b0;
-  double* dinv64; TP* dinvp;
+  double* dinv64; TP* dinvp; TP* alphap;
+  int jlo, jhi;     // columns [jlo, jhi) processed by k_update (0 = mean system)
   double *x0, *r0, *p0, *q0;
   TP *R, *P, *Q;
   double* s;
@@ -120,9 +128,9 @@ struct VecShared {
 // After the tile loop: CTA partials -> part[j][bx]; the last CTA reduces them in fixed
 // order and applies `fin(j, sum)` (one warp per column).
 template <typename Fin>
-__device__ void vec_finish(VecShared& sh, double* part, int stride, unsigned* counter, int m, Fin fin) {
+__device__ void vec_finish(VecShared& sh, double* part, int stride, unsigned* counter, int jlo, int jhi, Fin fin) {
   __syncthreads();
-  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+  for (int j = jlo + threadIdx.x; j < jhi; j += blockDim.x) {
     double v = 0.0;
 #pragma unroll
     for (int w = 0; w < VEC_THREADS / 32; ++w) v += sh.red[w][j];
@@ -135,7 +143,7 @@ __device__ void vec_finish(VecShared& sh, double* part, int stride, unsigned* co
   if (!sh.last) return;
   __threadfence();
   int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int j = warp; j < m; j += nw) {
+  for (int j = jlo + warp; j < jhi; j += nw) {
     double v = reduce_partials(part + (int64_t)j * stride, gridDim.x);
     if ((threadIdx.x & 31) == 0) fin(j, v);
   }
@@ -164,6 +172,12 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
       dp[e] = (TP)dv[e];
     }
     st8(a.dinv64 + d0, dv); st8(a.dinvp + d0, dp);
+    {
+      TP ap[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ap[e] = (TP)al[e];
+      st8(a.alphap + d0, ap);
+    }
     double z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     st8(a.s + d0, z8); st8(a.x0 + d0, z8);
     double p8[8], acc = 0.0;
@@ -189,7 +203,7 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
     }
   }
   ColState* cs = a.cs;
-  vec_finish(sh, a.part, a.part_stride, a.counter, a.m, [cs](int j, double v) {
+  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs](int j, double v) {
     ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
     c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
     cs[j] = c;
@@ -202,7 +216,7 @@ template <typename TP>
 __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
   __shared__ VecShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = threadIdx.x; j < a.m; j += blockDim.x) {
+  for (int j = a.jlo + threadIdx.x; j < a.jhi; j += blockDim.x) {
     ColState c = a.cs[j];
     sh.act[j] = !c.frozen;
     sh.a[j] = c.a;
@@ -210,9 +224,10 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
   }
   __syncthreads();
   const int64_t ntiles = a.Dp / VEC_TILE;
+  const int klo = a.jlo > 0 ? a.jlo - 1 : 0, khi = a.jhi - 1;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
-    if (sh.act[0]) {
+    if (a.jlo == 0 && sh.act[0]) {
       const double a0 = sh.a[0];
       double x[8], r[8], p[8], q[8], dv[8], acc = 0.0;
       ld8(a.x0 + d0, x); ld8(a.r0 + d0, r); ld8(a.p0 + d0, p); ld8(a.q0 + d0, q); ld8(a.dinv64 + d0, dv);
@@ -230,7 +245,7 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
     ld8(a.dinvp + d0, dp);
     double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool any = false;
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = klo; k < khi; ++k) {
       if (!sh.act[k + 1]) continue;
       any = true;
       const double ak = sh.a[k + 1];
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
     }
   }
   ColState* cs = a.cs;
-  vec_finish(sh, a.part, a.part_stride, a.counter, a.m, [cs](int j, double v) {
+  vec_finish(sh, a.part, a.part_stride, a.counter, a.jlo, a.jhi, [cs](int j, double v) {
     ColState c = cs[j];
     if (c.frozen) return;
     c.b = v / c.rho;
@@ -331,7 +346,8 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.D = c->D; a.Dp = c->Dp; a.K = K; a.m = K + 1; a.wpc = c->Dp / 32;
   a.beta = c->beta; a.precond = c->opt.precond;
   a.alpha = c->alpha; a.colsq = c->colsq; a.b0 = c->b0;
-  a.dinv64 = c->dinv64; a.dinvp = (TP*)c->dinvp;
+  a.dinv64 = c->dinv64; a.dinvp = (TP*)c->dinvp; a.alphap = (TP*)c->alphap;
+  a.jlo = 0; a.jhi = K + 1;
   a.x0 = c->x0; a.r0 = c->r0; a.p0 = c->p0; a.q0 = c->q0;
   a.R = (TP*)c->R; a.P = (TP*)c->P; a.Q = (TP*)c->Q;
   a.s = c->s; a.bits = c->bits;
@@ -401,6 +417,37 @@ static cofem_status validate_alpha(Ctx* c, const double* alpha_dev) {
 }
 
 // ------------------------------------------------------------------ E-step driver
+// U PCG iterations of the 1024 x 1024 DCT fast path: the fp64 mean column (its three
+// DCT passes and its update) runs on the side stream concurrently with the probe
+// columns on the main stream; the columns are independent (reading R3), so the two
+// chains only join at the end of the E-step.
+template <typename TP>
+static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned* counter, cudaStream_t st, int cls) {
+  VecArgs<TP> a = vec_args<TP>(c, K, invK);
+  a.jlo = jlo; a.jhi = jhi; a.counter = counter;
+  launch_begin(c, cls, st);
+  k_update<TP><<<c->vec_grid, VEC_THREADS, 0, st>>>(a);
+  launch_end(c, cls, st);
+}
+
+static cofem_status cg_loop_1k(Ctx* c, int K, double invK) {
+  const int m = K + 1;
+  CK(cudaEventRecord(c->ev_fork, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  for (int it = 0; it < c->opt.cg_iters; ++it) {
+    cofem_status st;
+    if ((st = dct1k_apply(c, 0, 1, it, it > 0, c->side)) != COFEM_OK) return st;
+    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->side, KC_MEAN);
+    if ((st = dct1k_apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
+    else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
+    if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
+  }
+  CK(cudaEventRecord(c->ev_join, c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return COFEM_OK;
+}
+
 // Runs Alg. 1 lines 3-7 with alpha already in c->alpha.  No host sync inside.
 static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offset, int K_total) {
   const int m = K + 1;
@@ -419,6 +466,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   else k_init<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
   launch_end(c, KC_INIT);
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
+  if (c->fast1k) return cg_loop_1k(c, K, invK);
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
     if (c->kind == COFEM_OP_DCT2_MASKED) {
@@ -490,12 +538,15 @@ static void free_all(Ctx* c) {
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
-                  c->ws1, c->ws2, c->ws1d, c->ws2d};
+                  c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
 }
 
 void cofem_destroy(cofem_ctx ctx) {
@@ -519,11 +570,15 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   CK(cudaGetDevice(&c->device));
   CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   CK(cudaEventCreate(&c->ev0)); CK(cudaEventCreate(&c->ev1));
+  CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
 
   const size_t tp = c->probe64 ? sizeof(double) : sizeof(float);
   const int64_t Dp = c->Dp;
   ALLOC(c->b0, Dp); ALLOC(c->colsq, Dp); ALLOC(c->alpha, Dp); ALLOC(c->dinv64, Dp);
   { char* p; ALLOC(p, Dp * tp); c->dinvp = p; }
+  { char* p; ALLOC(p, Dp * tp); c->alphap = p; }
   ALLOC(c->x0, Dp); ALLOC(c->r0, Dp); ALLOC(c->p0, Dp); ALLOC(c->q0, Dp); ALLOC(c->s, Dp);
   ALLOC(c->mu_out, Dp); ALLOC(c->s_out, Dp); ALLOC(c->alpha_out, Dp);
   { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->R = p; }
@@ -531,7 +586,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->Q = p; }
   ALLOC(c->bits, (size_t)c->Kcap * (Dp / 32));
   ALLOC(c->cs, c->m_cap);
-  ALLOC(c->counters, MAXM + 1);
+  ALLOC(c->counters, MAXM + 2);
   c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
   c->part_stride = std::max(c->vec_grid, 1);
 

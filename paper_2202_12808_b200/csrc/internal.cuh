@@ -22,7 +22,7 @@ enum KernelClass : int {
   KC_PROBES = 0, KC_INIT, KC_DIR, KC_UPDATE, KC_FINAL,
   KC_DENSE_PHI_P, KC_DENSE_PHIT_W,
   KC_DCT_ROWS_INV, KC_DCT_COLS, KC_DCT_ROWS_FWD,
-  KC_CONV_APPLY, KC_SETUP, KC_COUNT
+  KC_CONV_APPLY, KC_MEAN, KC_SETUP, KC_COUNT
 };
 
 // Per-column CG scalars (device).  Column 0 = mean system (R2).
@@ -52,6 +52,11 @@ struct Ctx {
   float* phi = nullptr; int64_t ld = 0; // DENSE device copy, row-major N x ld
   int rows = 0, cols = 0, conv = 0;     // DCT2
   uint8_t* mask_vvT = nullptr;          // DCT2: mask in v-order, transposed [cols][rows]
+  uint32_t* maskL = nullptr;            // DCT2 1024 fast path: lane-packed mask (op_dct1k.cu)
+  void* tab1k32 = nullptr; void* tab1k64 = nullptr;   // its twiddle tables (float / double)
+  bool fast1k = false;                  // DCT2 1024 x 1024: fast path, mean column on `side`
+  cudaStream_t side = nullptr;          // second stream (mean column of the fast DCT path)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu
   void* dct_tab64 = nullptr;            // (double)
   int ntaps = 0;                        // CIRCCONV
@@ -66,6 +71,7 @@ struct Ctx {
   double* alpha = nullptr;              // fp64 Dp
   double* dinv64 = nullptr;             // 1 / diag(A) fp64
   void* dinvp = nullptr;                // same in probe precision
+  void* alphap = nullptr;               // alpha in probe precision (probe-column applies)
   double *x0 = nullptr, *r0 = nullptr, *p0 = nullptr, *q0 = nullptr;  // mean column (fp64)
   void *R = nullptr, *P = nullptr, *Q = nullptr;                       // probe block [Kcap][Dp]
   double* s = nullptr;                  // accumulated (1/K) sum p_k o x_k  (fp64 Dp)
@@ -96,7 +102,7 @@ struct Ctx {
 
   // profiling
   uint32_t prof_mask = 0;
-  struct Rec { int cls; cudaEvent_t a, b; };
+  struct Rec { int cls; cudaEvent_t a, b; cudaStream_t st; };
   std::vector<Rec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[KC_COUNT] = {0};
@@ -106,8 +112,8 @@ struct Ctx {
 };
 
 // launch bookkeeping: call around every kernel launch
-void launch_begin(Ctx* c, int cls);
-void launch_end(Ctx* c, int cls);
+void launch_begin(Ctx* c, int cls, cudaStream_t st = nullptr);   // st = nullptr: the context stream
+void launch_end(Ctx* c, int cls, cudaStream_t st = nullptr);
 cudaError_t check_launch(Ctx* c, const char* what);
 
 // ---------------------------------------------------------------- device helpers
@@ -195,6 +201,10 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev);
 cofem_status dct_apply(Ctx* c, int m, int iter, bool dir);   // direction update fused into pass A
 cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host);
 cofem_status conv_apply(Ctx* c, int m, int iter);
+
+bool dct1k_eligible(const Ctx* c);
+cofem_status dct1k_setup(Ctx* c);
+cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
 
 // vector kernels (cofem.cu)
 cofem_status launch_dir(Ctx* c, int m);

@@ -252,3 +252,15 @@ def test_c5_full_size_vs_fft_closed_form():
     P = rademacher_probes(w.D, 4, 2, 0)
     emu, es, _ = cf.circconv_estep(w.taps, w.D, w.y, w.beta, 1.0, P)
     assert rel(mu, emu) <= 1e-4 and rel(s, es) <= 1e-4, (rel(mu, emu), rel(s, es))
+
+
+def test_c4_fast_path_em_two_iterations():
+    """The 1024 x 1024 fast path (op_dct1k.cu: warp-per-line FFTs, transposed
+    intermediates, concurrent fp64 mean column) through two EM iterations with the
+    direction update active, every element against the oracle."""
+    w = synth.preset("C4")
+    ctx = ctx_of(w, cg_iters=6, max_probes=3)
+    a, mu, s = gpu_em(ctx, w, 2, 3, 9)
+    oa, omu, os_ = cofem_em(op_of(w), w.y, w.beta, 2, 3, 9, 6)
+    assert rel(1 / a, 1 / oa) <= 1e-5 and rel(mu, omu) <= 1e-5 and rel(s, os_) <= 1e-4, \
+        (rel(1 / a, 1 / oa), rel(mu, omu), rel(s, os_))
