@@ -432,12 +432,14 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
 
 static cofem_status cg_loop_1k(Ctx* c, int K, double invK) {
   const int m = K + 1;
+  static const bool serial = getenv("COFEM_1K_SERIAL") != nullptr;   // tuning hook: mean column on the main stream
+  cudaStream_t ms = serial ? c->stream : c->side;
   CK(cudaEventRecord(c->ev_fork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
-    if ((st = dct1k_apply(c, 0, 1, it, it > 0, c->side)) != COFEM_OK) return st;
-    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->side, KC_MEAN);
+    if ((st = dct1k_apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
+    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
     if ((st = dct1k_apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
     if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
@@ -586,7 +588,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->Q = p; }
   ALLOC(c->bits, (size_t)c->Kcap * (Dp / 32));
   ALLOC(c->cs, c->m_cap);
-  ALLOC(c->counters, MAXM + 2);
+  ALLOC(c->counters, MAXM + 4);   // [0, MAXM): per column; MAXM..: per-launch tickets
   c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
   c->part_stride = std::max(c->vec_grid, 1);
 

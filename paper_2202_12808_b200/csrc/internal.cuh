@@ -177,6 +177,25 @@ __device__ __forceinline__ void column_finish(double v, int j, double* part, int
   }
 }
 
+// As column_finish, for persistent kernels: CTA work item `slot` of `count` per column.
+template <typename Fin>
+__device__ __forceinline__ void column_finish_n(double v, int j, int slot, int count, double* part, int stride,
+                                                unsigned* counters, Fin fin) {
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    part[(int64_t)j * stride + slot] = v;
+    __threadfence();
+    s_last = (atomicAdd(counters + j, 1u) == (unsigned)count - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double tot = reduce_partials(part + (int64_t)j * stride, count);
+    if (threadIdx.x == 0) { fin(tot); counters[j] = 0u; }
+  }
+}
+
 // CTA-wide sum of one double per thread (result valid in thread 0). blockDim.x <= 1024.
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double s_w[32];

@@ -21,8 +21,10 @@
 // Probe columns run in fp32 (8 rows per CTA); the fp64 mean column (4 rows per
 // CTA) runs on a second stream concurrently (cofem.cu).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
+#include <complex>
 #include <vector>
 
 #include "fft_common.cuh"
@@ -31,24 +33,28 @@ namespace cofem {
 namespace d1k {
 
 constexpr int L = 1024, M = 512;
-constexpr int XS1 = 68, XS2 = 72;      // exchange row strides: pads 4 and 8 words (conflict-free)
-constexpr int XPL = 8 * XS2;           // elements per plane of the exchange buffer
-constexpr int WREG = 2 * XPL;          // per-warp smem region (elements of T): exchange planes / one tile row (>= L)
+constexpr int XS1 = 66, XS2 = 72;      // exchange row strides in complex entries (conflict-free 8-byte accesses)
+constexpr int WREG = 2 * 8 * XS2;      // per-warp smem region (elements of T): exchange buffer / one tile row (>= L)
 template <typename T> struct Geo { static constexpr int RT = sizeof(T) == 8 ? 4 : 8; };   // rows (warps) per CTA
 
-// Twiddle tables, host-built in fp64 and rounded to T, copied to shared memory by every CTA
-// in layouts that make each warp access conflict-free (lanes read consecutive entries):
-//   w2[r*8 + k]  = W_64^{r k}      (stage 2, k = lane & 7)
-//   w3[r*64 + j] = W_512^{r j}     (stage 3, j = butterfly)
-//   tq[k] = exp(-i pi k / 2L) (k < L),  th[k] = exp(-2 pi i k / L) (k < M)   (Makhoul pre/post)
-constexpr int TW2 = 0, TW3 = 64, TTQ = TW3 + 512, TTH = TTQ + L, TTOT = TTH + M;   // offsets in complex entries
-template <typename T> struct Tw { const cplx<T>* w2; const cplx<T>* w3; const cplx<T>* tq; const cplx<T>* th; };
+// Tables, host-built in fp64 and rounded to T, copied to shared memory by every CTA in
+// layouts where each warp access is conflict-free (lanes read consecutive entries):
+//   w2[r*8 + k]  = W_64^{r k}      (FFT stage 2, k = lane & 7)
+//   w3[r*64 + j] = W_512^{r j}     (FFT stage 3, j = butterfly)
+//   DCT-III pre  (Makhoul):  W[k] = u1 P_k + u2 Q_k,  u1 = X[k] - i X[L-k], u2 = X[k+M] - i X[M-k]
+//   DCT-II  post:            X[k]   = Re(W_k R1_k) + Re(conj(W_{M-k}) R2_k)
+//                            X[k+M] = Re(W_k R3_k) + Re(conj(W_{M-k}) R4_k)
+// with the orthonormal scales, the 1/M of the inverse FFT and the even/odd split folded in
+// (k < M; the entries are derived in build_tables below).
+constexpr int TW2 = 0, TW3 = 64, TP = TW3 + 512, TQ = TP + M, TR1 = TQ + M, TR2 = TR1 + M, TR3 = TR2 + M,
+              TR4 = TR3 + M, TTOT = TR4 + M;   // offsets in complex entries
+template <typename T> struct Tw { const cplx<T>* base; };
 
 template <typename T>
 __device__ __forceinline__ Tw<T> load_tables(const cplx<T>* __restrict__ g, cplx<T>* sm) {
   for (int i = threadIdx.x; i < TTOT; i += blockDim.x) sm[i] = g[i];
   __syncthreads();
-  return {sm + TW2, sm + TW3, sm + TTQ, sm + TTH};
+  return {sm};
 }
 
 template <typename T, int SIGN>
@@ -57,84 +63,62 @@ __device__ __forceinline__ void twid(cplx<T>& v, cplx<T> w) { v = SIGN < 0 ? cmu
 // 512-point DFT (SIGN -1) / unnormalised inverse (SIGN +1) by one warp.
 // In:  va[r] = x[ja + 64 r], vb[r] = x[jb + 64 r].  Out: va[r] = X[ja + 64 r], vb[r] = X[jb + 64 r].
 // Stockham radix-8: stage s reads x[j + 64 r], twiddles by W_{8 Ns}^{r (j mod Ns)}, DFT8,
-// writes y[(j / Ns) 8 Ns + (j mod Ns) + r Ns]; Ns = 1, 8, 64.  Exchanges store [r][j].
+// writes y[(j / Ns) 8 Ns + (j mod Ns) + r Ns]; Ns = 1, 8, 64.  Exchanges store [r][j]
+// (complex entries, row strides XS1 / XS2).
 template <typename T, int SIGN>
-__device__ __forceinline__ void fft512(cplx<T> (&va)[8], cplx<T> (&vb)[8], int lane, T* __restrict__ re,
-                                       T* __restrict__ im, const Tw<T>& tw) {
+__device__ __forceinline__ void fft512(cplx<T> (&va)[8], cplx<T> (&vb)[8], int lane, cplx<T>* __restrict__ x,
+                                       const Tw<T>& tw) {
   const int ja = lane, jb = lane ? 64 - lane : 32;
   dft8<SIGN>(va); dft8<SIGN>(vb);                       // stage 1 (Ns = 1): butterflies ja, jb
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    re[r * XS1 + ja] = va[r].x; im[r * XS1 + ja] = va[r].y;
-    re[r * XS1 + jb] = vb[r].x; im[r * XS1 + jb] = vb[r].y;
-  }
+  for (int r = 0; r < 8; ++r) { x[r * XS1 + ja] = va[r]; x[r * XS1 + jb] = vb[r]; }
   __syncwarp();
   {   // stage 2 (Ns = 8): butterflies lane, lane + 32; y[i] lives at [(i & 7)][i >> 3]
     const int base = (lane & 7) * XS1 + (lane >> 3);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      va[r] = {re[base + 8 * r], im[base + 8 * r]};
-      vb[r] = {re[base + 4 + 8 * r], im[base + 4 + 8 * r]};
-    }
-    const int k = lane & 7;
+    for (int r = 0; r < 8; ++r) { va[r] = x[base + 8 * r]; vb[r] = x[base + 4 + 8 * r]; }
+    const cplx<T>* w2 = tw.base + TW2 + (lane & 7);
 #pragma unroll
     for (int r = 1; r < 8; ++r) {
-      const cplx<T> w = tw.w2[r * 8 + k];
+      const cplx<T> w = w2[r * 8];
       twid<T, SIGN>(va[r], w); twid<T, SIGN>(vb[r], w);
     }
   }
   dft8<SIGN>(va); dft8<SIGN>(vb);
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    re[r * XS2 + lane] = va[r].x; im[r * XS2 + lane] = va[r].y;
-    re[r * XS2 + lane + 32] = vb[r].x; im[r * XS2 + lane + 32] = vb[r].y;
-  }
+  for (int r = 0; r < 8; ++r) { x[r * XS2 + lane] = va[r]; x[r * XS2 + lane + 32] = vb[r]; }
   __syncwarp();
   {   // stage 3 (Ns = 64): butterflies ja, jb; y'[i] written by j2 = 8 (i >> 6) + (i & 7), r2 = (i >> 3) & 7
     const int ba = (ja >> 3) * XS2 + (ja & 7), bb = (jb >> 3) * XS2 + (jb & 7);
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      va[r] = {re[ba + 8 * r], im[ba + 8 * r]};
-      vb[r] = {re[bb + 8 * r], im[bb + 8 * r]};
-    }
+    for (int r = 0; r < 8; ++r) { va[r] = x[ba + 8 * r]; vb[r] = x[bb + 8 * r]; }
+    const cplx<T>* w3 = tw.base + TW3;
 #pragma unroll
     for (int r = 1; r < 8; ++r) {
-      twid<T, SIGN>(va[r], tw.w3[r * 64 + ja]);
-      twid<T, SIGN>(vb[r], tw.w3[r * 64 + jb]);
+      twid<T, SIGN>(va[r], w3[r * 64 + ja]);
+      twid<T, SIGN>(vb[r], w3[r * 64 + jb]);
     }
   }
   dft8<SIGN>(va); dft8<SIGN>(vb);
   __syncwarp();                                         // exchange region free again
 }
 
-// DCT-III (orthonormal inverse) pre-processing for one k (Makhoul): packed spectrum W[k]
-// from X[k], X[L-k], X[k+M], X[M-k]; the 1/M IFFT normalisation and 1/s_k are folded in.
+// DCT-III (orthonormal inverse) pre-processing for one k: W[k] = u1 P_k + u2 Q_k.
 template <typename T>
 __device__ __forceinline__ cplx<T> dct3_pre(int k, T Xk, T XLk, T XkM, T XMk, const Tw<T>& tb) {
-  const T sc0 = (T)0.0625, sc = (T)0.044194173824159216;   // sqrt(L)/M, sqrt(L/2)/M
-  const T xk = Xk * (k == 0 ? sc0 : sc);
-  const T xLk = k == 0 ? (T)0 : XLk * sc;
-  const T xkM = XkM * sc, xMk = XMk * sc;
-  const cplx<T> V1 = cmulc(cplx<T>{xk, -xLk}, tb.tq[k]);
-  const cplx<T> V2 = cmulc(cplx<T>{xkM, -xMk}, tb.tq[k + M]);
-  const cplx<T> Ve = {(V1.x + V2.x) * (T)0.5, (V1.y + V2.y) * (T)0.5};
-  const cplx<T> Vo = cmulc(cplx<T>{(V1.x - V2.x) * (T)0.5, (V1.y - V2.y) * (T)0.5}, tb.th[k]);
-  return {Ve.x - Vo.y, Ve.y + Vo.x};
+  const cplx<T> P = tb.base[TP + k], Q = tb.base[TQ + k];
+  // (Xk - i XLk) P + (XkM - i XMk) Q
+  return {Xk * P.x + XLk * P.y + XkM * Q.x + XMk * Q.y, Xk * P.y - XLk * P.x + XkM * Q.y - XMk * Q.x};
 }
 
 // DCT-II post-processing for one k from W[k], W[(M-k) mod M]: orthonormal X[k], X[k+M].
 template <typename T>
 __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const Tw<T>& tb, T& lo, T& hi) {
-  const T s0 = (T)0.03125, s = (T)0.044194173824159216;    // sqrt(1/L), sqrt(2/L)
-  const cplx<T> Ve = {(Wk.x + Wm.x) * (T)0.5, (Wk.y - Wm.y) * (T)0.5};
-  const cplx<T> Vo = {(Wk.y + Wm.y) * (T)0.5, (Wm.x - Wk.x) * (T)0.5};
-  const cplx<T> tt = cmul(tb.th[k], Vo);
-  const cplx<T> V1 = cadd(Ve, tt), V2 = csub(Ve, tt);
-  const cplx<T> q1 = tb.tq[k], q2 = tb.tq[k + M];
-  lo = (q1.x * V1.x - q1.y * V1.y) * (k == 0 ? s0 : s);
-  hi = (q2.x * V2.x - q2.y * V2.y) * s;
+  const cplx<T> R1 = tb.base[TR1 + k], R2 = tb.base[TR2 + k], R3 = tb.base[TR3 + k], R4 = tb.base[TR4 + k];
+  lo = Wk.x * R1.x - Wk.y * R1.y + Wm.x * R2.x + Wm.y * R2.y;
+  hi = Wk.x * R3.x - Wk.y * R3.y + Wm.x * R4.x + Wm.y * R4.y;
 }
 
 // Canonical positions of a lane in a line: slot A r -> ja + 64r, B -> jb + 64r,
@@ -212,17 +196,51 @@ template <typename T> __device__ __forceinline__ const cplx<T>* tab1k(const DctA
 
 // ---------------------------------------------------------------- pass A
 // Shared memory: [RT warps][WREG] (FFT exchange / output tile row) then the twiddle tables.
+// Persistent kernels: work item w = (column j0 + w / NTILE, tile w % NTILE), grid-strided.
+template <typename T> struct Work { static constexpr int NTILE = L / Geo<T>::RT; };
+
+// Per-launch column info, read once per CTA: frozen flags and direction coefficients b_j
+// (R5; a6), plus per-warp gamma accumulators for pass C (reduced once per CTA at exit).
+struct ColInfo {
+  int frozen[MAXM];
+  double b[MAXM];
+  double g[8][MAXM];
+};
+__device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, int j0, int ncols, bool zero_g) {
+  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
+    const ColState c = cs[j0 + jj];
+    ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
+    if (zero_g)
+      for (int w = 0; w < 8; ++w) ci.g[w][jj] = 0.0;
+  }
+}
+
 template <typename T>
-__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j0, int dir) {
-  constexpr int RT = Geo<T>::RT;
+__device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile, int dir, double bcoef, T* sm,
+                                              const Tw<T>& tb);
+
+template <typename T>
+__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j0, int ncols, int dir) {
+  constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int j = j0 + blockIdx.y;
-  const ColState st = a.cs[j];
-  if (st.frozen) return;
   T* sm = reinterpret_cast<T*>(smraw);
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));
+  __shared__ ColInfo ci;
+  load_colinfo(ci, a.cs, j0, ncols, false);
+  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
+    const int jj = w / NT;
+    if (ci.frozen[jj]) continue;
+    rows_inv_item<T>(a, j0 + jj, w % NT, dir, ci.b[jj], sm, tb);
+    __syncthreads();                 // smem tile reuse
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile, int dir, double bcoef, T* sm,
+                                              const Tw<T>& tb) {
+  constexpr int RT = Geo<T>::RT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * RT;
+  const int row0 = tile * RT;
   const DctCol<T> c = col_of<T>(a, j);
   const int64_t rb = (int64_t)(row0 + warp) * L;
   T A[8], B[8], C[8], E[8];
@@ -230,7 +248,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
     T* __restrict__ pr = c.p + rb;
     const T* __restrict__ rr = c.r + rb;
     const T* __restrict__ dv = c.dinv + rb;
-    const T bb = (T)st.b;
+    const T bb = (T)bcoef;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       int o[4];
@@ -258,7 +276,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
   cplx<T> va[8], vb[8];
   pre_all<T>(lane, A, B, C, E, va, vb, tb);
   T* reg = sm + warp * WREG;
-  fft512<T, +1>(va, vb, lane, reg, reg + XPL, tb);
+  fft512<T, +1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   const int ja = lane, jb = lane ? 64 - lane : 32;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {     // packed v-order output w[n] = v[2n] + i v[2n+1]
@@ -279,17 +297,30 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
 
 // ---------------------------------------------------------------- pass B
 template <typename T>
-__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0) {
-  constexpr int RT = Geo<T>::RT;
+__device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
+
+template <typename T>
+__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, int ncols) {
+  constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int j = j0 + blockIdx.y;
-  if (a.cs[j].frozen) return;
   T* sm = reinterpret_cast<T*>(smraw);
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));
+  __shared__ ColInfo ci;
+  load_colinfo(ci, a.cs, j0, ncols, false);
+  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
+    const int jj = w / NT;
+    if (ci.frozen[jj]) continue;
+    cols_item<T>(a, j0 + jj, w % NT, sm, tb);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb) {
+  constexpr int RT = Geo<T>::RT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int line = blockIdx.x * RT + warp;          // v-order image column cv
+  const int line = tile * RT + warp;                // v-order image column cv
   const DctCol<T> c = col_of<T>(a, j);
-  T* __restrict__ ln = c.t1 + (int64_t)line * L;
+  const T* __restrict__ ln = c.t1 + (int64_t)line * L;
   const uint32_t mb = a.maskL[line * 32 + lane];    // bits (2r, 2r+1): slot a; (16+2r, 17+2r): slot b
   T A[8], B[8], C[8], E[8];
 #pragma unroll
@@ -301,7 +332,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0) {
   cplx<T> va[8], vb[8];
   pre_all<T>(lane, A, B, C, E, va, vb, tb);
   T* reg = sm + warp * WREG;
-  fft512<T, +1>(va, vb, lane, reg, reg + XPL, tb);
+  fft512<T, +1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     if (!((mb >> (2 * r)) & 1u)) va[r].x = (T)0;
@@ -309,51 +340,90 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0) {
     if (!((mb >> (16 + 2 * r)) & 1u)) vb[r].x = (T)0;
     if (!((mb >> (17 + 2 * r)) & 1u)) vb[r].y = (T)0;
   }
-  fft512<T, -1>(va, vb, lane, reg, reg + XPL, tb);
+  fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   post_all<T>(lane, va, vb, A, B, C, E, tb);
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < 8; ++r) {     // natural-order column values -> tile row (the exchange region is free)
     int o[4];
     canon(lane, r, o);
-    ln[o[0]] = A[r]; ln[o[1]] = B[r]; ln[o[2]] = C[r]; ln[o[3]] = E[r];
+    reg[o[0]] = A[r]; reg[o[1]] = B[r]; reg[o[2]] = C[r]; reg[o[3]] = E[r];
   }
+  __syncthreads();
+  T* __restrict__ out = c.t2;       // T2[row][cv] row-major: 32-byte segments of RT v-order columns
+#pragma unroll
+  for (int it = 0; it < L / (RT * 32); ++it) {
+    const int row = it * RT * 32 + threadIdx.x;
+    T v[RT];
+#pragma unroll
+    for (int i = 0; i < RT; ++i) v[i] = sm[i * WREG + row];
+    st32B<T, RT>(out + (int64_t)row * L + tile * RT, v);
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------- pass C
 template <typename T>
-__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j0) {
-  constexpr int RT = Geo<T>::RT;
+__device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
+
+template <typename T>
+__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j0, int ncols) {
+  constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int j = j0 + blockIdx.y;
-  if (a.cs[j].frozen) return;
   T* sm = reinterpret_cast<T*>(smraw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * RT;
-  const DctCol<T> c = col_of<T>(a, j);
-  {
-    const T* __restrict__ tin = c.t1;
-    T v[L / (RT * 32)][RT];
-#pragma unroll
-    for (int it = 0; it < L / (RT * 32); ++it)
-      ld32B<T, RT>(tin + (int64_t)(it * RT * 32 + threadIdx.x) * L + row0, v[it]);
-#pragma unroll
-    for (int it = 0; it < L / (RT * 32); ++it)
-#pragma unroll
-      for (int i = 0; i < RT; ++i) sm[i * WREG + it * RT * 32 + threadIdx.x] = v[it][i];
-  }
+  __shared__ ColInfo ci;
+  load_colinfo(ci, a.cs, j0, ncols, true);
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  const int warp = threadIdx.x >> 5;
+  for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
+    const int jj = w / NT;
+    if (ci.frozen[jj]) continue;
+    const double gw = rows_fwd_item<T>(a, j0 + jj, w % NT, sm, tb);   // warp-reduced, valid in lane 0
+    if ((threadIdx.x & 31) == 0) ci.g[warp][jj] += gw;
+  }
+  // a4: gamma_j = p_j^T q_j.  CTA partials (fixed warp order) -> part[j][cta]; the last CTA
+  // reduces all columns in fixed order and applies the freeze rule / step length (R5).
+  __syncthreads();
+  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < RT; ++ww) v += ci.g[ww][jj];
+    a.part[(int64_t)(j0 + jj) * a.stride + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(a.counters + MAXM + 2 + (j0 == 0 ? 1 : 0), 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int jj = warp; jj < ncols; jj += RT) {
+    const int j = j0 + jj;
+    const double tot = reduce_partials(a.part + (int64_t)j * a.stride, gridDim.x);
+    if ((threadIdx.x & 31) == 0 && !ci.frozen[jj]) {
+      ColState cc = a.cs[j]; finish_gamma(cc, tot, a.iter); a.cs[j] = cc;
+    }
+  }
+  if (threadIdx.x == 0) a.counters[MAXM + 2 + (j0 == 0 ? 1 : 0)] = 0u;
+}
+
+template <typename T>
+__device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb) {
+  constexpr int RT = Geo<T>::RT;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = tile * RT;
+  const DctCol<T> c = col_of<T>(a, j);
+  const int64_t rb = (int64_t)(row0 + warp) * L;
   T* reg = sm + warp * WREG;
   const int ja = lane, jb = lane ? 64 - lane : 32;
   cplx<T> va[8], vb[8];
+  {
+    const cplx<T>* __restrict__ rowc = reinterpret_cast<const cplx<T>*>(c.t2 + rb);   // packed v-order z[n]
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    va[r] = *reinterpret_cast<const cplx<T>*>(reg + 2 * (ja + 64 * r));
-    vb[r] = *reinterpret_cast<const cplx<T>*>(reg + 2 * (jb + 64 * r));
+    for (int r = 0; r < 8; ++r) { va[r] = rowc[ja + 64 * r]; vb[r] = rowc[jb + 64 * r]; }
   }
-  fft512<T, -1>(va, vb, lane, reg, reg + XPL, tb);
+  fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   T A[8], B[8], C[8], E[8];
   post_all<T>(lane, va, vb, A, B, C, E, tb);
-  const int64_t rb = (int64_t)(row0 + warp) * L;
   const T* __restrict__ pp = c.p + rb;
   const T* __restrict__ al = alpha_of<T>(a, j) + rb;
   T* __restrict__ qq = c.q + rb;
@@ -377,12 +447,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
     canon(lane, r, o);
     qq[o[0]] = A[r]; qq[o[1]] = B[r]; qq[o[2]] = C[r]; qq[o[3]] = E[r];
   }
-  g = block_sum(g);
-  ColState* cs = a.cs;
-  const int iter = a.iter;
-  column_finish(g, j, a.part, a.stride, a.counters, [cs, j, iter](double tot) {
-    ColState cc = cs[j]; finish_gamma(cc, tot, iter); cs[j] = cc;
-  });
+  return warp_sum(g);
 }
 
 // ---------------------------------------------------------------- setup: lane-packed mask
@@ -420,17 +485,37 @@ template <typename T> static void set_attrs() {
 
 bool dct1k_eligible(const Ctx* c) { return c->kind == COFEM_OP_DCT2_MASKED && c->rows == 1024 && c->cols == 1024; }
 
+// Derivation (Makhoul, orthonormal): with q1 = e^{-i pi k/2L}, q2 = e^{-i pi (k+M)/2L},
+// h = e^{-2 pi i k/L}, the DCT-III spectrum is W = [V1 + V2]/2 + i conj(h) [V1 - V2]/2 with
+// V1 = sc_k u1 conj(q1), V2 = sc u2 conj(q2), so P = sc_k conj(q1)(1 + i conj h)/2,
+// Q = sc conj(q2)(1 - i conj h)/2 (sc = sqrt(L/2)/M, sc_0 = sqrt(L)/M).  The DCT-II outputs
+// X[k] = s_k Re(q1 V1'), X[k+M] = s Re(q2 V2'), V1' = W_k (1 - i h)/2 + conj(W_m)(1 + i h)/2,
+// V2' = W_k (1 + i h)/2 + conj(W_m)(1 - i h)/2, so R1 = s_k q1 (1 - i h)/2, R2 = s_k q1 (1 + i h)/2,
+// R3 = s q2 (1 + i h)/2, R4 = s q2 (1 - i h)/2 (s = sqrt(2/L), s_0 = sqrt(1/L)); the device
+// evaluates Re(conj(w) b) as w.x b.x + w.y b.y.
 template <typename T> static std::vector<cplx<T>> build_tables() {
   using namespace d1k;
+  typedef std::complex<double> C;
   const double PI = 3.14159265358979323846;
   std::vector<cplx<T>> h(TTOT);
-  auto e = [&](double ang) { return cplx<T>{(T)cos(ang), (T)sin(ang)}; };
+  auto put = [&](int i, C z) { h[i] = cplx<T>{(T)z.real(), (T)z.imag()}; };
+  auto e = [](double ang) { return C(cos(ang), sin(ang)); };
   for (int r = 0; r < 8; ++r)
-    for (int k = 0; k < 8; ++k) h[TW2 + r * 8 + k] = e(-2 * PI * r * k / 64.0);
+    for (int k = 0; k < 8; ++k) put(TW2 + r * 8 + k, e(-2 * PI * r * k / 64.0));
   for (int r = 0; r < 8; ++r)
-    for (int jj = 0; jj < 64; ++jj) h[TW3 + r * 64 + jj] = e(-2 * PI * r * jj / 512.0);
-  for (int k = 0; k < L; ++k) h[TTQ + k] = e(-PI * k / (2.0 * L));
-  for (int k = 0; k < M; ++k) h[TTH + k] = e(-2 * PI * k / L);
+    for (int jj = 0; jj < 64; ++jj) put(TW3 + r * 64 + jj, e(-2 * PI * r * jj / 512.0));
+  const C I(0, 1);
+  const double sc = sqrt(L / 2.0) / M, sc0 = sqrt((double)L) / M, s = sqrt(2.0 / L), s0 = sqrt(1.0 / L);
+  for (int k = 0; k < M; ++k) {
+    const C q1 = e(-PI * k / (2.0 * L)), q2 = e(-PI * (k + M) / (2.0 * L)), hh = e(-2 * PI * k / L);
+    const double sck = k == 0 ? sc0 : sc, sk = k == 0 ? s0 : s;
+    put(TP + k, sck * std::conj(q1) * (1.0 + I * std::conj(hh)) / 2.0);
+    put(TQ + k, sc * std::conj(q2) * (1.0 - I * std::conj(hh)) / 2.0);
+    const C r1 = sk * q1 * (1.0 - I * hh) / 2.0, r2 = sk * q1 * (1.0 + I * hh) / 2.0;
+    const C r3 = s * q2 * (1.0 + I * hh) / 2.0, r4 = s * q2 * (1.0 - I * hh) / 2.0;
+    // lo = Re(Wk r1) + Re(conj(Wm) r2) = Wk.x r1.x - Wk.y r1.y + Wm.x r2.x + Wm.y r2.y
+    put(TR1 + k, r1); put(TR2 + k, r2); put(TR3 + k, r3); put(TR4 + k, r4);
+  }
   return h;
 }
 
@@ -450,7 +535,7 @@ cofem_status dct1k_setup(Ctx* c) {
   launch_end(c, KC_SETUP);
   set_attrs<float>();
   set_attrs<double>();
-  c->part_stride = std::max(c->part_stride, L / Geo<double>::RT);
+  c->part_stride = std::max(c->part_stride, std::max(L / Geo<double>::RT, c->num_sms * 8));   // >= persistent grids
   return check_launch(c, "dct1k setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
@@ -462,17 +547,28 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   using namespace d1k;
   DctArgs a = dct_args(c, j1, iter);
   constexpr int RT = Geo<T>::RT;
-  const dim3 g(L / RT, j1 - j0), blk(RT * 32);
+  const int ncols = j1 - j0;
   const size_t sm = smem_bytes<T>();
+  // persistent grids at full occupancy (measured best: tools/sweep_slots.sh)
+  static const int slots_env = getenv("COFEM_1K_SLOTS") ? atoi(getenv("COFEM_1K_SLOTS")) : -1;   // tuning hook
+  auto grid_of = [&](const void* fn) {
+    const int items = ncols * Work<T>::NTILE;
+    if (slots_env == 0) return items;                  // one CTA per work item
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, RT * 32, sm);
+    const int per_sm = slots_env > 0 ? std::min(slots_env, occ) : occ;
+    return std::min(std::min(c->num_sms * per_sm, items), c->part_stride);
+  };
+  const dim3 blk(RT * 32);
   const bool mean = j0 == 0;        // the fp64 mean column is timed as its own class
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
-  k1k_rows_inv<T><<<g, blk, sm, st>>>(a, j0, dir ? 1 : 0);
+  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>), blk, sm, st>>>(a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_COLS, st);
-  k1k_cols<T><<<g, blk, sm, st>>>(a, j0);
+  k1k_cols<T><<<grid_of((const void*)k1k_cols<T>), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_COLS, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
-  k1k_rows_fwd<T><<<g, blk, sm, st>>>(a, j0);
+  k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
   return check_launch(c, "dct1k apply") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
