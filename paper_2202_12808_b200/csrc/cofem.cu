@@ -537,6 +537,7 @@ const char* cofem_kernel_class_name(int32_t cls) {
 const char* cofem_last_error(cofem_ctx ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 
 static void free_all(Ctx* c) {
+  dense_tc_free(c);
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,

@@ -89,6 +89,7 @@ struct Ctx {
   void* ws1 = nullptr; void* ws2 = nullptr;   // probe-precision scratch (dense W partials / DCT T1,T2)
   double* ws1d = nullptr; double* ws2d = nullptr;   // mean-column scratch
   int dense_splits = 1;
+  void* dense_tc = nullptr;             // tensor-core dense path state (op_dense_tc.cu), NULL: SIMT
 
   // host mirrors for the report
   std::vector<ColState> cs_host;
@@ -216,6 +217,9 @@ __device__ __forceinline__ double block_sum(double v) {
 // every apply computes Q = A P for all active columns and finishes gamma_j / a_j.
 cofem_status dense_setup(Ctx* c, const float* y_dev);
 cofem_status dense_apply(Ctx* c, int m, int iter);
+cofem_status dense_tc_setup(Ctx* c);
+cofem_status dense_tc_apply(Ctx* c, int m, int iter);
+void dense_tc_free(Ctx* c);
 cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev);
 cofem_status dct_apply(Ctx* c, int m, int iter, bool dir);   // direction update fused into pass A
 cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host);

@@ -243,7 +243,7 @@ cofem_status dense_setup(Ctx* c, const float* y_dev) {
     cudaFuncSetAttribute(k_dense_phiP<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     cudaFuncSetAttribute(k_dense_phiTW<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   }
-  return COFEM_OK;
+  return dense_tc_setup(c);
 }
 
 template <typename TP>
@@ -277,6 +277,7 @@ static cofem_status dense_apply_t(Ctx* c, int m, int iter) {
 }
 
 cofem_status dense_apply(Ctx* c, int m, int iter) {
+  if (c->dense_tc) return dense_tc_apply(c, m, iter);     // tcgen05 3xTF32 path (op_dense_tc.cu)
   return c->probe64 ? dense_apply_t<double>(c, m, iter) : dense_apply_t<float>(c, m, iter);
 }
 

@@ -1,0 +1,587 @@
+// op_dense_tc.cu — dense Gram apply on the 5th-generation tensor cores (sm_100a):
+//   W = Phi P            (N x K probes; split-K over D)          k_tc_phiP
+//   Q = beta Phi^T W + alpha o P,  gamma_j = p_j^T q_j           k_tc_phiTW
+// (Eq. 7; batched "matrix-matrix" CG apply, §3.2; BASELINE north_star:
+// "tcgen05/TMA tiles with a 3xTF32 split").
+//
+// 3xTF32: every fp32 operand x is split into hi = x with its 13 low mantissa bits cleared
+// (exactly a tf32 value) and lo = x - hi (exact in fp32), and C = A_hi B_hi + A_hi B_lo +
+// A_lo B_hi on kind::tf32 MMAs with fp32 accumulation in TMEM; the dropped A_lo B_lo term is
+// <= 2^-22 |A||B| per product (DESIGN.md §7 error budget).
+//
+// Per CTA (one 128-row output tile; 6 warps):
+//   warp 0      TMA producer: Phi tile (16 KB) + B_hi, B_lo tiles (K-major, SWIZZLE_128B) per
+//               32-wide K step into a STAGES-deep shared-memory ring (mbarrier complete_tx)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM, B from smem)
+//   warps 2-5   "splitters": each thread owns one output row m; per K step it reads its row
+//               of the Phi tile from shared memory (this is where Phi^T's transposition
+//               happens for k_tc_phiTW: the tile is MN-major in smem, the row is gathered
+//               across the swizzled 128-B lines), writes A_hi / A_lo into TMEM
+//               (tcgen05.st, double-buffered), and accumulates the fp64 mean column
+//               (column 0 of B = [b0 | p_1..p_K], reading R2; fp64 per DESIGN.md R10)
+//               in a register with DFMA; after the last step they are the epilogue
+//               (tcgen05.ld of the fp32 accumulator -> q, gamma partials / W partials).
+// The probe B operand's hi/lo split is done once per apply in global memory (B is
+// O((N + D) K), Phi is O(N D)).  Only the probe columns use the tensor cores; parity
+// mode (fp64 probes) keeps the SIMT path (op_dense.cu).
+#include <cuda.h>
+#include <stdio.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace cofem {
+namespace tc {
+
+constexpr int BM = 128, BK = 32, NSPLIT = 8, THREADS = 64 + 32 * NSPLIT;   // warps 0-1 + 8 splitter warps
+constexpr int TMEM_COLS = 256;             // [0, BN) accumulator; [128, 256) two A buffers (hi 32 | lo 32)
+constexpr int TM_A = 128;
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+// Bounded wait: a protocol error traps (reported as a CUDA error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  for (long long spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1ll << 28)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem], kind::tf32, M = 128, cta_group::1
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)) : "memory");
+}
+
+// 32 consecutive 32-bit TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+        "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, 128-byte swizzle (the layout TMA writes for a
+// box whose inner dimension is 128 B): rows of 128 B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address >> 4
+  d |= (uint64_t)1 << 16;                          // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor: kind::tf32, fp32 accumulate, A and B K-major, M = 128, N = bn.
+__host__ __device__ constexpr uint32_t idesc_tf32(int bn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) { return __int_as_float(__float_as_int(x) & 0xFFFFE000); }
+
+// Shared-memory plan (dynamic, 1024-aligned):
+// STAGES x [A 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64]
+struct Plan {
+  int bn, stages, stage_bytes;
+  __host__ __device__ int a_off(int s) const { return s * stage_bytes; }
+  __host__ __device__ int bhi_off(int s) const { return s * stage_bytes + BM * BK * 4; }
+  __host__ __device__ int blo_off(int s) const { return s * stage_bytes + BM * BK * 4 + bn * 128; }
+  __host__ __device__ int w_off(int s) const { return s * stage_bytes + BM * BK * 4 + 2 * bn * 128; }
+};
+
+struct Bars {
+  uint64_t full[8], empty[8], split_done[2], tfree[2], acc_full;
+  uint32_t tmem_base;
+  double red[NSPLIT][MAXM]; // epilogue per-warp column partials
+  double mean[NSPLIT][32];  // mean-column partials of the two halves of each row
+  int last;
+};
+
+// ---------------------------------------------------------------- the shared mainloop
+// MN = true: the A tile is Phi[n0 : n0+32][d0 : d0+128] stored as four MN-major 32x32 boxes
+// (k_tc_phiTW, A = Phi^T); false: Phi[n0 : n0+128][d0 : d0+32] K-major (k_tc_phiP, A = Phi).
+// mean_w: the fp64 mean-column operand along K (w0 for phiTW, p0 for phiP); returns the
+// thread's fp64 mean-column accumulator (row m = its splitter index).
+template <bool MN>
+__device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mBh,
+                           const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
+                           int ktot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tmem = bs.tmem_base;
+  double acc0 = 0.0;
+  if (warp == 0) {
+    if (lane == 0) {                                  // ---- TMA producer
+      const uint32_t bytes = BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kt = 0; kt < nk; ++kt) {
+        if (kt >= pl.stages) mbar_wait(&bs.empty[s], ph ^ 1);
+        mbar_expect_tx(&bs.full[s], bytes);
+        const int kc = k0 + kt * BK;
+        unsigned char* a = sm + pl.a_off(s);
+        if (MN) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) tma_load_2d(a + i * 4096, mA, &bs.full[s], row0 + 32 * i, kc);
+        } else {
+          tma_load_2d(a, mA, &bs.full[s], kc, row0);
+        }
+        tma_load_2d(sm + pl.bhi_off(s), mBh, &bs.full[s], kc, 0);
+        tma_load_2d(sm + pl.blo_off(s), mBl, &bs.full[s], kc, 0);
+        bulk_load(sm + pl.w_off(s), mean_w + kc, BK * 8, &bs.full[s]);
+        if (++s == pl.stages) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                  // ---- MMA issuer
+      const uint32_t idesc = idesc_tf32(pl.bn);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kt = 0; kt < nk; ++kt) {
+        const int b = kt & 1;
+        mbar_wait(&bs.full[s], ph);
+        mbar_wait(&bs.split_done[b], (kt >> 1) & 1);
+        fence_after();
+        const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
+        const uint32_t ahi = tmem + TM_A + 64 * b, alo = ahi + 32;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {          // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
+          const uint64_t dbh = desc_k_sw128(bh + kk * 32), dbl = desc_k_sw128(bl + kk * 32);
+          mma_ts(tmem, ahi + kk * 8, dbh, idesc, (kt | kk) != 0);
+          mma_ts(tmem, ahi + kk * 8, dbl, idesc, 1);
+          mma_ts(tmem, alo + kk * 8, dbh, idesc, 1);
+        }
+        mma_commit(&bs.empty[s]);                       // smem stage reusable once these MMAs retire
+        mma_commit(&bs.tfree[b]);                       // TMEM A buffer b reusable
+        if (++s == pl.stages) { s = 0; ph ^= 1; }
+      }
+      mma_commit(&bs.acc_full);
+    }
+  } else {                                            // ---- splitters (warps 2..9)
+    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and K half h: it owns row m and
+    // the 16 K columns [16h, 16h + 16) of every step.
+    const int q = warp & 3, h = (warp - 2) >> 2, m = 32 * q + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
+    double acc[4] = {0, 0, 0, 0};                     // independent DFMA chains (fixed-order sum below)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int kt = 0; kt < nk; ++kt) {
+      const int b = kt & 1;
+      mbar_wait(&bs.full[s], ph);
+      if (kt >= 2) mbar_wait(&bs.tfree[b], ((kt >> 1) - 1) & 1);
+      const unsigned char* a = sm + pl.a_off(s);
+      const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s)) + 16 * h;
+      float x[16];
+      if (MN) {       // box (m >> 5): 32 rows n of 128 B; element (n, d') at n*128 + ((d'>>2 ^ n&7) << 4) + (d'&3)*4
+        const unsigned char* box = a + (m >> 5) * 4096;
+        const int dq = (m & 31) >> 2, dr = (m & 3) * 4;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = 16 * h + i;
+          x[i] = *reinterpret_cast<const float*>(box + n * 128 + (((dq ^ (n & 7))) << 4) + dr);
+        }
+      } else {        // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
+        const unsigned char* rowp = a + m * 128;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * h + cc;
+          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
+          x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
+        }
+      }
+      float hi[16], lo[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        hi[i] = tf32_hi(x[i]);
+        lo[i] = x[i] - hi[i];
+        acc[i & 3] = fma((double)x[i], w[i], acc[i & 3]);   // mean column, fp64 (R10)
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bs.empty[s]);       // this warp has consumed its reads of the smem stage
+      tmem_st16(lane_addr + TM_A + 64 * b + 16 * h, hi);
+      tmem_st16(lane_addr + TM_A + 64 * b + 32 + 16 * h, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bs.split_done[b]);
+      if (++s == pl.stages) { s = 0; ph ^= 1; }
+    }
+    // combine the two K halves of row m in fixed order
+    bs.mean[warp - 2][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
+    acc0 = bs.mean[(warp - 2) & 3][lane] + bs.mean[((warp - 2) & 3) + 4][lane];   // halves h = 0, 1
+  }
+  return acc0;
+}
+
+__device__ void setup_cta(Bars& bs, int stages) {
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.empty[s], 1 + NSPLIT); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&bs.split_done[b], NSPLIT); mbar_init(&bs.tfree[b], 1); }
+    mbar_init(&bs.acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&bs.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+}
+
+__device__ void teardown_cta(Bars& bs) {
+  fence_before();
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(bs.tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- K1: W partials = Phi P (split-K over D)
+struct PhiPArgs {
+  Plan pl;
+  int N, D, K, kchunk;             // kchunk: multiple of BK
+  const double* p0;                // mean column p (fp64, D)
+  float* Wpart;                    // [split][K][Npad]
+  double* W0part;                  // [split][Npad]
+  int Npad;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ CUtensorMap mA,
+                                                        const __grid_constant__ CUtensorMap mBh,
+                                                        const __grid_constant__ CUtensorMap mBl, PhiPArgs a) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ Bars bs;
+  setup_cta(bs, a.pl.stages);
+  const int row0 = blockIdx.x * BM, split = blockIdx.y;
+  const int k0 = split * a.kchunk, k1 = min(a.D, k0 + a.kchunk);
+  const int nk = (k1 - k0 + BK - 1) / BK;
+  const double acc0 = mainloop<false>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, k1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= 2) {
+    const int q = warp & 3, h = (warp - 2) >> 2, n = row0 + 32 * q + lane;
+    const int cph = ((a.pl.bn / 16 + 1) / 2) * 16;    // accumulator columns per half
+    mbar_wait(&bs.acc_full, 0);
+    fence_after();
+    const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
+    float* wp = a.Wpart + (size_t)split * a.K * a.Npad;
+    for (int c = h * cph; c < min(a.pl.bn, (h + 1) * cph); c += 16) {
+      float v[16];
+      tmem_ld16(la + c, v);
+      if (n < a.N)
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c + i < a.K) wp[(size_t)(c + i) * a.Npad + n] = v[i];
+    }
+    if (h == 0 && n < a.N) a.W0part[(size_t)split * a.Npad + n] = acc0;
+  }
+  teardown_cta(bs);
+}
+
+// Split-K reduction in fixed order; writes W (for the SIMT fallback check), W_hi, W_lo and w0.
+__global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* __restrict__ Wpart,
+                              const double* __restrict__ W0part, float* __restrict__ Whi, float* __restrict__ Wlo,
+                              double* __restrict__ w0) {
+  const int64_t tot = (int64_t)K * Npad;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot + Npad; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < tot) {
+      const int n = (int)(i % Npad);
+      float v = 0.f;
+      if (n < N)
+        for (int s = 0; s < splits; ++s) v += Wpart[(int64_t)s * tot + i];
+      const float h = tf32_hi(v);
+      Whi[i] = h; Wlo[i] = v - h;
+    } else {
+      const int n = (int)(i - tot);
+      double v = 0.0;
+      if (n < N)
+        for (int s = 0; s < splits; ++s) v += W0part[(int64_t)s * Npad + n];
+      w0[n] = v;
+    }
+  }
+}
+
+// P_hi / P_lo of the probe block (B operand of K1), [K][Dp]
+__global__ void k_tc_split_p(int64_t n, const float* __restrict__ P, float* __restrict__ Phi_, float* __restrict__ Plo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(P)[i];
+    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    reinterpret_cast<float4*>(Phi_)[i] = h;
+    reinterpret_cast<float4*>(Plo)[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
+// ---------------------------------------------------------------- K2: Q = beta Phi^T W + alpha o P, gamma
+struct PhiTWArgs {
+  Plan pl;
+  int N, D, K;
+  int64_t Dp;
+  double beta;
+  const double* alpha; const double* w0; const double* p0; double* q0;
+  const float* P; float* Q;
+  ColState* cs; double* part; int stride; unsigned* counter; int iter;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__ CUtensorMap mA,
+                                                         const __grid_constant__ CUtensorMap mBh,
+                                                         const __grid_constant__ CUtensorMap mBl, PhiTWArgs a) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  __shared__ Bars bs;
+  for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
+  setup_cta(bs, a.pl.stages);
+  const int row0 = blockIdx.x * BM;
+  const int nk = (a.N + BK - 1) / BK;
+  const double acc0 = mainloop<true>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, a.N);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = a.K + 1;
+  if (warp >= 2) {
+    const int wi = warp - 2, q = warp & 3, h = wi >> 2, d = row0 + 32 * q + lane;
+    const int cph = ((a.pl.bn / 16 + 1) / 2) * 16;    // accumulator columns per half
+    const bool valid = d < a.D;
+    const double al = valid ? a.alpha[d] : 0.0;
+    if (h == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
+      double g = 0.0;
+      if (valid) {
+        const double p = a.p0[d], qv = a.beta * acc0 + al * p;
+        a.q0[d] = qv;
+        g = p * qv;
+      }
+      g = warp_sum(g);
+      if (lane == 0) bs.red[wi][0] = g;
+    }
+    mbar_wait(&bs.acc_full, 0);
+    fence_after();
+    const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
+    const float bt = (float)a.beta, alf = (float)al;
+    for (int c = h * cph; c < min(a.pl.bn, (h + 1) * cph); c += 16) {
+      float v[16];
+      tmem_ld16(la + c, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = c + i;
+        if (k < a.K) {                                // warp-uniform
+          double g = 0.0;
+          if (valid) {
+            const float p = a.P[(int64_t)k * a.Dp + d];
+            const float qv = bt * v[i] + alf * p;     // a3: q = beta Phi^T Phi p + alpha o p
+            a.Q[(int64_t)k * a.Dp + d] = qv;
+            g = (double)p * (double)qv;               // a4
+          }
+          g = warp_sum(g);
+          if (lane == 0) bs.red[wi][k + 1] = g;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // CTA partials (fixed warp order) -> part[j][cta]; last CTA reduces (deterministic), R5
+  for (int j = threadIdx.x; j < m; j += THREADS) {
+    double v = 0.0;
+#pragma unroll
+    for (int wi = 0; wi < NSPLIT; ++wi) v += bs.red[wi][j];
+    a.part[(int64_t)j * a.stride + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) bs.last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (bs.last) {
+    __threadfence();
+    for (int j = warp; j < m; j += THREADS / 32) {
+      const double v = reduce_partials(a.part + (int64_t)j * a.stride, gridDim.x);
+      if (lane == 0) { ColState c = a.cs[j]; finish_gamma(c, v, a.iter); a.cs[j] = c; }
+    }
+    if (threadIdx.x == 0) *a.counter = 0u;
+  }
+  teardown_cta(bs);
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiled)p;
+  }
+  return fn;
+}
+
+// 2D fp32 tensor [rows][cols] (cols contiguous, row pitch ld elements), box {bx (cols), by (rows)}, 128-B swizzle
+static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int bx, int by) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+static Plan plan_for(int bn) {
+  Plan p;
+  p.bn = bn;
+  p.stage_bytes = BM * BK * 4 + 2 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
+  p.stages = std::min(8, (200 * 1024) / p.stage_bytes);
+  return p;
+}
+static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes + 1024; }
+
+}  // namespace tc
+
+struct DenseTC {
+  CUtensorMap phi_k, phi_mn, phh, plo, whh, wlo;
+  float *Phi_, *Plo, *Whi, *Wlo, *Wpart;
+  double *W0part, *w0;
+  int bn, splits, kchunk, Npad;
+  tc::Plan pl;
+};
+
+void dense_tc_free(Ctx* c) {
+  DenseTC* t = (DenseTC*)c->dense_tc;
+  if (!t) return;
+  void* ptrs[] = {t->Phi_, t->Plo, t->Whi, t->Wlo, t->Wpart, t->W0part, t->w0};
+  for (void* p : ptrs) if (p) cudaFree(p);
+  delete t;
+  c->dense_tc = nullptr;
+}
+
+// Set up the tensor-core path (fp32 probes only).  Returns false (SIMT path stays) when
+// the shape cannot use it; errors in allocation are reported.
+cofem_status dense_tc_setup(Ctx* c) {
+  using namespace tc;
+  if (c->probe64 || getenv("COFEM_DENSE_SIMT")) return COFEM_OK;    // env: test hook for the SIMT path
+  if (c->D % 4 != 0 || c->Kcap > 128) return COFEM_OK;              // TMA needs 16-B row pitches; N <= 128 per MMA
+  if (!encoder()) return COFEM_OK;
+  DenseTC* t = new DenseTC();
+  memset(t, 0, sizeof *t);
+  c->dense_tc = t;
+  t->bn = std::max(16, (c->Kcap + 15) / 16 * 16);
+  t->pl = plan_for(t->bn);
+  t->Npad = (int)((c->N + 31) / 32 * 32);
+  const int mt = (int)((c->N + BM - 1) / BM);
+  // split-K so that the K1 grid covers the SMs about four times (>= 8 K steps per split)
+  const int ksteps = (int)((c->D + BK - 1) / BK);
+  int splits = std::max(1, std::min(ksteps / 8, (4 * c->num_sms + mt - 1) / mt));
+  t->kchunk = ((ksteps + splits - 1) / splits) * BK;
+  t->splits = (int)((c->D + t->kchunk - 1) / t->kchunk);
+  const size_t pk = (size_t)c->Kcap * c->Dp, wk = (size_t)c->Kcap * t->Npad;
+  if (cudaMalloc(&t->Phi_, pk * 4) || cudaMalloc(&t->Plo, pk * 4) || cudaMalloc(&t->Whi, wk * 4) ||
+      cudaMalloc(&t->Wlo, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
+      cudaMalloc(&t->W0part, (size_t)t->splits * t->Npad * 8) || cudaMalloc(&t->w0, (size_t)t->Npad * 8)) {
+    c->err = "cudaMalloc dense tensor-core workspace"; return COFEM_ERR_OOM;
+  }
+  cudaMemset(t->Phi_, 0, pk * 4); cudaMemset(t->Plo, 0, pk * 4);
+  cudaMemset(t->Whi, 0, wk * 4); cudaMemset(t->Wlo, 0, wk * 4);
+  bool ok = make_map(&t->phi_k, c->phi, c->D, c->N, c->ld, BK, BM) &&       // K1 A: Phi[n][d], box 32 d x 128 n
+            make_map(&t->phi_mn, c->phi, c->D, c->N, c->ld, 32, BK) &&      // K2 A: box 32 d x 32 n (x4 per tile)
+            make_map(&t->phh, t->Phi_, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&
+            make_map(&t->plo, t->Plo, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&
+            make_map(&t->whh, t->Whi, t->Npad, c->Kcap, t->Npad, BK, t->bn) &&
+            make_map(&t->wlo, t->Wlo, t->Npad, c->Kcap, t->Npad, BK, t->bn);
+  if (!ok) { c->err = "cuTensorMapEncodeTiled failed"; return COFEM_ERR_CUDA; }
+  const int sm = (int)smem_of(t->pl);
+  cudaFuncSetAttribute(k_tc_phiP, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiTW, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
+  return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
+cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
+  using namespace tc;
+  DenseTC* t = (DenseTC*)c->dense_tc;
+  const int K = m - 1;
+  const size_t sm = smem_of(t->pl);
+  launch_begin(c, KC_DENSE_PHI_P);
+  k_tc_split_p<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * c->Dp, (const float*)c->P, t->Phi_, t->Plo);
+  PhiPArgs a1;
+  a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
+  a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
+  k_tc_phiP<<<dim3((unsigned)((c->N + BM - 1) / BM), t->splits), THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->plo, a1);
+  k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Whi,
+                                                       t->Wlo, t->w0);
+  launch_end(c, KC_DENSE_PHI_P);
+  if (check_launch(c, "k_tc_phiP")) return COFEM_ERR_CUDA;
+  PhiTWArgs a2;
+  a2.pl = t->pl; a2.N = (int)c->N; a2.D = (int)c->D; a2.K = K; a2.Dp = c->Dp; a2.beta = c->beta;
+  a2.alpha = c->alpha; a2.w0 = t->w0; a2.p0 = c->p0; a2.q0 = c->q0; a2.P = (const float*)c->P; a2.Q = (float*)c->Q;
+  a2.cs = c->cs; a2.part = c->part; a2.stride = c->part_stride; a2.counter = c->counters + MAXM; a2.iter = iter;
+  launch_begin(c, KC_DENSE_PHIT_W);
+  k_tc_phiTW<<<(unsigned)((c->D + BM - 1) / BM), THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wlo, a2);
+  launch_end(c, KC_DENSE_PHIT_W);
+  if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
+  return COFEM_OK;
+}
+
+}  // namespace cofem
