@@ -21,8 +21,9 @@
 //               (column 0 of B = [b0 | p_1..p_K], reading R2; fp64 per DESIGN.md R10)
 //               in a register with DFMA; after the last step they are the epilogue
 //               (tcgen05.ld of the fp32 accumulator -> q, gamma partials / W partials).
-// The probe B operand's hi/lo split is done once per apply in global memory (B is
-// O((N + D) K), Phi is O(N D)).  Only the probe columns use the tensor cores; parity
+// The probe B operand (P for K1, W for K2) arrives once per K step by TMA in fp32 and is
+// split into hi/lo shared-memory tiles by the same splitter warps (fence.proxy.async before
+// the MMA reads them), so B crosses L2 once, not twice.  Only the probe columns use the tensor cores; parity
 // mode (fp64 probes) keeps the SIMT path (op_dense.cu).
 #include <cuda.h>
 #include <stdio.h>
@@ -34,8 +35,12 @@
 namespace cofem {
 namespace tc {
 
-constexpr int BM = 128, BK = 32, NSPLIT = 8, THREADS = 64 + 32 * NSPLIT;   // warps 0-1 + 8 splitter warps
-constexpr int TMEM_COLS = 256;             // [0, BN) accumulator; [128, 256) two A buffers (hi 32 | lo 32)
+constexpr int BM = 128, BK = 32;
+constexpr int NGROUP = 4;                  // splitter groups: group g handles K steps kt = g (mod NGROUP)
+constexpr int NSPLIT = 4 * NGROUP;         // splitter warps (one per TMEM lane quarter per group)
+constexpr int THREADS = 64 + 32 * NSPLIT;  // warps 0-1 + splitters
+constexpr int NAB = 6;                     // TMEM A buffers (hi 32 | lo 32 columns each)
+constexpr int TMEM_COLS = 512;             // [0, BN) accumulator; [128, 128 + 64 NAB) A buffers (1 CTA / SM)
 constexpr int TM_A = 128;
 
 // ---------------------------------------------------------------- PTX wrappers
@@ -138,17 +143,18 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int bn) {
 __device__ __forceinline__ float tf32_hi(float x) { return __int_as_float(__float_as_int(x) & 0xFFFFE000); }
 
 // Shared-memory plan (dynamic, 1024-aligned):
-// STAGES x [A 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64]
+// STAGES x [A 16 KB | B (TMA) bn x 128 B | Bhi | Blo | mean-column operand 32 x fp64]
 struct Plan {
   int bn, stages, stage_bytes;
   __host__ __device__ int a_off(int s) const { return s * stage_bytes; }
-  __host__ __device__ int bhi_off(int s) const { return s * stage_bytes + BM * BK * 4; }
-  __host__ __device__ int blo_off(int s) const { return s * stage_bytes + BM * BK * 4 + bn * 128; }
-  __host__ __device__ int w_off(int s) const { return s * stage_bytes + BM * BK * 4 + 2 * bn * 128; }
+  __host__ __device__ int b_off(int s) const { return s * stage_bytes + BM * BK * 4; }
+  __host__ __device__ int bhi_off(int s) const { return s * stage_bytes + BM * BK * 4 + bn * 128; }
+  __host__ __device__ int blo_off(int s) const { return s * stage_bytes + BM * BK * 4 + 2 * bn * 128; }
+  __host__ __device__ int w_off(int s) const { return s * stage_bytes + BM * BK * 4 + 3 * bn * 128; }
 };
 
 struct Bars {
-  uint64_t full[8], empty[8], split_done[2], tfree[2], acc_full;
+  uint64_t full[8], empty[8], split_done[NAB], tfree[NAB], acc_full;
   uint32_t tmem_base;
   double red[NSPLIT][MAXM]; // epilogue per-warp column partials
   double mean[NSPLIT][32];  // mean-column partials of the two halves of each row
@@ -161,15 +167,15 @@ struct Bars {
 // mean_w: the fp64 mean-column operand along K (w0 for phiTW, p0 for phiP); returns the
 // thread's fp64 mean-column accumulator (row m = its splitter index).
 template <bool MN>
-__device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mBh,
-                           const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
+__device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mB,
+                           int row0, int k0, int nk, const double* __restrict__ mean_w,
                            int ktot) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
   double acc0 = 0.0;
   if (warp == 0) {
     if (lane == 0) {                                  // ---- TMA producer
-      const uint32_t bytes = BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
+      const uint32_t bytes = BM * BK * 4 + pl.bn * 128 + BK * 8;
       int s = 0;
       uint32_t ph = 0;
       for (int kt = 0; kt < nk; ++kt) {
@@ -178,13 +184,11 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
         const int kc = k0 + kt * BK;
         unsigned char* a = sm + pl.a_off(s);
         if (MN) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) tma_load_2d(a + i * 4096, mA, &bs.full[s], row0 + 32 * i, kc);
+          tma_load_2d(a, mA, &bs.full[s], row0, kc);   // one box: 32 rows n of 128 d (512 B), no swizzle
         } else {
           tma_load_2d(a, mA, &bs.full[s], kc, row0);
         }
-        tma_load_2d(sm + pl.bhi_off(s), mBh, &bs.full[s], kc, 0);
-        tma_load_2d(sm + pl.blo_off(s), mBl, &bs.full[s], kc, 0);
+        tma_load_2d(sm + pl.b_off(s), mB, &bs.full[s], kc, 0);
         bulk_load(sm + pl.w_off(s), mean_w + kc, BK * 8, &bs.full[s]);
         if (++s == pl.stages) { s = 0; ph ^= 1; }
       }
@@ -195,9 +199,9 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
       int s = 0;
       uint32_t ph = 0;
       for (int kt = 0; kt < nk; ++kt) {
-        const int b = kt & 1;
+        const int b = kt % NAB;
         mbar_wait(&bs.full[s], ph);
-        mbar_wait(&bs.split_done[b], (kt >> 1) & 1);
+        mbar_wait(&bs.split_done[b], (kt / NAB) & 1);
         fence_after();
         const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
         const uint32_t ahi = tmem + TM_A + 64 * b, alo = ahi + 32;
@@ -214,59 +218,77 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
       }
       mma_commit(&bs.acc_full);
     }
-  } else {                                            // ---- splitters (warps 2..9)
-    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and K half h: it owns row m and
-    // the 16 K columns [16h, 16h + 16) of every step.
-    const int q = warp & 3, h = (warp - 2) >> 2, m = 32 * q + lane;
+  } else {                                            // ---- splitters (warps 2 .. 2 + NSPLIT)
+    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m for
+    // the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently.
+    const int wi = warp - 2, q = warp & 3, g = wi >> 2, m = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
     double acc[4] = {0, 0, 0, 0};                     // independent DFMA chains (fixed-order sum below)
-    int s = 0;
-    uint32_t ph = 0;
-    for (int kt = 0; kt < nk; ++kt) {
-      const int b = kt & 1;
+    int s = g % pl.stages;
+    uint32_t ph = (g / pl.stages) & 1;
+    for (int kt = g; kt < nk; kt += NGROUP) {
+      const int b = kt % NAB;
       mbar_wait(&bs.full[s], ph);
-      if (kt >= 2) mbar_wait(&bs.tfree[b], ((kt >> 1) - 1) & 1);
+      if (kt >= NAB) mbar_wait(&bs.tfree[b], ((kt / NAB) - 1) & 1);
       const unsigned char* a = sm + pl.a_off(s);
-      const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s)) + 16 * h;
-      float x[16];
-      if (MN) {       // box (m >> 5): 32 rows n of 128 B; element (n, d') at n*128 + ((d'>>2 ^ n&7) << 4) + (d'&3)*4
-        const unsigned char* box = a + (m >> 5) * 4096;
-        const int dq = (m & 31) >> 2, dr = (m & 3) * 4;
+      const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float x[16];
+        if (MN) {     // [32 n][128 d] dense: a warp reads 128 contiguous bytes per n (conflict-free)
+          const float* col = reinterpret_cast<const float*>(a) + m;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) x[i] = col[(16 * h + i) * BM];
+        } else {      // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
+          const unsigned char* rowp = a + m * 128;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = 4 * h + cc;
+            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
+            x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
+          }
+        }
+        float hi[16], lo[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const int n = 16 * h + i;
-          x[i] = *reinterpret_cast<const float*>(box + n * 128 + (((dq ^ (n & 7))) << 4) + dr);
+          hi[i] = tf32_hi(x[i]);
+          lo[i] = x[i] - hi[i];
+#ifndef COFEM_TC_EXPERIMENT_NOMEAN
+          acc[i & 3] = fma((double)x[i], w[16 * h + i], acc[i & 3]);   // mean column, fp64 (R10)
+#endif
         }
-      } else {        // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
-        const unsigned char* rowp = a + m * 128;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c = 4 * h + cc;
-          const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
-          x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
-        }
+        tmem_st16(lane_addr + TM_A + 64 * b + 16 * h, hi);
+        tmem_st16(lane_addr + TM_A + 64 * b + 32 + 16 * h, lo);
       }
-      float hi[16], lo[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        hi[i] = tf32_hi(x[i]);
-        lo[i] = x[i] - hi[i];
-        acc[i & 3] = fma((double)x[i], w[i], acc[i & 3]);   // mean column, fp64 (R10)
+      {   // this group's share of the B split (layout-agnostic: hi / lo at the same offsets)
+        const int t = 32 * q + lane;                  // 0..127 within the group
+        const float4* bsrc = reinterpret_cast<const float4*>(sm + pl.b_off(s));
+        float4* bh = reinterpret_cast<float4*>(sm + pl.bhi_off(s));
+        float4* bl = reinterpret_cast<float4*>(sm + pl.blo_off(s));
+        for (int i = t; i < pl.bn * 8; i += 128) {
+          const float4 v = bsrc[i];
+          const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          bh[i] = hv;
+          bl[i] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy smem writes -> tensor core
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bs.empty[s]);       // this warp has consumed its reads of the smem stage
-      tmem_st16(lane_addr + TM_A + 64 * b + 16 * h, hi);
-      tmem_st16(lane_addr + TM_A + 64 * b + 32 + 16 * h, lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bs.split_done[b]);
-      if (++s == pl.stages) { s = 0; ph ^= 1; }
+      s += NGROUP;
+      while (s >= pl.stages) { s -= pl.stages; ph ^= 1; }
     }
-    // combine the two K halves of row m in fixed order
-    bs.mean[warp - 2][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    // combine the groups' partial sums of row m in fixed order (g = 0 .. NGROUP-1)
+    bs.mean[wi][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
-    acc0 = bs.mean[(warp - 2) & 3][lane] + bs.mean[((warp - 2) & 3) + 4][lane];   // halves h = 0, 1
+    double t = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < NGROUP; ++gg) t += bs.mean[4 * gg + (wi & 3)][lane];
+    acc0 = t;
   }
   return acc0;
 }
@@ -274,8 +296,8 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
 __device__ void setup_cta(Bars& bs, int stages) {
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.empty[s], 1 + NSPLIT); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&bs.split_done[b], NSPLIT); mbar_init(&bs.tfree[b], 1); }
+    for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.empty[s], 1 + 4); }
+    for (int b = 0; b < NAB; ++b) { mbar_init(&bs.split_done[b], 4); mbar_init(&bs.tfree[b], 1); }
     mbar_init(&bs.acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -309,20 +331,18 @@ struct PhiPArgs {
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ CUtensorMap mA,
-                                                        const __grid_constant__ CUtensorMap mBh,
-                                                        const __grid_constant__ CUtensorMap mBl, PhiPArgs a) {
-  extern __shared__ __align__(1024) unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  __shared__ Bars bs;
+                                                        const __grid_constant__ CUtensorMap mB, PhiPArgs a) {
+  extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
+  Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   setup_cta(bs, a.pl.stages);
   const int row0 = blockIdx.x * BM, split = blockIdx.y;
   const int k0 = split * a.kchunk, k1 = min(a.D, k0 + a.kchunk);
   const int nk = (k1 - k0 + BK - 1) / BK;
-  const double acc0 = mainloop<false>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, k1);
+  const double acc0 = mainloop<false>(a.pl, sm, bs, &mA, &mB, row0, k0, nk, a.p0, k1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= 2) {
     const int q = warp & 3, h = (warp - 2) >> 2, n = row0 + 32 * q + lane;
-    const int cph = ((a.pl.bn / 16 + 1) / 2) * 16;    // accumulator columns per half
+    const int cph = ((a.pl.bn / 16 + NGROUP - 1) / NGROUP) * 16;   // accumulator columns per group
     mbar_wait(&bs.acc_full, 0);
     fence_after();
     const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
@@ -342,8 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ 
 
 // Split-K reduction in fixed order; writes W (for the SIMT fallback check), W_hi, W_lo and w0.
 __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* __restrict__ Wpart,
-                              const double* __restrict__ W0part, float* __restrict__ Whi, float* __restrict__ Wlo,
-                              double* __restrict__ w0) {
+                              const double* __restrict__ W0part, float* __restrict__ W, double* __restrict__ w0) {
   const int64_t tot = (int64_t)K * Npad;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot + Npad; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < tot) {
@@ -351,8 +370,7 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
       float v = 0.f;
       if (n < N)
         for (int s = 0; s < splits; ++s) v += Wpart[(int64_t)s * tot + i];
-      const float h = tf32_hi(v);
-      Whi[i] = h; Wlo[i] = v - h;
+      W[i] = v;
     } else {
       const int n = (int)(i - tot);
       double v = 0.0;
@@ -360,16 +378,6 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
         for (int s = 0; s < splits; ++s) v += W0part[(int64_t)s * Npad + n];
       w0[n] = v;
     }
-  }
-}
-
-// P_hi / P_lo of the probe block (B operand of K1), [K][Dp]
-__global__ void k_tc_split_p(int64_t n, const float* __restrict__ P, float* __restrict__ Phi_, float* __restrict__ Plo) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 v = reinterpret_cast<const float4*>(P)[i];
-    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-    reinterpret_cast<float4*>(Phi_)[i] = h;
-    reinterpret_cast<float4*>(Plo)[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
   }
 }
 
@@ -385,21 +393,19 @@ struct PhiTWArgs {
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__ CUtensorMap mA,
-                                                         const __grid_constant__ CUtensorMap mBh,
-                                                         const __grid_constant__ CUtensorMap mBl, PhiTWArgs a) {
-  extern __shared__ __align__(1024) unsigned char smraw[];
-  unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  __shared__ Bars bs;
+                                                         const __grid_constant__ CUtensorMap mB, PhiTWArgs a) {
+  extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
+  Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
   setup_cta(bs, a.pl.stages);
   const int row0 = blockIdx.x * BM;
   const int nk = (a.N + BK - 1) / BK;
-  const double acc0 = mainloop<true>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, a.N);
+  const double acc0 = mainloop<true>(a.pl, sm, bs, &mA, &mB, row0, 0, nk, a.w0, a.N);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.K + 1;
   if (warp >= 2) {
     const int wi = warp - 2, q = warp & 3, h = wi >> 2, d = row0 + 32 * q + lane;
-    const int cph = ((a.pl.bn / 16 + 1) / 2) * 16;    // accumulator columns per half
+    const int cph = ((a.pl.bn / 16 + NGROUP - 1) / NGROUP) * 16;   // accumulator columns per group
     const bool valid = d < a.D;
     const double al = valid ? a.alpha[d] : 0.0;
     if (h == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
@@ -477,7 +483,8 @@ static EncodeTiled encoder() {
 }
 
 // 2D fp32 tensor [rows][cols] (cols contiguous, row pitch ld elements), box {bx (cols), by (rows)}, 128-B swizzle
-static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int bx, int by) {
+static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, int bx, int by,
+                     bool swizzle = true) {
   EncodeTiled enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -485,24 +492,25 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t ro
   cuuint32_t box[2] = {(cuuint32_t)bx, (cuuint32_t)by};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
 static Plan plan_for(int bn) {
   Plan p;
   p.bn = bn;
-  p.stage_bytes = BM * BK * 4 + 2 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
-  p.stages = std::min(8, (200 * 1024) / p.stage_bytes);
+  p.stage_bytes = BM * BK * 4 + 3 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
+  p.stages = std::min(8, (int)((220 * 1024 - sizeof(Bars)) / p.stage_bytes));
   return p;
 }
-static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes + 1024; }
+static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes + sizeof(Bars); }
 
 }  // namespace tc
 
 struct DenseTC {
-  CUtensorMap phi_k, phi_mn, phh, plo, whh, wlo;
-  float *Phi_, *Plo, *Whi, *Wlo, *Wpart;
+  CUtensorMap phi_k, phi_mn, pmap, wmap;
+  float *W, *Wpart;
   double *W0part, *w0;
   int bn, splits, kchunk, Npad;
   tc::Plan pl;
@@ -511,7 +519,7 @@ struct DenseTC {
 void dense_tc_free(Ctx* c) {
   DenseTC* t = (DenseTC*)c->dense_tc;
   if (!t) return;
-  void* ptrs[] = {t->Phi_, t->Plo, t->Whi, t->Wlo, t->Wpart, t->W0part, t->w0};
+  void* ptrs[] = {t->W, t->Wpart, t->W0part, t->w0};
   for (void* p : ptrs) if (p) cudaFree(p);
   delete t;
   c->dense_tc = nullptr;
@@ -536,20 +544,16 @@ cofem_status dense_tc_setup(Ctx* c) {
   int splits = std::max(1, std::min(ksteps / 8, (4 * c->num_sms + mt - 1) / mt));
   t->kchunk = ((ksteps + splits - 1) / splits) * BK;
   t->splits = (int)((c->D + t->kchunk - 1) / t->kchunk);
-  const size_t pk = (size_t)c->Kcap * c->Dp, wk = (size_t)c->Kcap * t->Npad;
-  if (cudaMalloc(&t->Phi_, pk * 4) || cudaMalloc(&t->Plo, pk * 4) || cudaMalloc(&t->Whi, wk * 4) ||
-      cudaMalloc(&t->Wlo, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
+  const size_t wk = (size_t)c->Kcap * t->Npad;
+  if (cudaMalloc(&t->W, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
       cudaMalloc(&t->W0part, (size_t)t->splits * t->Npad * 8) || cudaMalloc(&t->w0, (size_t)t->Npad * 8)) {
     c->err = "cudaMalloc dense tensor-core workspace"; return COFEM_ERR_OOM;
   }
-  cudaMemset(t->Phi_, 0, pk * 4); cudaMemset(t->Plo, 0, pk * 4);
-  cudaMemset(t->Whi, 0, wk * 4); cudaMemset(t->Wlo, 0, wk * 4);
+  cudaMemset(t->W, 0, wk * 4);
   bool ok = make_map(&t->phi_k, c->phi, c->D, c->N, c->ld, BK, BM) &&       // K1 A: Phi[n][d], box 32 d x 128 n
-            make_map(&t->phi_mn, c->phi, c->D, c->N, c->ld, 32, BK) &&      // K2 A: box 32 d x 32 n (x4 per tile)
-            make_map(&t->phh, t->Phi_, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&
-            make_map(&t->plo, t->Plo, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&
-            make_map(&t->whh, t->Whi, t->Npad, c->Kcap, t->Npad, BK, t->bn) &&
-            make_map(&t->wlo, t->Wlo, t->Npad, c->Kcap, t->Npad, BK, t->bn);
+            make_map(&t->phi_mn, c->phi, c->D, c->N, c->ld, BM, BK, false) &&   // K2 A: box 128 d x 32 n, dense
+            make_map(&t->pmap, (const float*)c->P, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&   // K1 B: P [K][Dp]
+            make_map(&t->wmap, t->W, t->Npad, c->Kcap, t->Npad, BK, t->bn);                // K2 B: W [K][Npad]
   if (!ok) { c->err = "cuTensorMapEncodeTiled failed"; return COFEM_ERR_CUDA; }
   const int sm = (int)smem_of(t->pl);
   cudaFuncSetAttribute(k_tc_phiP, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
@@ -564,13 +568,12 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   const int K = m - 1;
   const size_t sm = smem_of(t->pl);
   launch_begin(c, KC_DENSE_PHI_P);
-  k_tc_split_p<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * c->Dp, (const float*)c->P, t->Phi_, t->Plo);
   PhiPArgs a1;
   a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
   a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
-  k_tc_phiP<<<dim3((unsigned)((c->N + BM - 1) / BM), t->splits), THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->plo, a1);
-  k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Whi,
-                                                       t->Wlo, t->w0);
+  k_tc_phiP<<<dim3((unsigned)((c->N + BM - 1) / BM), t->splits), THREADS, sm, c->stream>>>(t->phi_k, t->pmap, a1);
+  k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->W,
+                                                       t->w0);
   launch_end(c, KC_DENSE_PHI_P);
   if (check_launch(c, "k_tc_phiP")) return COFEM_ERR_CUDA;
   PhiTWArgs a2;
@@ -578,7 +581,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   a2.alpha = c->alpha; a2.w0 = t->w0; a2.p0 = c->p0; a2.q0 = c->q0; a2.P = (const float*)c->P; a2.Q = (float*)c->Q;
   a2.cs = c->cs; a2.part = c->part; a2.stride = c->part_stride; a2.counter = c->counters + MAXM; a2.iter = iter;
   launch_begin(c, KC_DENSE_PHIT_W);
-  k_tc_phiTW<<<(unsigned)((c->D + BM - 1) / BM), THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wlo, a2);
+  k_tc_phiTW<<<(unsigned)((c->D + BM - 1) / BM), THREADS, sm, c->stream>>>(t->phi_mn, t->wmap, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
   return COFEM_OK;
