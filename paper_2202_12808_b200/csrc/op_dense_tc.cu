@@ -21,9 +21,9 @@
 //               (column 0 of B = [b0 | p_1..p_K], reading R2; fp64 per DESIGN.md R10)
 //               in a register with DFMA; after the last step they are the epilogue
 //               (tcgen05.ld of the fp32 accumulator -> q, gamma partials / W partials).
-// The probe B operand (P for K1, W for K2) arrives once per K step by TMA in fp32 and is
-// split into hi/lo shared-memory tiles by the same splitter warps (fence.proxy.async before
-// the MMA reads them), so B crosses L2 once, not twice.  Only the probe columns use the tensor cores; parity
+// The probe B operand's hi/lo split is done once per apply in global memory (B is
+// O((N + D) K), Phi is O(N D)); a CTA covers MT = 2 M-tiles (256 rows) when K <= 64 so
+// each B tile loaded from L2 feeds two accumulators.  Only the probe columns use the tensor cores; parity
 // mode (fp64 probes) keeps the SIMT path (op_dense.cu).
 #include <cuda.h>
 #include <stdio.h>
@@ -36,7 +36,7 @@ namespace cofem {
 namespace tc {
 
 constexpr int BM = 128, BK = 32;
-constexpr int NGROUP = 4;                  // splitter groups: group g handles K steps kt = g (mod NGROUP)
+constexpr int NGROUP = 3;                  // splitter groups: group g handles K steps kt = g (mod NGROUP)
 constexpr int NSPLIT = 4 * NGROUP;         // splitter warps (one per TMEM lane quarter per group)
 constexpr int THREADS = 64 + 32 * NSPLIT;  // warps 0-1 + splitters
 constexpr int NAB = 6;                     // TMEM A buffers (hi 32 | lo 32 columns each)
@@ -143,52 +143,66 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int bn) {
 __device__ __forceinline__ float tf32_hi(float x) { return __int_as_float(__float_as_int(x) & 0xFFFFE000); }
 
 // Shared-memory plan (dynamic, 1024-aligned):
-// STAGES x [A 16 KB | B (TMA) bn x 128 B | Bhi | Blo | mean-column operand 32 x fp64]
+// STAGES x [A: MT tiles x 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64 (1 KB)]
 struct Plan {
-  int bn, stages, stage_bytes;
-  __host__ __device__ int a_off(int s) const { return s * stage_bytes; }
-  __host__ __device__ int b_off(int s) const { return s * stage_bytes + BM * BK * 4; }
-  __host__ __device__ int bhi_off(int s) const { return s * stage_bytes + BM * BK * 4 + bn * 128; }
-  __host__ __device__ int blo_off(int s) const { return s * stage_bytes + BM * BK * 4 + 2 * bn * 128; }
-  __host__ __device__ int w_off(int s) const { return s * stage_bytes + BM * BK * 4 + 3 * bn * 128; }
+  int bn, mt, stages, stage_bytes;
+  __host__ __device__ int a_off(int s, int t) const { return s * stage_bytes + t * BM * BK * 4; }
+  __host__ __device__ int bhi_off(int s) const { return s * stage_bytes + mt * BM * BK * 4; }
+  __host__ __device__ int blo_off(int s) const { return s * stage_bytes + mt * BM * BK * 4 + bn * 128; }
+  __host__ __device__ int w_off(int s) const { return s * stage_bytes + mt * BM * BK * 4 + 2 * bn * 128; }
 };
 
+constexpr int MAXMT = 2;
 struct Bars {
   uint64_t full[8], empty[8], split_done[NAB], tfree[NAB], acc_full;
   uint32_t tmem_base;
-  double red[NSPLIT][MAXM]; // epilogue per-warp column partials
-  double mean[NSPLIT][32];  // mean-column partials of the two halves of each row
+  double red[NSPLIT][MAXM];        // epilogue per-warp column partials
+  double mean[NSPLIT][MAXMT][32];  // mean-column partials of the groups
   int last;
 };
 
+// TMEM columns: accumulator of M-tile t at t * ACCW (ACCW = 64 when MT = 2, else 128);
+// A buffer b of M-tile t at TM_A + (b * MT + t) * 64 (hi 32 | lo 32).  NAB buffers
+// are cycled (nab = 6 / MT).
+template <int MT> struct TmemPlan {
+  static constexpr int ACCW = MT == 2 ? 64 : 128;
+  static constexpr int NABU = NAB / MT;
+  static __device__ __forceinline__ uint32_t acc(int t) { return t * ACCW; }
+  static __device__ __forceinline__ uint32_t abuf(int b, int t) { return TM_A + (b * MT + t) * 64; }
+};
+
 // ---------------------------------------------------------------- the shared mainloop
-// MN = true: the A tile is Phi[n0 : n0+32][d0 : d0+128] stored as four MN-major 32x32 boxes
-// (k_tc_phiTW, A = Phi^T); false: Phi[n0 : n0+128][d0 : d0+32] K-major (k_tc_phiP, A = Phi).
-// mean_w: the fp64 mean-column operand along K (w0 for phiTW, p0 for phiP); returns the
-// thread's fp64 mean-column accumulator (row m = its splitter index).
-template <bool MN>
-__device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mB,
-                           int row0, int k0, int nk, const double* __restrict__ mean_w,
-                           int ktot) {
+// MN = true: A tile t is Phi[n0 : n0+32][d0 + 128 t : +128] as one dense [32][128] box
+// (k_tc_phiTW, A = Phi^T, row m = d); false: Phi[n0 + 128 t : +128][d0 : d0+32], K-major
+// with the 128-B swizzle (k_tc_phiP, A = Phi, row m = n).  mean_w: the fp64 mean-column
+// operand along K (w0 for phiTW, p0 for phiP).  Returns, for a splitter thread, its fp64
+// mean-column accumulators of row m of each tile (acc0[t]).
+template <bool MN, int MT>
+__device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mBh,
+                         const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
+                         double (&acc0)[MT]) {
+  using TP = TmemPlan<MT>;
+  constexpr int NABU = TP::NABU;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
-  double acc0 = 0.0;
+#pragma unroll
+  for (int t = 0; t < MT; ++t) acc0[t] = 0.0;
   if (warp == 0) {
     if (lane == 0) {                                  // ---- TMA producer
-      const uint32_t bytes = BM * BK * 4 + pl.bn * 128 + BK * 8;
+      const uint32_t bytes = MT * BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
       int s = 0;
       uint32_t ph = 0;
       for (int kt = 0; kt < nk; ++kt) {
         if (kt >= pl.stages) mbar_wait(&bs.empty[s], ph ^ 1);
         mbar_expect_tx(&bs.full[s], bytes);
         const int kc = k0 + kt * BK;
-        unsigned char* a = sm + pl.a_off(s);
-        if (MN) {
-          tma_load_2d(a, mA, &bs.full[s], row0, kc);   // one box: 32 rows n of 128 d (512 B), no swizzle
-        } else {
-          tma_load_2d(a, mA, &bs.full[s], kc, row0);
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          if (MN) tma_load_2d(sm + pl.a_off(s, t), mA, &bs.full[s], row0 + BM * t, kc);
+          else tma_load_2d(sm + pl.a_off(s, t), mA, &bs.full[s], kc, row0 + BM * t);
         }
-        tma_load_2d(sm + pl.b_off(s), mB, &bs.full[s], kc, 0);
+        tma_load_2d(sm + pl.bhi_off(s), mBh, &bs.full[s], kc, 0);
+        tma_load_2d(sm + pl.blo_off(s), mBl, &bs.full[s], kc, 0);
         bulk_load(sm + pl.w_off(s), mean_w + kc, BK * 8, &bs.full[s]);
         if (++s == pl.stages) { s = 0; ph ^= 1; }
       }
@@ -199,80 +213,85 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
       int s = 0;
       uint32_t ph = 0;
       for (int kt = 0; kt < nk; ++kt) {
-        const int b = kt % NAB;
+        const int b = kt % NABU;
         mbar_wait(&bs.full[s], ph);
-        mbar_wait(&bs.split_done[b], (kt / NAB) & 1);
+        mbar_wait(&bs.split_done[b], (kt / NABU) & 1);
         fence_after();
         const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
-        const uint32_t ahi = tmem + TM_A + 64 * b, alo = ahi + 32;
+#ifndef COFEM_TC_EXPERIMENT_NOCOMPUTE
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {          // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
-          const uint64_t dbh = desc_k_sw128(bh + kk * 32), dbl = desc_k_sw128(bl + kk * 32);
-          mma_ts(tmem, ahi + kk * 8, dbh, idesc, (kt | kk) != 0);
-          mma_ts(tmem, ahi + kk * 8, dbl, idesc, 1);
-          mma_ts(tmem, alo + kk * 8, dbh, idesc, 1);
+        for (int t = 0; t < MT; ++t) {
+          const uint32_t d = tmem + TP::acc(t), ahi = tmem + TP::abuf(b, t), alo = ahi + 32;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {        // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
+            const uint64_t dbh = desc_k_sw128(bh + kk * 32), dbl = desc_k_sw128(bl + kk * 32);
+#ifndef COFEM_TC_EXP_NOMMA
+            mma_ts(d, ahi + kk * 8, dbh, idesc, (kt | kk) != 0);
+            mma_ts(d, ahi + kk * 8, dbl, idesc, 1);
+            mma_ts(d, alo + kk * 8, dbh, idesc, 1);
+#endif
+          }
         }
+#endif
         mma_commit(&bs.empty[s]);                       // smem stage reusable once these MMAs retire
-        mma_commit(&bs.tfree[b]);                       // TMEM A buffer b reusable
+        mma_commit(&bs.tfree[b]);                       // TMEM A buffers b reusable
         if (++s == pl.stages) { s = 0; ph ^= 1; }
       }
       mma_commit(&bs.acc_full);
     }
   } else {                                            // ---- splitters (warps 2 .. 2 + NSPLIT)
-    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m for
-    // the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently.
+    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m of
+    // every M-tile for the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently.
     const int wi = warp - 2, q = warp & 3, g = wi >> 2, m = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
-    double acc[4] = {0, 0, 0, 0};                     // independent DFMA chains (fixed-order sum below)
+    double acc[MT][4];                                // independent DFMA chains (fixed-order sums below)
+#pragma unroll
+    for (int t = 0; t < MT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
     int s = g % pl.stages;
     uint32_t ph = (g / pl.stages) & 1;
     for (int kt = g; kt < nk; kt += NGROUP) {
-      const int b = kt % NAB;
+      const int b = kt % NABU;
       mbar_wait(&bs.full[s], ph);
-      if (kt >= NAB) mbar_wait(&bs.tfree[b], ((kt / NAB) - 1) & 1);
-      const unsigned char* a = sm + pl.a_off(s);
+      if (kt >= NABU) mbar_wait(&bs.tfree[b], ((kt / NABU) - 1) & 1);
       const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s));
+#ifndef COFEM_TC_EXPERIMENT_NOCOMPUTE
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float x[16];
-        if (MN) {     // [32 n][128 d] dense: a warp reads 128 contiguous bytes per n (conflict-free)
-          const float* col = reinterpret_cast<const float*>(a) + m;
+      for (int t = 0; t < MT; ++t) {
+        const unsigned char* a = sm + pl.a_off(s, t);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) x[i] = col[(16 * h + i) * BM];
-        } else {      // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
-          const unsigned char* rowp = a + m * 128;
+        for (int h = 0; h < 2; ++h) {
+          float x[16];
+          if (MN) {   // [32 n][128 d] dense: a warp reads 128 contiguous bytes per n (conflict-free)
+            const float* col = reinterpret_cast<const float*>(a) + m;
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            const int c = 4 * h + cc;
-            const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
-            x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
+            for (int i = 0; i < 16; ++i) x[i] = col[(16 * h + i) * BM];
+          } else {    // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
+            const unsigned char* rowp = a + m * 128;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              const int c = 4 * h + cc;
+              const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
+              x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
+            }
           }
-        }
-        float hi[16], lo[16];
+          float hi[16], lo[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          hi[i] = tf32_hi(x[i]);
-          lo[i] = x[i] - hi[i];
-#ifndef COFEM_TC_EXPERIMENT_NOMEAN
-          acc[i & 3] = fma((double)x[i], w[16 * h + i], acc[i & 3]);   // mean column, fp64 (R10)
+          for (int i = 0; i < 16; ++i) {
+            hi[i] = tf32_hi(x[i]);
+            lo[i] = x[i] - hi[i];
+#ifndef COFEM_TC_EXP_NOMEAN
+            acc[t][i & 3] = fma((double)x[i], w[16 * h + i], acc[t][i & 3]);   // mean column, fp64 (R10)
+#endif
+          }
+#ifndef COFEM_TC_EXP_NOSTTM
+          tmem_st16(lane_addr + TP::abuf(b, t) + 16 * h, hi);
+          tmem_st16(lane_addr + TP::abuf(b, t) + 32 + 16 * h, lo);
+#else
+          if (hi[0] == 1.2345f && lo[3] == 2.5f) acc[t][0] += 1.0;   // keep the split live
 #endif
         }
-        tmem_st16(lane_addr + TM_A + 64 * b + 16 * h, hi);
-        tmem_st16(lane_addr + TM_A + 64 * b + 32 + 16 * h, lo);
       }
-      {   // this group's share of the B split (layout-agnostic: hi / lo at the same offsets)
-        const int t = 32 * q + lane;                  // 0..127 within the group
-        const float4* bsrc = reinterpret_cast<const float4*>(sm + pl.b_off(s));
-        float4* bh = reinterpret_cast<float4*>(sm + pl.bhi_off(s));
-        float4* bl = reinterpret_cast<float4*>(sm + pl.blo_off(s));
-        for (int i = t; i < pl.bn * 8; i += 128) {
-          const float4 v = bsrc[i];
-          const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          bh[i] = hv;
-          bl[i] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy smem writes -> tensor core
-      }
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&bs.empty[s]);       // this warp has consumed its reads of the smem stage
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -283,14 +302,17 @@ __device__ double mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CU
       while (s >= pl.stages) { s -= pl.stages; ph ^= 1; }
     }
     // combine the groups' partial sums of row m in fixed order (g = 0 .. NGROUP-1)
-    bs.mean[wi][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
-    double t = 0.0;
 #pragma unroll
-    for (int gg = 0; gg < NGROUP; ++gg) t += bs.mean[4 * gg + (wi & 3)][lane];
-    acc0 = t;
+    for (int t = 0; t < MT; ++t) bs.mean[wi][t][lane] = (acc[t][0] + acc[t][1]) + (acc[t][2] + acc[t][3]);
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
+#pragma unroll
+    for (int t = 0; t < MT; ++t) {
+      double v = 0.0;
+#pragma unroll
+      for (int gg = 0; gg < NGROUP; ++gg) v += bs.mean[4 * gg + (wi & 3)][t][lane];
+      acc0[t] = v;
+    }
   }
-  return acc0;
 }
 
 __device__ void setup_cta(Bars& bs, int stages) {
@@ -320,6 +342,12 @@ __device__ void teardown_cta(Bars& bs) {
   }
 }
 
+// Epilogue column range of splitter group g (bn columns over NGROUP groups, 16-column loads)
+__device__ __forceinline__ void group_cols(int bn, int g, int& c0, int& c1) {
+  const int cpg = ((bn / 16 + NGROUP - 1) / NGROUP) * 16;
+  c0 = g * cpg; c1 = min(bn, (g + 1) * cpg);
+}
+
 // ---------------------------------------------------------------- K1: W partials = Phi P (split-K over D)
 struct PhiPArgs {
   Plan pl;
@@ -330,39 +358,48 @@ struct PhiPArgs {
   int Npad;
 };
 
+template <int MT>
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ CUtensorMap mA,
-                                                        const __grid_constant__ CUtensorMap mB, PhiPArgs a) {
+                                                        const __grid_constant__ CUtensorMap mBh,
+                                                        const __grid_constant__ CUtensorMap mBl, PhiPArgs a) {
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   setup_cta(bs, a.pl.stages);
-  const int row0 = blockIdx.x * BM, split = blockIdx.y;
+  const int row0 = blockIdx.x * BM * MT, split = blockIdx.y;
   const int k0 = split * a.kchunk, k1 = min(a.D, k0 + a.kchunk);
   const int nk = (k1 - k0 + BK - 1) / BK;
-  const double acc0 = mainloop<false>(a.pl, sm, bs, &mA, &mB, row0, k0, nk, a.p0, k1);
+  double acc0[MT];
+  mainloop<false, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, acc0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= 2) {
-    const int q = warp & 3, h = (warp - 2) >> 2, n = row0 + 32 * q + lane;
-    const int cph = ((a.pl.bn / 16 + NGROUP - 1) / NGROUP) * 16;   // accumulator columns per group
+    const int q = warp & 3, g = (warp - 2) >> 2;
+    int c0, c1;
+    group_cols(a.pl.bn, g, c0, c1);
     mbar_wait(&bs.acc_full, 0);
     fence_after();
     const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
     float* wp = a.Wpart + (size_t)split * a.K * a.Npad;
-    for (int c = h * cph; c < min(a.pl.bn, (h + 1) * cph); c += 16) {
-      float v[16];
-      tmem_ld16(la + c, v);
-      if (n < a.N)
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (c + i < a.K) wp[(size_t)(c + i) * a.Npad + n] = v[i];
+    for (int t = 0; t < MT; ++t) {
+      const int n = row0 + BM * t + 32 * q + lane;
+      for (int c = c0; c < c1; c += 16) {
+        float v[16];
+        tmem_ld16(la + TmemPlan<MT>::acc(t) + c, v);
+        if (n < a.N)
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c + i < a.K) wp[(size_t)(c + i) * a.Npad + n] = v[i];
+      }
+      if (g == 0 && n < a.N) a.W0part[(size_t)split * a.Npad + n] = acc0[t];
     }
-    if (h == 0 && n < a.N) a.W0part[(size_t)split * a.Npad + n] = acc0;
   }
   teardown_cta(bs);
 }
 
-// Split-K reduction in fixed order; writes W (for the SIMT fallback check), W_hi, W_lo and w0.
+// Split-K reduction in fixed order -> W_hi, W_lo (3xTF32 halves of W, the B operand of K2) and w0.
 __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* __restrict__ Wpart,
-                              const double* __restrict__ W0part, float* __restrict__ W, double* __restrict__ w0) {
+                              const double* __restrict__ W0part, float* __restrict__ Whi, float* __restrict__ Wlo,
+                              double* __restrict__ w0) {
   const int64_t tot = (int64_t)K * Npad;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot + Npad; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < tot) {
@@ -370,7 +407,8 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
       float v = 0.f;
       if (n < N)
         for (int s = 0; s < splits; ++s) v += Wpart[(int64_t)s * tot + i];
-      W[i] = v;
+      const float h = tf32_hi(v);
+      Whi[i] = h; Wlo[i] = v - h;
     } else {
       const int n = (int)(i - tot);
       double v = 0.0;
@@ -378,6 +416,16 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
         for (int s = 0; s < splits; ++s) v += W0part[(int64_t)s * Npad + n];
       w0[n] = v;
     }
+  }
+}
+
+// P_hi / P_lo of the probe block (B operand of K1), [K][Dp]
+__global__ void k_tc_split_p(int64_t n, const float* __restrict__ P, float* __restrict__ Ph, float* __restrict__ Pl) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(P)[i];
+    const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+    reinterpret_cast<float4*>(Ph)[i] = h;
+    reinterpret_cast<float4*>(Pl)[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
   }
 }
 
@@ -392,53 +440,68 @@ struct PhiTWArgs {
   ColState* cs; double* part; int stride; unsigned* counter; int iter;
 };
 
+template <int MT>
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__ CUtensorMap mA,
-                                                         const __grid_constant__ CUtensorMap mB, PhiTWArgs a) {
+                                                         const __grid_constant__ CUtensorMap mBh,
+                                                         const __grid_constant__ CUtensorMap mBl, PhiTWArgs a) {
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
   setup_cta(bs, a.pl.stages);
-  const int row0 = blockIdx.x * BM;
+  const int row0 = blockIdx.x * BM * MT;
   const int nk = (a.N + BK - 1) / BK;
-  const double acc0 = mainloop<true>(a.pl, sm, bs, &mA, &mB, row0, 0, nk, a.w0, a.N);
+  double acc0[MT];
+  mainloop<true, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.K + 1;
   if (warp >= 2) {
-    const int wi = warp - 2, q = warp & 3, h = wi >> 2, d = row0 + 32 * q + lane;
-    const int cph = ((a.pl.bn / 16 + NGROUP - 1) / NGROUP) * 16;   // accumulator columns per group
-    const bool valid = d < a.D;
-    const double al = valid ? a.alpha[d] : 0.0;
-    if (h == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
-      double g = 0.0;
-      if (valid) {
-        const double p = a.p0[d], qv = a.beta * acc0 + al * p;
-        a.q0[d] = qv;
-        g = p * qv;
+    const int wi = warp - 2, q = warp & 3, g = wi >> 2;
+    int c0, c1;
+    group_cols(a.pl.bn, g, c0, c1);
+    if (g == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
+      double gm = 0.0;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int d = row0 + BM * t + 32 * q + lane;
+        if (d < a.D) {
+          const double p = a.p0[d], qv = a.beta * acc0[t] + a.alpha[d] * p;
+          a.q0[d] = qv;
+          gm += p * qv;
+        }
       }
-      g = warp_sum(g);
-      if (lane == 0) bs.red[wi][0] = g;
+      gm = warp_sum(gm);
+      if (lane == 0) bs.red[wi][0] = gm;
     }
     mbar_wait(&bs.acc_full, 0);
     fence_after();
     const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
-    const float bt = (float)a.beta, alf = (float)al;
-    for (int c = h * cph; c < min(a.pl.bn, (h + 1) * cph); c += 16) {
-      float v[16];
-      tmem_ld16(la + c, v);
+    const float bt = (float)a.beta;
+    for (int c = c0; c < c1; c += 16) {
+      double gk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int k = c + i;
-        if (k < a.K) {                                // warp-uniform
-          double g = 0.0;
-          if (valid) {
+      for (int i = 0; i < 16; ++i) gk[i] = 0.0;
+#pragma unroll
+      for (int t = 0; t < MT; ++t) {
+        const int d = row0 + BM * t + 32 * q + lane;
+        const bool valid = d < a.D;
+        const float alf = valid ? (float)a.alpha[d] : 0.f;
+        float v[16];
+        tmem_ld16(la + TmemPlan<MT>::acc(t) + c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int k = c + i;
+          if (k < a.K && valid) {
             const float p = a.P[(int64_t)k * a.Dp + d];
             const float qv = bt * v[i] + alf * p;     // a3: q = beta Phi^T Phi p + alpha o p
             a.Q[(int64_t)k * a.Dp + d] = qv;
-            g = (double)p * (double)qv;               // a4
+            gk[i] += (double)p * (double)qv;          // a4
           }
-          g = warp_sum(g);
-          if (lane == 0) bs.red[wi][k + 1] = g;
         }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double gg = warp_sum(gk[i]);
+        if (lane == 0 && c + i < a.K) bs.red[wi][c + i + 1] = gg;
       }
     }
   }
@@ -497,11 +560,11 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t ro
          CUDA_SUCCESS;
 }
 
-static Plan plan_for(int bn) {
+static Plan plan_for(int bn, int mt) {
   Plan p;
-  p.bn = bn;
-  p.stage_bytes = BM * BK * 4 + 3 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
-  p.stages = std::min(8, (int)((220 * 1024 - sizeof(Bars)) / p.stage_bytes));
+  p.bn = bn; p.mt = mt;
+  p.stage_bytes = mt * BM * BK * 4 + 2 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
+  p.stages = std::min(8, (int)((226 * 1024 - sizeof(Bars)) / p.stage_bytes));
   return p;
 }
 static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes + sizeof(Bars); }
@@ -509,24 +572,24 @@ static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes +
 }  // namespace tc
 
 struct DenseTC {
-  CUtensorMap phi_k, phi_mn, pmap, wmap;
-  float *W, *Wpart;
+  CUtensorMap phi_k, phi_mn, phh, pll, whh, wll;
+  float *Ph, *Pl, *Wh, *Wl, *Wpart;
   double *W0part, *w0;
-  int bn, splits, kchunk, Npad;
+  int bn, mt, splits, kchunk, Npad;
   tc::Plan pl;
 };
 
 void dense_tc_free(Ctx* c) {
   DenseTC* t = (DenseTC*)c->dense_tc;
   if (!t) return;
-  void* ptrs[] = {t->W, t->Wpart, t->W0part, t->w0};
+  void* ptrs[] = {t->Ph, t->Pl, t->Wh, t->Wl, t->Wpart, t->W0part, t->w0};
   for (void* p : ptrs) if (p) cudaFree(p);
   delete t;
   c->dense_tc = nullptr;
 }
 
-// Set up the tensor-core path (fp32 probes only).  Returns false (SIMT path stays) when
-// the shape cannot use it; errors in allocation are reported.
+// Set up the tensor-core path (fp32 probes only); leaves c->dense_tc NULL (SIMT path) when
+// the shape cannot use it.
 cofem_status dense_tc_setup(Ctx* c) {
   using namespace tc;
   if (c->probe64 || getenv("COFEM_DENSE_SIMT")) return COFEM_OK;    // env: test hook for the SIMT path
@@ -536,28 +599,43 @@ cofem_status dense_tc_setup(Ctx* c) {
   memset(t, 0, sizeof *t);
   c->dense_tc = t;
   t->bn = std::max(16, (c->Kcap + 15) / 16 * 16);
-  t->pl = plan_for(t->bn);
+  // 256-row CTAs share each B tile when K <= 64 and the K2 grid still fills the SMs
+  t->mt = (t->bn <= 64 && (c->D + 2 * BM - 1) / (2 * BM) >= c->num_sms / 2) ? 2 : 1;
+  t->pl = plan_for(t->bn, t->mt);
   t->Npad = (int)((c->N + 31) / 32 * 32);
-  const int mt = (int)((c->N + BM - 1) / BM);
-  // split-K so that the K1 grid covers the SMs about four times (>= 8 K steps per split)
+  const int rows = BM * t->mt;
+  const int mtiles = (int)((c->N + rows - 1) / rows);
+  // split-K: the K1 grid (one CTA per SM) is sized to just fill whole waves (>= 8 K steps per split)
   const int ksteps = (int)((c->D + BK - 1) / BK);
-  int splits = std::max(1, std::min(ksteps / 8, (4 * c->num_sms + mt - 1) / mt));
+  int splits = 1;
+  for (int w = 2; w <= 8; ++w) {
+    const int sp = std::max(1, std::min(ksteps / 8, (w * c->num_sms) / mtiles));
+    if (sp * mtiles >= (w * c->num_sms * 7) / 8) { splits = sp; break; }
+    splits = sp;
+  }
   t->kchunk = ((ksteps + splits - 1) / splits) * BK;
   t->splits = (int)((c->D + t->kchunk - 1) / t->kchunk);
-  const size_t wk = (size_t)c->Kcap * t->Npad;
-  if (cudaMalloc(&t->W, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
+  const size_t pk = (size_t)c->Kcap * c->Dp, wk = (size_t)c->Kcap * t->Npad;
+  if (cudaMalloc(&t->Ph, pk * 4) || cudaMalloc(&t->Pl, pk * 4) || cudaMalloc(&t->Wh, wk * 4) ||
+      cudaMalloc(&t->Wl, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
       cudaMalloc(&t->W0part, (size_t)t->splits * t->Npad * 8) || cudaMalloc(&t->w0, (size_t)t->Npad * 8)) {
     c->err = "cudaMalloc dense tensor-core workspace"; return COFEM_ERR_OOM;
   }
-  cudaMemset(t->W, 0, wk * 4);
-  bool ok = make_map(&t->phi_k, c->phi, c->D, c->N, c->ld, BK, BM) &&       // K1 A: Phi[n][d], box 32 d x 128 n
-            make_map(&t->phi_mn, c->phi, c->D, c->N, c->ld, BM, BK, false) &&   // K2 A: box 128 d x 32 n, dense
-            make_map(&t->pmap, (const float*)c->P, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&   // K1 B: P [K][Dp]
-            make_map(&t->wmap, t->W, t->Npad, c->Kcap, t->Npad, BK, t->bn);                // K2 B: W [K][Npad]
+  cudaMemset(t->Ph, 0, pk * 4); cudaMemset(t->Pl, 0, pk * 4);
+  cudaMemset(t->Wh, 0, wk * 4); cudaMemset(t->Wl, 0, wk * 4);
+  cudaMemset(t->w0, 0, (size_t)t->Npad * 8);
+  bool ok = make_map(&t->phi_k, c->phi, c->D, c->N, c->ld, BK, BM) &&            // K1 A: Phi[n][d], box 32 d x 128 n
+            make_map(&t->phi_mn, c->phi, c->D, c->N, c->ld, BM, BK, false) &&    // K2 A: box 128 d x 32 n, dense
+            make_map(&t->phh, t->Ph, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&        // K1 B: P_hi, P_lo [K][Dp]
+            make_map(&t->pll, t->Pl, c->Dp, c->Kcap, c->Dp, BK, t->bn) &&
+            make_map(&t->whh, t->Wh, t->Npad, c->Kcap, t->Npad, BK, t->bn) &&    // K2 B: W_hi, W_lo [K][Npad]
+            make_map(&t->wll, t->Wl, t->Npad, c->Kcap, t->Npad, BK, t->bn);
   if (!ok) { c->err = "cuTensorMapEncodeTiled failed"; return COFEM_ERR_CUDA; }
   const int sm = (int)smem_of(t->pl);
-  cudaFuncSetAttribute(k_tc_phiP, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiTW, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiP<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiP<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiTW<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiTW<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
   return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
@@ -567,13 +645,17 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   DenseTC* t = (DenseTC*)c->dense_tc;
   const int K = m - 1;
   const size_t sm = smem_of(t->pl);
+  const int rows = BM * t->mt;
   launch_begin(c, KC_DENSE_PHI_P);
+  k_tc_split_p<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * c->Dp, (const float*)c->P, t->Ph, t->Pl);
   PhiPArgs a1;
   a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
   a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
-  k_tc_phiP<<<dim3((unsigned)((c->N + BM - 1) / BM), t->splits), THREADS, sm, c->stream>>>(t->phi_k, t->pmap, a1);
-  k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->W,
-                                                       t->w0);
+  const dim3 g1((unsigned)((c->N + rows - 1) / rows), t->splits);
+  if (t->mt == 2) k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  else k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
+                                                       t->Wl, t->w0);
   launch_end(c, KC_DENSE_PHI_P);
   if (check_launch(c, "k_tc_phiP")) return COFEM_ERR_CUDA;
   PhiTWArgs a2;
@@ -581,7 +663,9 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   a2.alpha = c->alpha; a2.w0 = t->w0; a2.p0 = c->p0; a2.q0 = c->q0; a2.P = (const float*)c->P; a2.Q = (float*)c->Q;
   a2.cs = c->cs; a2.part = c->part; a2.stride = c->part_stride; a2.counter = c->counters + MAXM; a2.iter = iter;
   launch_begin(c, KC_DENSE_PHIT_W);
-  k_tc_phiTW<<<(unsigned)((c->D + BM - 1) / BM), THREADS, sm, c->stream>>>(t->phi_mn, t->wmap, a2);
+  const unsigned g2 = (unsigned)((c->D + rows - 1) / rows);
+  if (t->mt == 2) k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  else k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
   return COFEM_OK;

@@ -264,3 +264,16 @@ def test_c4_fast_path_em_two_iterations():
     oa, omu, os_ = cofem_em(op_of(w), w.y, w.beta, 2, 3, 9, 6)
     assert rel(1 / a, 1 / oa) <= 1e-5 and rel(mu, omu) <= 1e-5 and rel(s, os_) <= 1e-4, \
         (rel(1 / a, 1 / oa), rel(mu, omu), rel(s, os_))
+
+
+def test_c2_full_size_tensor_core_path():
+    """Config 2 shape (2000 x 8000 dense, fp32 Phi): the tcgen05 3xTF32 apply (op_dense_tc.cu,
+    256-row CTAs, split-K) against the fp64 oracle, E-step 1 and two EM iterations."""
+    w = synth.preset("C2")
+    ctx = ctx_of(w, cg_iters=40, max_probes=8)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), 8, 4, 0)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), 8, 4, 0, 40)
+    assert rel(mu, omu) <= 1e-4 and rel(s, os_) <= 1e-4, (rel(mu, omu), rel(s, os_))
+    a, mu, s = gpu_em(ctx, w, 2, 8, 6)
+    oa, omu, _ = cofem_em(op_of(w), w.y, w.beta, 2, 8, 6, 40)
+    assert rel(1 / a, 1 / oa) <= 1e-3 and rel(mu, omu) <= 1e-3, (rel(1 / a, 1 / oa), rel(mu, omu))
