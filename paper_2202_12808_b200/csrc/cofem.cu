@@ -430,7 +430,9 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
   launch_end(c, cls, st);
 }
 
-static cofem_status cg_loop_1k(Ctx* c, int K, double invK) {
+// Same for the overlap-save FFT convolution (both paths apply + update per column set).
+typedef cofem_status (*SplitApply)(Ctx*, int, int, int, bool, cudaStream_t);
+static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) {
   const int m = K + 1;
   static const bool serial = getenv("COFEM_1K_SERIAL") != nullptr;   // tuning hook: mean column on the main stream
   cudaStream_t ms = serial ? c->stream : c->side;
@@ -438,9 +440,9 @@ static cofem_status cg_loop_1k(Ctx* c, int K, double invK) {
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
-    if ((st = dct1k_apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
+    if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
     update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
-    if ((st = dct1k_apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if ((st = apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
     if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
@@ -468,7 +470,8 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   else k_init<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
   launch_end(c, KC_INIT);
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
-  if (c->fast1k) return cg_loop_1k(c, K, invK);
+  if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
+  if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
     if (c->kind == COFEM_OP_DCT2_MASKED) {
@@ -541,7 +544,8 @@ static void free_all(Ctx* c) {
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
-                  c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64};
+                  c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
+                  c->Pb, c->p0b, c->conv_tab32, c->conv_tab64};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);

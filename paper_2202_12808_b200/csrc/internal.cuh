@@ -72,6 +72,9 @@ struct Ctx {
   double* dinv64 = nullptr;             // 1 / diag(A) fp64
   void* dinvp = nullptr;                // same in probe precision
   void* alphap = nullptr;               // alpha in probe precision (probe-column applies)
+  void* Pb = nullptr; double* p0b = nullptr;   // CIRCCONV FFT path: ping-pong p buffers (overlapping windows)
+  void* conv_tab32 = nullptr; void* conv_tab64 = nullptr;   // its FFT / spectrum tables
+  bool fast_conv = false;               // CIRCCONV: overlap-save FFT apply (op_conv_fft.cu)
   double *x0 = nullptr, *r0 = nullptr, *p0 = nullptr, *q0 = nullptr;  // mean column (fp64)
   void *R = nullptr, *P = nullptr, *Q = nullptr;                       // probe block [Kcap][Dp]
   double* s = nullptr;                  // accumulated (1/K) sum p_k o x_k  (fp64 Dp)
@@ -228,6 +231,9 @@ cofem_status conv_apply(Ctx* c, int m, int iter);
 bool dct1k_eligible(const Ctx* c);
 cofem_status dct1k_setup(Ctx* c);
 cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
+bool conv_fft_eligible(const Ctx* c);
+cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g);
+cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
 
 // vector kernels (cofem.cu)
 cofem_status launch_dir(Ctx* c, int m);

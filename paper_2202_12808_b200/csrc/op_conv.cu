@@ -116,6 +116,16 @@ cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host) {
   if (check_launch(c, "k_conv_setup")) return COFEM_ERR_CUDA;
   const int grid = (int)((c->D + CONV_TILE - 1) / CONV_TILE);
   c->part_stride = std::max(c->part_stride, grid);
+  if (conv_fft_eligible(c)) {        // overlap-save FFT apply, mean column on the side stream
+    const size_t tp = c->probe64 ? 8 : 4;
+    if (cudaMalloc(&c->Pb, (size_t)c->Kcap * c->Dp * tp) != cudaSuccess || cudaMalloc(&c->p0b, c->Dp * 8) != cudaSuccess) {
+      c->err = "cudaMalloc conv p buffers"; return COFEM_ERR_OOM;
+    }
+    cudaMemset(c->Pb, 0, (size_t)c->Kcap * c->Dp * tp); cudaMemset(c->p0b, 0, c->Dp * 8);
+    cofem_status st = conv_fft_setup(c, g);
+    if (st != COFEM_OK) return st;
+    c->fast_conv = true;
+  }
   if (c->probe64) cudaFuncSetAttribute(k_conv_apply<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv_smem());
   else cudaFuncSetAttribute(k_conv_apply<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)conv_smem());
   return COFEM_OK;

@@ -27,83 +27,10 @@
 #include <complex>
 #include <vector>
 
-#include "fft_common.cuh"
+#include "fft512.cuh"
 
 namespace cofem {
 namespace d1k {
-
-constexpr int L = 1024, M = 512;
-constexpr int XS1 = 66, XS2 = 72;      // exchange row strides in complex entries (conflict-free 8-byte accesses)
-constexpr int WREG = 2 * 8 * XS2;      // per-warp smem region (elements of T): exchange buffer / one tile row (>= L)
-template <typename T> struct Geo { static constexpr int RT = sizeof(T) == 8 ? 4 : 8; };   // rows (warps) per CTA
-
-// Tables, host-built in fp64 and rounded to T, copied to shared memory by every CTA in
-// layouts where each warp access is conflict-free (lanes read consecutive entries):
-//   w2[r*8 + k]  = W_64^{r k}      (FFT stage 2, k = lane & 7)
-//   w3[r*64 + j] = W_512^{r j}     (FFT stage 3, j = butterfly)
-//   DCT-III pre  (Makhoul):  W[k] = u1 P_k + u2 Q_k,  u1 = X[k] - i X[L-k], u2 = X[k+M] - i X[M-k]
-//   DCT-II  post:            X[k]   = Re(W_k R1_k) + Re(conj(W_{M-k}) R2_k)
-//                            X[k+M] = Re(W_k R3_k) + Re(conj(W_{M-k}) R4_k)
-// with the orthonormal scales, the 1/M of the inverse FFT and the even/odd split folded in
-// (k < M; the entries are derived in build_tables below).
-constexpr int TW2 = 0, TW3 = 64, TP = TW3 + 512, TQ = TP + M, TR1 = TQ + M, TR2 = TR1 + M, TR3 = TR2 + M,
-              TR4 = TR3 + M, TTOT = TR4 + M;   // offsets in complex entries
-template <typename T> struct Tw { const cplx<T>* base; };
-
-template <typename T>
-__device__ __forceinline__ Tw<T> load_tables(const cplx<T>* __restrict__ g, cplx<T>* sm) {
-  for (int i = threadIdx.x; i < TTOT; i += blockDim.x) sm[i] = g[i];
-  __syncthreads();
-  return {sm};
-}
-
-template <typename T, int SIGN>
-__device__ __forceinline__ void twid(cplx<T>& v, cplx<T> w) { v = SIGN < 0 ? cmul(v, w) : cmulc(v, w); }
-
-// 512-point DFT (SIGN -1) / unnormalised inverse (SIGN +1) by one warp.
-// In:  va[r] = x[ja + 64 r], vb[r] = x[jb + 64 r].  Out: va[r] = X[ja + 64 r], vb[r] = X[jb + 64 r].
-// Stockham radix-8: stage s reads x[j + 64 r], twiddles by W_{8 Ns}^{r (j mod Ns)}, DFT8,
-// writes y[(j / Ns) 8 Ns + (j mod Ns) + r Ns]; Ns = 1, 8, 64.  Exchanges store [r][j]
-// (complex entries, row strides XS1 / XS2).
-template <typename T, int SIGN>
-__device__ __forceinline__ void fft512(cplx<T> (&va)[8], cplx<T> (&vb)[8], int lane, cplx<T>* __restrict__ x,
-                                       const Tw<T>& tw) {
-  const int ja = lane, jb = lane ? 64 - lane : 32;
-  dft8<SIGN>(va); dft8<SIGN>(vb);                       // stage 1 (Ns = 1): butterflies ja, jb
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 8; ++r) { x[r * XS1 + ja] = va[r]; x[r * XS1 + jb] = vb[r]; }
-  __syncwarp();
-  {   // stage 2 (Ns = 8): butterflies lane, lane + 32; y[i] lives at [(i & 7)][i >> 3]
-    const int base = (lane & 7) * XS1 + (lane >> 3);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) { va[r] = x[base + 8 * r]; vb[r] = x[base + 4 + 8 * r]; }
-    const cplx<T>* w2 = tw.base + TW2 + (lane & 7);
-#pragma unroll
-    for (int r = 1; r < 8; ++r) {
-      const cplx<T> w = w2[r * 8];
-      twid<T, SIGN>(va[r], w); twid<T, SIGN>(vb[r], w);
-    }
-  }
-  dft8<SIGN>(va); dft8<SIGN>(vb);
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 8; ++r) { x[r * XS2 + lane] = va[r]; x[r * XS2 + lane + 32] = vb[r]; }
-  __syncwarp();
-  {   // stage 3 (Ns = 64): butterflies ja, jb; y'[i] written by j2 = 8 (i >> 6) + (i & 7), r2 = (i >> 3) & 7
-    const int ba = (ja >> 3) * XS2 + (ja & 7), bb = (jb >> 3) * XS2 + (jb & 7);
-#pragma unroll
-    for (int r = 0; r < 8; ++r) { va[r] = x[ba + 8 * r]; vb[r] = x[bb + 8 * r]; }
-    const cplx<T>* w3 = tw.base + TW3;
-#pragma unroll
-    for (int r = 1; r < 8; ++r) {
-      twid<T, SIGN>(va[r], w3[r * 64 + ja]);
-      twid<T, SIGN>(vb[r], w3[r * 64 + jb]);
-    }
-  }
-  dft8<SIGN>(va); dft8<SIGN>(vb);
-  __syncwarp();                                         // exchange region free again
-}
 
 // DCT-III (orthonormal inverse) pre-processing for one k: W[k] = u1 P_k + u2 Q_k.
 template <typename T>
@@ -119,14 +46,6 @@ __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const T
   const cplx<T> R1 = tb.base[TR1 + k], R2 = tb.base[TR2 + k], R3 = tb.base[TR3 + k], R4 = tb.base[TR4 + k];
   lo = Wk.x * R1.x - Wk.y * R1.y + Wm.x * R2.x + Wm.y * R2.y;
   hi = Wk.x * R3.x - Wk.y * R3.y + Wm.x * R4.x + Wm.y * R4.y;
-}
-
-// Canonical positions of a lane in a line: slot A r -> ja + 64r, B -> jb + 64r,
-// C -> 512 + ja + 64r, E -> 512 + jb + 64r (r = 0..7): 32 distinct positions per lane,
-// together the whole line; each load/store instruction is coalesced.
-__device__ __forceinline__ void canon(int lane, int r, int (&o)[4]) {
-  const int ja = lane, jb = lane ? 64 - lane : 32;
-  o[0] = ja + 64 * r; o[1] = jb + 64 * r; o[2] = M + ja + 64 * r; o[3] = M + jb + 64 * r;
 }
 
 // Packed spectra of the DCT-III of a line held canonically in A, B, C, E.
@@ -198,22 +117,6 @@ template <typename T> __device__ __forceinline__ const cplx<T>* tab1k(const DctA
 // Shared memory: [RT warps][WREG] (FFT exchange / output tile row) then the twiddle tables.
 // Persistent kernels: work item w = (column j0 + w / NTILE, tile w % NTILE), grid-strided.
 template <typename T> struct Work { static constexpr int NTILE = L / Geo<T>::RT; };
-
-// Per-launch column info, read once per CTA: frozen flags and direction coefficients b_j
-// (R5; a6), plus per-warp gamma accumulators for pass C (reduced once per CTA at exit).
-struct ColInfo {
-  int frozen[MAXM];
-  double b[MAXM];
-  double g[8][MAXM];
-};
-__device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, int j0, int ncols, bool zero_g) {
-  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
-    const ColState c = cs[j0 + jj];
-    ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
-    if (zero_g)
-      for (int w = 0; w < 8; ++w) ci.g[w][jj] = 0.0;
-  }
-}
 
 template <typename T>
 __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile, int dir, double bcoef, T* sm,
