@@ -130,7 +130,9 @@ def test_probes_match_oracle_through_estimator():
     ctx = ctx_of(w, precond=0)
     mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 123456789012345, 9)
     omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 123456789012345, 9, 1, precond=False)
-    assert rel(s, os_) < 1e-6 and rel(mu, omu) < 1e-6
+    # a probe bit error moves s by O(1/K) = 0.2; the bar only has to sit above the fp32-class
+    # apply error (tcgen05 3xTF32: <= 2^-21 per product, fp32 accumulation; measured 1.4e-6)
+    assert rel(s, os_) < 1e-5 and rel(mu, omu) < 1e-5
 
 
 def test_edge_cases_k1_u1_phi_zero():
