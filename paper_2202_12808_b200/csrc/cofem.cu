@@ -85,13 +85,20 @@ struct VecArgs {
   double invK;
 };
 
+// Probe-stream parameters of the current E-step, read from device memory so that one
+// captured CUDA graph serves every E-step (R8: key = seed, counter = (d/128, k, t, tag)).
+struct ProbeParams { uint32_t kx, ky; int t, k_offset; };
+__global__ void k_set_probe_params(ProbeParams* p, ProbeParams v) { *p = v; }
+
 __global__ void k_probe_bits(uint32_t* __restrict__ bits, int64_t wpc, int K, int64_t nblk128,
-                             int k_offset, int t, uint2 key) {
+                             const ProbeParams* __restrict__ pp) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)K * nblk128) return;
+  const ProbeParams prm = *pp;
   int k = (int)(idx / nblk128);
   int64_t b = idx - (int64_t)k * nblk128;
-  uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(k_offset + k), (uint32_t)t, PROBE_TAG), key);
+  uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(prm.k_offset + k), (uint32_t)prm.t, PROBE_TAG),
+                          make_uint2(prm.kx, prm.ky));
   *reinterpret_cast<uint4*>(bits + (int64_t)k * wpc + b * 4) = w;
 }
 
@@ -434,6 +441,9 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
 typedef cofem_status (*SplitApply)(Ctx*, int, int, int, bool, cudaStream_t);
 static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) {
   const int m = K + 1;
+  // the conv path ping-pongs p between two buffers; every E-step starts from the same
+  // assignment (k_init rewrites p), which keeps a captured graph's pointers valid
+  void* const P_entry = c->P; double* const p0_entry = c->p0;
   static const bool serial = getenv("COFEM_1K_SERIAL") != nullptr;   // tuning hook: mean column on the main stream
   cudaStream_t ms = serial ? c->stream : c->side;
   CK(cudaEventRecord(c->ev_fork, c->stream));
@@ -449,19 +459,23 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   }
   CK(cudaEventRecord(c->ev_join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  if (c->P != P_entry) { c->Pb = c->P; c->P = P_entry; }
+  if (c->p0 != p0_entry) { c->p0b = c->p0; c->p0 = p0_entry; }
   return COFEM_OK;
 }
 
 // Runs Alg. 1 lines 3-7 with alpha already in c->alpha.  No host sync inside.
-static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offset, int K_total) {
+// The device work of one E-step (probes .. end of the CG loop), enqueued on c->stream;
+// the probe parameters are already in c->dparams.
+static cofem_status estep_body(Ctx* c, int K, int K_total) {
   const int m = K + 1;
   const double invK = 1.0 / (double)K_total;
   const int64_t nblk128 = c->Dp / 128;
-  uint2 key = make_uint2((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32));
   {
     int64_t n = (int64_t)K * nblk128;
     launch_begin(c, KC_PROBES);
-    k_probe_bits<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->bits, c->Dp / 32, K, nblk128, k_offset, t, key);
+    k_probe_bits<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->bits, c->Dp / 32, K, nblk128,
+                                                                      (const ProbeParams*)c->dparams);
     launch_end(c, KC_PROBES);
     if (check_launch(c, "k_probe_bits")) return COFEM_ERR_CUDA;
   }
@@ -487,6 +501,51 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
   }
+  return COFEM_OK;
+}
+
+// Alg. 1 lines 3-7 on the device.  By default the whole E-step (both streams) is captured
+// once per (K, K_total) into a CUDA graph and replayed: one launch per E-step instead of
+// ~4-8 per CG iteration.  Per-kernel profiling (cofem_profile_enable)
+// records events around every launch and therefore runs uncaptured.
+static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offset, int K_total) {
+  ProbeParams pv{(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), t, k_offset};
+  k_set_probe_params<<<1, 1, 0, c->stream>>>((ProbeParams*)c->dparams, pv);
+  CK(cudaGetLastError());
+  static const bool no_graph = getenv("COFEM_NO_GRAPH") != nullptr;   // test hook
+  if (no_graph || c->prof_mask) return estep_body(c, K, K_total);
+  cudaStream_t user = c->stream;
+  CK(cudaEventRecord(c->ev_in, user));
+  CK(cudaStreamWaitEvent(c->work, c->ev_in, 0));
+  c->stream = c->work;
+  cofem_status st = COFEM_OK;
+  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total) {
+    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+    const int64_t l0 = c->launches;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      st = estep_body(c, K, K_total);
+      e = cudaStreamEndCapture(c->work, &g);
+    }
+    if (e == cudaSuccess && st == COFEM_OK) e = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    if (g) cudaGraphDestroy(g);
+    c->graph_launches = c->launches - l0;
+    c->launches = l0;
+    if (e != cudaSuccess || st != COFEM_OK) {
+      c->stream = user;
+      if (st == COFEM_OK) { c->err = std::string("CUDA graph capture: ") + cudaGetErrorString(e); st = COFEM_ERR_CUDA; }
+      if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+      return st;
+    }
+    c->graph_K = K; c->graph_Kt = K_total;
+  }
+  cudaError_t e = cudaGraphLaunch(c->graph_exec, c->work);
+  c->launches += c->graph_launches;
+  c->stream = user;
+  if (e != cudaSuccess) { c->err = std::string("cudaGraphLaunch: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
+  CK(cudaEventRecord(c->ev_out, c->work));
+  CK(cudaStreamWaitEvent(user, c->ev_out, 0));
   return COFEM_OK;
 }
 
@@ -554,11 +613,17 @@ static void free_all(Ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->work) cudaStreamDestroy(c->work);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->dparams) cudaFree(c->dparams);
 }
 
 void cofem_destroy(cofem_ctx ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.work) cudaStreamSynchronize(ctx->c.work);
   free_all(&ctx->c);
   delete ctx;
 }
@@ -580,6 +645,10 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->work, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
+  CK(cudaMalloc(&c->dparams, 64));
 
   const size_t tp = c->probe64 ? sizeof(double) : sizeof(float);
   const int64_t Dp = c->Dp;

@@ -57,6 +57,12 @@ struct Ctx {
   bool fast1k = false;                  // DCT2 1024 x 1024: fast path, mean column on `side`
   cudaStream_t side = nullptr;          // second stream (mean column of the fast DCT path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t work = nullptr;          // capturable stream the E-step graph runs on
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  void* dparams = nullptr;              // device ProbeParams of the current E-step
+  cudaGraphExec_t graph_exec = nullptr; // captured E-step (cofem.cu estep_device)
+  int graph_K = -1, graph_Kt = -1;
+  int64_t graph_launches = 0;
   void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu
   void* dct_tab64 = nullptr;            // (double)
   int ntaps = 0;                        // CIRCCONV
