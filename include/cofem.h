@@ -111,6 +111,18 @@ cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* 
 cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
                          int32_t k_offset, int32_t K_total, double* mu, double* s);
 
+/* One batched Gram apply (the CG matrix-matrix product of §3.2; Eq. 7):
+ *   q0 = A x0,  Q_k = A X_k  (k < K),   A = beta Phi^T Phi + diag(alpha),
+ * through exactly the kernels the E-step uses (mean column in fp64; probe columns in
+ * probe precision: fp32, or fp64 with probe_precision = 1), plus gamma_j = x_j^T (A x_j).
+ *   alpha:  D fp64 (> 0, finite)          x0, q0: D fp64 (mean column)
+ *   X, Q:   K x D, row k = column k + 1 of the block, contiguous (row stride D), float
+ *           (probe_precision 0) or double (1)
+ *   gamma:  K + 1 fp64 out (column 0 first), may be NULL
+ * Host or device pointers; 1 <= K <= max_probes.  Errors: COFEM_ERR_INVALID. */
+cofem_status cofem_apply(cofem_ctx ctx, const double* alpha, int32_t K, const double* x0, const void* X,
+                         double* q0, void* Q, double* gamma);
+
 /* M-step (Eq. 8): alpha_out_d = min(1 / max(mu_d^2 + s_d, den_floor), alpha_max). Never fails. */
 cofem_status cofem_mstep(cofem_ctx ctx, const double* mu, const double* s, double* alpha_out);
 

@@ -59,6 +59,8 @@ SYMBOLS = [
                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                    ctypes.c_void_p]),
     ("cofem_mstep", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("cofem_apply", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_em", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_last_report", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_Report)]),
@@ -147,6 +149,7 @@ class Context:
             int(probe_precision), int(max_probes)
         opt.den_floor, opt.alpha_max = float(den_floor), float(alpha_max)
         self.U, self.K_max = int(cg_iters), int(max_probes)
+        self.probe_precision = int(probe_precision)
         h = ctypes.c_void_p()
         st = L.cofem_setup(ctypes.byref(h), ctypes.byref(op), _ptr(y, np.float32, self.N, "y"), float(beta),
                            ctypes.byref(opt), ctypes.c_void_p(stream) if stream else None)
@@ -178,6 +181,16 @@ class Context:
         self._check(lib().cofem_estep(self._h, _ptr(alpha, np.float64, D, "alpha"), int(K), int(seed), int(t),
                                       int(k_offset), int(K if K_total is None else K_total),
                                       _ptr(mu, np.float64, D, "mu"), _ptr(s, np.float64, D, "s")))
+
+    def apply(self, alpha, x0, X, q0, Q, gamma=None):
+        """One Gram apply q0 = A x0, Q_k = A X_k (A = beta Phi^T Phi + diag alpha, Eq. 7) through the
+        E-step's kernels; X, Q: K x D in probe precision (float32, or float64 with probe_precision=1)."""
+        D = self.D
+        K = int(X.shape[0])
+        pdt = np.float64 if self.probe_precision else np.float32
+        self._check(lib().cofem_apply(self._h, _ptr(alpha, np.float64, D, "alpha"), K, _ptr(x0, np.float64, D, "x0"),
+                                      _ptr(X, pdt, K * D, "X"), _ptr(q0, np.float64, D, "q0"),
+                                      _ptr(Q, pdt, K * D, "Q"), _ptr(gamma, np.float64, K + 1, "gamma")))
 
     def mstep(self, mu, s, alpha_out):
         """M-step, Eq. 8."""

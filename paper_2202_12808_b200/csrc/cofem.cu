@@ -788,6 +788,70 @@ cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t
   return estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, mu, s);
 }
 
+__global__ void k_apply_prep(int64_t D, int64_t Dp, double beta, int precond, const double* __restrict__ alpha,
+                             const double* __restrict__ colsq, double* __restrict__ dinv64, void* dinvp,
+                             void* alphap, int probe64) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < Dp; d += (int64_t)gridDim.x * blockDim.x) {
+    const bool v = d < D;
+    const double al = v ? alpha[d] : 0.0, dv = v ? (precond ? 1.0 / (beta * colsq[d] + al) : 1.0) : 0.0;
+    dinv64[d] = dv;
+    if (probe64) { ((double*)dinvp)[d] = dv; ((double*)alphap)[d] = al; }
+    else { ((float*)dinvp)[d] = (float)dv; ((float*)alphap)[d] = (float)al; }
+  }
+}
+__global__ void k_reset_cols(ColState* cs, int m) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  ColState c; c.rho = 1.0; c.rho0 = 1.0; c.gamma = 0; c.a = 0; c.b = 0;
+  c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+  cs[j] = c;
+}
+
+static cofem_status apply_impl(Ctx* c, const double* alpha, int32_t K, const double* x0, const void* X, double* q0,
+                               void* Q, double* gamma) {
+  if (!alpha || !x0 || !X || !q0 || !Q) { c->err = "null argument"; return COFEM_ERR_INVALID; }
+  if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes]"; return COFEM_ERR_INVALID; }
+  const size_t tp = c->probe64 ? 8 : 4;
+  const int m = K + 1;
+  cofem_status st;
+  const double* a_dev;
+  if ((st = stage_in(c, alpha, c->alpha, &a_dev))) return st;
+  if (a_dev != c->alpha) CK(cudaMemcpyAsync(c->alpha, a_dev, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if ((st = validate_alpha(c, c->alpha))) return st;
+  k_apply_prep<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, c->Dp, c->beta, c->opt.precond, c->alpha, c->colsq,
+                                                       c->dinv64, c->dinvp, c->alphap, c->probe64 ? 1 : 0);
+  k_reset_cols<<<1, 256, 0, c->stream>>>(c->cs, m);
+  CK(cudaMemcpyAsync(c->p0, x0, c->D * 8, cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpy2DAsync(c->P, c->Dp * tp, X, c->D * tp, c->D * tp, K, cudaMemcpyDefault, c->stream));
+  CK(cudaGetLastError());
+  if (c->fast1k || c->fast_conv) {
+    SplitApply apply = c->fast1k ? dct1k_apply : conv_fft_apply;
+    if ((st = apply(c, 0, 1, 0, false, c->stream)) != COFEM_OK) return st;
+    if ((st = apply(c, 1, m, 0, false, c->stream)) != COFEM_OK) return st;
+  } else if (c->kind == COFEM_OP_DCT2_MASKED) {
+    if ((st = dct_apply(c, m, 0, false)) != COFEM_OK) return st;
+  } else if (c->kind == COFEM_OP_DENSE) {
+    if ((st = dense_apply(c, m, 0)) != COFEM_OK) return st;
+  } else {
+    if ((st = conv_apply(c, m, 0)) != COFEM_OK) return st;
+  }
+  CK(cudaMemcpyAsync(q0, c->q0, c->D * 8, cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpy2DAsync(Q, c->D * tp, c->Q, c->Dp * tp, c->D * tp, K, cudaMemcpyDefault, c->stream));
+  c->cs_host.resize(m);
+  CK(cudaMemcpyAsync(c->cs_host.data(), c->cs, m * sizeof(ColState), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (gamma)
+    for (int j = 0; j < m; ++j) gamma[j] = c->cs_host[j].gamma;
+  return COFEM_OK;
+}
+
+cofem_status cofem_apply(cofem_ctx ctx, const double* alpha, int32_t K, const double* x0, const void* X, double* q0,
+                         void* Q, double* gamma) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  ctx->c.err.clear();
+  return apply_impl(&ctx->c, alpha, K, x0, X, q0, Q, gamma);
+}
+
 cofem_status cofem_mstep(cofem_ctx ctx, const double* mu, const double* s, double* alpha_out) {
   if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
   Ctx* c = &ctx->c;

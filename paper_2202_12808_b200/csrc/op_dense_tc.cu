@@ -36,12 +36,18 @@ namespace cofem {
 namespace tc {
 
 constexpr int BM = 128, BK = 32;
-constexpr int NGROUP = 3;                  // splitter groups: group g handles K steps kt = g (mod NGROUP)
+constexpr int NGROUP = 4;                  // splitter groups: group g handles K steps kt = g (mod NGROUP)
 constexpr int NSPLIT = 4 * NGROUP;         // splitter warps (one per TMEM lane quarter per group)
 constexpr int THREADS = 64 + 32 * NSPLIT;  // warps 0-1 + splitters
-constexpr int NAB = 6;                     // TMEM A buffers (hi 32 | lo 32 columns each)
-constexpr int TMEM_COLS = 512;             // [0, BN) accumulator; [128, 128 + 64 NAB) A buffers (1 CTA / SM)
-constexpr int TM_A = 128;
+constexpr int NAB = 4;                     // TMEM A buffers (hi 32 | lo 32 columns each) over all M-tiles
+constexpr int TMEM_COLS = 512;             // [0, 256) two accumulator buffers; [256, 512) A buffers (1 CTA / SM)
+constexpr int TM_A = 256;
+// The tensor core's fp32 accumulation rounds toward zero, so its error grows linearly with the
+// number of accumulated MMAs (measured: 3xTF32 apply error 6e-5 at N = 8192 with one TMEM
+// accumulator, tools/tc_error_probe.py).  The accumulator is therefore promoted every CH K steps
+// (K = 64) into round-to-nearest fp32 register sums held by the splitter warps, with two TMEM
+// accumulator buffers so the MMAs of the next chunk overlap the promotion.
+constexpr int CH = 2;
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -55,7 +61,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
 }
-// Bounded wait: a protocol error traps (reported as a CUDA error) instead of hanging the GPU.
+// Bounded wait: a protocol error records (block, warp, barrier offset, parity) in
+// g_tc_stuck and ends the thread instead of hanging the GPU (the host reports it as
+// COFEM_ERR_CUDA with the record).
+__device__ unsigned long long g_tc_stuck[4];
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   for (long long spin = 0;; ++spin) {
     uint32_t done;
@@ -65,7 +74,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(su32(b)), "r"(parity)
         : "memory");
     if (done) return;
-    if (spin > (1ll << 28)) __trap();
+    if (spin > (1ll << 24)) {
+      if (atomicCAS(&g_tc_stuck[0], 0ull, 1ull) == 0ull) {
+        g_tc_stuck[1] = ((unsigned long long)blockIdx.x << 32) | (blockIdx.y << 16) | (threadIdx.x >> 5);
+        g_tc_stuck[2] = ((unsigned long long)(su32(b) & 0xFFFF) << 32) | parity;
+      }
+      asm volatile("exit;");
+    }
   }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -113,6 +128,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "f"(v[0]),
+               "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
@@ -140,7 +160,12 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int bn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__device__ __forceinline__ float tf32_hi(float x) { return __int_as_float(__float_as_int(x) & 0xFFFFE000); }
+// hi = x rounded to the nearest tf32 (cvt.rna), so lo = x - hi is exact and |lo| <= 2^-12 |x|.
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 // Shared-memory plan (dynamic, 1024-aligned):
 // STAGES x [A: MT tiles x 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64 (1 KB)]
@@ -154,7 +179,7 @@ struct Plan {
 
 constexpr int MAXMT = 2;
 struct Bars {
-  uint64_t full[8], empty[8], split_done[NAB], tfree[NAB], acc_full;
+  uint64_t full[8], empty[8], split_done[NAB], tfree[NAB], chunk_full[2], chunk_free[2];
   uint32_t tmem_base;
   double red[NSPLIT][MAXM];        // epilogue per-warp column partials
   double mean[NSPLIT][MAXMT][32];  // mean-column partials of the groups
@@ -167,7 +192,8 @@ struct Bars {
 template <int MT> struct TmemPlan {
   static constexpr int ACCW = MT == 2 ? 64 : 128;
   static constexpr int NABU = NAB / MT;
-  static __device__ __forceinline__ uint32_t acc(int t) { return t * ACCW; }
+  static constexpr int CPG = ACCW / NGROUP;        // accumulator columns promoted by each splitter group
+  static __device__ __forceinline__ uint32_t acc(int ab, int t) { return (ab * MT + t) * ACCW; }
   static __device__ __forceinline__ uint32_t abuf(int b, int t) { return TM_A + (b * MT + t) * 64; }
 };
 
@@ -180,13 +206,18 @@ template <int MT> struct TmemPlan {
 template <bool MN, int MT>
 __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mBh,
                          const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
-                         double (&acc0)[MT]) {
+                         double (&acc0)[MT], float (&sum)[MT][TmemPlan<MT>::CPG]) {
   using TP = TmemPlan<MT>;
-  constexpr int NABU = TP::NABU;
+  constexpr int NABU = TP::NABU, CPG = TP::CPG;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
+  const int nch = (nk + CH - 1) / CH;
 #pragma unroll
-  for (int t = 0; t < MT; ++t) acc0[t] = 0.0;
+  for (int t = 0; t < MT; ++t) {
+    acc0[t] = 0.0;
+#pragma unroll
+    for (int i = 0; i < CPG; ++i) sum[t][i] = 0.f;
+  }
   if (warp == 0) {
     if (lane == 0) {                                  // ---- TMA producer
       const uint32_t bytes = MT * BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
@@ -213,85 +244,97 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       int s = 0;
       uint32_t ph = 0;
       for (int kt = 0; kt < nk; ++kt) {
-        const int b = kt % NABU;
+        const int b = kt % NABU, c = kt / CH, ab = c & 1, kin = kt % CH;
+        if (kin == 0 && c >= 2) mbar_wait(&bs.chunk_free[ab], ((c >> 1) - 1) & 1);   // promoted by the splitters
         mbar_wait(&bs.full[s], ph);
         mbar_wait(&bs.split_done[b], (kt / NABU) & 1);
         fence_after();
         const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
-#ifndef COFEM_TC_EXPERIMENT_NOCOMPUTE
 #pragma unroll
         for (int t = 0; t < MT; ++t) {
-          const uint32_t d = tmem + TP::acc(t), ahi = tmem + TP::abuf(b, t), alo = ahi + 32;
+          const uint32_t d = tmem + TP::acc(ab, t), ahi = tmem + TP::abuf(b, t), alo = ahi + 32;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {        // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
             const uint64_t dbh = desc_k_sw128(bh + kk * 32), dbl = desc_k_sw128(bl + kk * 32);
-#ifndef COFEM_TC_EXP_NOMMA
-            mma_ts(d, ahi + kk * 8, dbh, idesc, (kt | kk) != 0);
+            mma_ts(d, ahi + kk * 8, dbh, idesc, (kin | kk) != 0);
             mma_ts(d, ahi + kk * 8, dbl, idesc, 1);
             mma_ts(d, alo + kk * 8, dbh, idesc, 1);
-#endif
           }
         }
-#endif
         mma_commit(&bs.empty[s]);                       // smem stage reusable once these MMAs retire
         mma_commit(&bs.tfree[b]);                       // TMEM A buffers b reusable
+        if (kin == CH - 1 || kt == nk - 1) mma_commit(&bs.chunk_full[ab]);   // chunk c accumulated
         if (++s == pl.stages) { s = 0; ph ^= 1; }
       }
-      mma_commit(&bs.acc_full);
     }
-  } else {                                            // ---- splitters (warps 2 .. 2 + NSPLIT)
+  } else {                                            // ---- splitters / promoters (warps 2 .. 2 + NSPLIT)
     // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m of
-    // every M-tile for the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently.
+    // every M-tile for the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently,
+    // and it promotes accumulator columns [g CPG, (g+1) CPG) of row m after every chunk.
     const int wi = warp - 2, q = warp & 3, g = wi >> 2, m = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
-    double acc[MT][4];                                // independent DFMA chains (fixed-order sums below)
+    double acc[MT][2];                                // independent DFMA chains (fixed-order sums below)
 #pragma unroll
-    for (int t = 0; t < MT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0;
+    for (int t = 0; t < MT; ++t) acc[t][0] = acc[t][1] = 0.0;
     int s = g % pl.stages;
     uint32_t ph = (g / pl.stages) & 1;
+    int cdone = 0;                                    // chunks promoted so far
+    auto promote = [&](int c) {                       // chunk c: TMEM accumulator -> register sums (RN)
+      const int ab = c & 1;
+      mbar_wait(&bs.chunk_full[ab], (c >> 1) & 1);
+      fence_after();
+#pragma unroll
+      for (int t = 0; t < MT; ++t)
+#pragma unroll
+        for (int cc = 0; cc < CPG; cc += 16) {
+          float v[16];
+          tmem_ld16(lane_addr + TP::acc(ab, t) + g * CPG + cc, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) sum[t][cc + i] += v[i];
+        }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bs.chunk_free[ab]);
+    };
     for (int kt = g; kt < nk; kt += NGROUP) {
+      // promote the chunks two behind this step (their MMAs need no split work of ours anymore)
+      while (cdone < nch && (cdone + 2) * CH <= kt) promote(cdone++);
       const int b = kt % NABU;
       mbar_wait(&bs.full[s], ph);
       if (kt >= NABU) mbar_wait(&bs.tfree[b], ((kt / NABU) - 1) & 1);
       const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s));
-#ifndef COFEM_TC_EXPERIMENT_NOCOMPUTE
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const unsigned char* a = sm + pl.a_off(s, t);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float x[16];
+        for (int h = 0; h < 4; ++h) {
+          float x[8];
           if (MN) {   // [32 n][128 d] dense: a warp reads 128 contiguous bytes per n (conflict-free)
             const float* col = reinterpret_cast<const float*>(a) + m;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = col[(16 * h + i) * BM];
+            for (int i = 0; i < 8; ++i) x[i] = col[(8 * h + i) * BM];
           } else {    // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
             const unsigned char* rowp = a + m * 128;
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-              const int c = 4 * h + cc;
+            for (int cc = 0; cc < 2; ++cc) {
+              const int c = 2 * h + cc;
               const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
               x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
             }
           }
-          float hi[16], lo[16];
+          float hi[8], lo[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 8; ++i) {
             hi[i] = tf32_hi(x[i]);
             lo[i] = x[i] - hi[i];
 #ifndef COFEM_TC_EXP_NOMEAN
-            acc[t][i & 3] = fma((double)x[i], w[16 * h + i], acc[t][i & 3]);   // mean column, fp64 (R10)
+            acc[t][i & 1] = fma((double)x[i], w[8 * h + i], acc[t][i & 1]);   // mean column, fp64 (R10)
 #endif
           }
-#ifndef COFEM_TC_EXP_NOSTTM
-          tmem_st16(lane_addr + TP::abuf(b, t) + 16 * h, hi);
-          tmem_st16(lane_addr + TP::abuf(b, t) + 32 + 16 * h, lo);
-#else
-          if (hi[0] == 1.2345f && lo[3] == 2.5f) acc[t][0] += 1.0;   // keep the split live
-#endif
+          tmem_st8(lane_addr + TP::abuf(b, t) + 8 * h, hi);
+          tmem_st8(lane_addr + TP::abuf(b, t) + 32 + 8 * h, lo);
         }
       }
-#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&bs.empty[s]);       // this warp has consumed its reads of the smem stage
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -301,9 +344,10 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       s += NGROUP;
       while (s >= pl.stages) { s -= pl.stages; ph ^= 1; }
     }
+    while (cdone < nch) promote(cdone++);
     // combine the groups' partial sums of row m in fixed order (g = 0 .. NGROUP-1)
 #pragma unroll
-    for (int t = 0; t < MT; ++t) bs.mean[wi][t][lane] = (acc[t][0] + acc[t][1]) + (acc[t][2] + acc[t][3]);
+    for (int t = 0; t < MT; ++t) bs.mean[wi][t][lane] = acc[t][0] + acc[t][1];
     asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
@@ -320,7 +364,7 @@ __device__ void setup_cta(Bars& bs, int stages) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.empty[s], 1 + 4); }
     for (int b = 0; b < NAB; ++b) { mbar_init(&bs.split_done[b], 4); mbar_init(&bs.tfree[b], 1); }
-    mbar_init(&bs.acc_full, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(&bs.chunk_full[b], 1); mbar_init(&bs.chunk_free[b], NSPLIT); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -340,12 +384,6 @@ __device__ void teardown_cta(Bars& bs) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(bs.tmem_base), "r"(TMEM_COLS));
   }
-}
-
-// Epilogue column range of splitter group g (bn columns over NGROUP groups, 16-column loads)
-__device__ __forceinline__ void group_cols(int bn, int g, int& c0, int& c1) {
-  const int cpg = ((bn / 16 + NGROUP - 1) / NGROUP) * 16;
-  c0 = g * cpg; c1 = min(bn, (g + 1) * cpg);
 }
 
 // ---------------------------------------------------------------- K1: W partials = Phi P (split-K over D)
@@ -369,28 +407,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ 
   const int k0 = split * a.kchunk, k1 = min(a.D, k0 + a.kchunk);
   const int nk = (k1 - k0 + BK - 1) / BK;
   double acc0[MT];
-  mainloop<false, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, acc0);
+  float sum[MT][TmemPlan<MT>::CPG];
+  mainloop<false, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, acc0, sum);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= 2) {
+    constexpr int CPG = TmemPlan<MT>::CPG;
     const int q = warp & 3, g = (warp - 2) >> 2;
-    int c0, c1;
-    group_cols(a.pl.bn, g, c0, c1);
-    mbar_wait(&bs.acc_full, 0);
-    fence_after();
-    const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
     float* wp = a.Wpart + (size_t)split * a.K * a.Npad;
 #pragma unroll
     for (int t = 0; t < MT; ++t) {
       const int n = row0 + BM * t + 32 * q + lane;
-      for (int c = c0; c < c1; c += 16) {
-        float v[16];
-        tmem_ld16(la + TmemPlan<MT>::acc(t) + c, v);
-        if (n < a.N)
+      if (n < a.N) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c + i < a.K) wp[(size_t)(c + i) * a.Npad + n] = v[i];
+        for (int i = 0; i < CPG; ++i) {
+          const int col = g * CPG + i;
+          if (col < a.K) wp[(size_t)col * a.Npad + n] = sum[t][i];
+        }
+        if (g == 0) a.W0part[(size_t)split * a.Npad + n] = acc0[t];
       }
-      if (g == 0 && n < a.N) a.W0part[(size_t)split * a.Npad + n] = acc0[t];
     }
   }
   teardown_cta(bs);
@@ -451,13 +485,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
   const int row0 = blockIdx.x * BM * MT;
   const int nk = (a.N + BK - 1) / BK;
   double acc0[MT];
-  mainloop<true, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0);
+  float sum[MT][TmemPlan<MT>::CPG];
+  mainloop<true, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0, sum);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.K + 1;
   if (warp >= 2) {
+    constexpr int CPG = TmemPlan<MT>::CPG;
     const int wi = warp - 2, q = warp & 3, g = wi >> 2;
-    int c0, c1;
-    group_cols(a.pl.bn, g, c0, c1);
     if (g == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
       double gm = 0.0;
 #pragma unroll
@@ -472,37 +506,30 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
       gm = warp_sum(gm);
       if (lane == 0) bs.red[wi][0] = gm;
     }
-    mbar_wait(&bs.acc_full, 0);
-    fence_after();
-    const uint32_t la = bs.tmem_base + ((uint32_t)(32 * q) << 16);
     const float bt = (float)a.beta;
-    for (int c = c0; c < c1; c += 16) {
-      double gk[16];
+    float alf[MT];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) gk[i] = 0.0;
+    for (int t = 0; t < MT; ++t) {
+      const int d = row0 + BM * t + 32 * q + lane;
+      alf[t] = d < a.D ? (float)a.alpha[d] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < CPG; ++i) {
+      const int k = g * CPG + i;
+      if (k >= a.K) break;                            // warp-uniform
+      double gk = 0.0;
 #pragma unroll
       for (int t = 0; t < MT; ++t) {
         const int d = row0 + BM * t + 32 * q + lane;
-        const bool valid = d < a.D;
-        const float alf = valid ? (float)a.alpha[d] : 0.f;
-        float v[16];
-        tmem_ld16(la + TmemPlan<MT>::acc(t) + c, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int k = c + i;
-          if (k < a.K && valid) {
-            const float p = a.P[(int64_t)k * a.Dp + d];
-            const float qv = bt * v[i] + alf * p;     // a3: q = beta Phi^T Phi p + alpha o p
-            a.Q[(int64_t)k * a.Dp + d] = qv;
-            gk[i] += (double)p * (double)qv;          // a4
-          }
+        if (d < a.D) {
+          const float p = a.P[(int64_t)k * a.Dp + d];
+          const float qv = bt * sum[t][i] + alf[t] * p;   // a3: q = beta Phi^T Phi p + alpha o p
+          a.Q[(int64_t)k * a.Dp + d] = qv;
+          gk += (double)p * (double)qv;               // a4
         }
       }
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const double gg = warp_sum(gk[i]);
-        if (lane == 0 && c + i < a.K) bs.red[wi][c + i + 1] = gg;
-      }
+      gk = warp_sum(gk);
+      if (lane == 0) bs.red[wi][k + 1] = gk;
     }
   }
   __syncthreads();
@@ -600,7 +627,9 @@ cofem_status dense_tc_setup(Ctx* c) {
   c->dense_tc = t;
   t->bn = std::max(16, (c->Kcap + 15) / 16 * 16);
   // 256-row CTAs share each B tile when K <= 64 and the K2 grid still fills the SMs
-  t->mt = (t->bn <= 64 && (c->D + 2 * BM - 1) / (2 * BM) >= c->num_sms / 2) ? 2 : 1;
+  // MT = 2 (256-row CTAs sharing B tiles) hangs with the chunked-promotion protocol (two
+  // TMEM A buffers); it stays off until that is resolved.
+  t->mt = (getenv("COFEM_TC_MT2") && t->bn <= 64) ? 2 : 1;
   t->pl = plan_for(t->bn, t->mt);
   t->Npad = (int)((c->N + 31) / 32 * 32);
   const int rows = BM * t->mt;
@@ -668,6 +697,16 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   else k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
+  if (getenv("COFEM_TC_DEBUG")) {     // synchronous protocol check (debug hook)
+    cudaStreamSynchronize(c->stream);
+    unsigned long long h[4];
+    cudaMemcpyFromSymbol(h, g_tc_stuck, sizeof h);
+    if (h[0]) {
+      fprintf(stderr, "cofem tc: stuck wait: block (%llu,%llu) warp %llu smem offset 0x%llx parity %llu\n", h[1] >> 32,
+              (h[1] >> 16) & 0xFFFF, h[1] & 0xFFFF, h[2] >> 32, h[2] & 0xFFFFFFFF);
+      c->err = "tensor-core pipeline stall"; return COFEM_ERR_CUDA;
+    }
+  }
   return COFEM_OK;
 }
 
