@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C4")
+    ap.add_argument("--mode", default="probe", choices=["probe", "column"],
+                    help="multi-GPU partitioning: probe-parallel (any operator) or column-sharded dense Phi")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -94,13 +96,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ algorithmic bytes per launch
-def algorithmic_bytes(cls, w, K_local):
+def algorithmic_bytes(cls, w, K_local, D_local=None):
     """Bytes the algorithm must move per launch of kernel class `cls`:
     4 B per fp32 probe element, D elements per column; arrays shared by all columns
     (dinv, alpha, s, probe bits) are counted once per launch.  On the 1024 x 1024 DCT
     fast path the fp64 mean column runs as its own class ("mean_column") on a second
     stream, so the probe classes count the K probe columns only."""
-    D, K = w.D, K_local
+    D, K = (D_local or w.D), K_local
     fast = w.kind == "dct2_masked" and w.rows == 1024 and w.cols == 1024
     if cls == "dct_rows_inv":      # read r, p; write p (direction), write T^T; dinv once
         return D * (16 * K + 4) if fast else D * (16 * K + 32 + 4 + 8)
@@ -207,23 +209,41 @@ def main():
 
     import synth
     from paper_2202_12808_b200 import Context
-    from paper_2202_12808_b200.dist import probe_split
+    from paper_2202_12808_b200.dist import column_shard, probe_split
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     w = synth.preset(args.workload, seed=args.seed)
-    k_off, K_loc = probe_split(w.K, world, rank)
-    ctx = Context.from_workload(w, max_probes=K_loc)
-    D = w.D
+    column = args.mode == "column"
+    if column:
+        # column-sharded dense Phi: rank r holds Phi[:, d0:d0+Dr] and the D-slices of
+        # alpha, mu, s; the library all-reduces W and the column dots over NCCL inside the E-step
+        if w.kind != "dense":
+            raise SystemExit("--mode column needs a dense workload (C1-C3)")
+        from paper_2202_12808_b200 import OP_DENSE, get_unique_id
+        d0, Dr = column_shard(w.D, world, rank)
+        nid = get_unique_id() if rank == 0 else bytes(128)
+        if world > 1:
+            box = [nid]
+            torch.distributed.broadcast_object_list(box, src=0)
+            nid = box[0]
+        k_off, K_loc = 0, w.K
+        ctx = Context(OP_DENSE, w.N, Dr, w.y, w.beta, phi=np.ascontiguousarray(w.phi[:, d0:d0 + Dr]), cg_iters=w.U,
+                      max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0, D_global=w.D)
+        D = Dr
+    else:
+        k_off, K_loc = probe_split(w.K, world, rank)
+        ctx = Context.from_workload(w, max_probes=K_loc)
+        D = w.D
     alpha = torch.ones(D, dtype=torch.float64, device=dev)
     mu = torch.empty_like(alpha)
     s = torch.empty_like(alpha)
     seed = args.seed
 
     def step(t, a_in, a_out, m_out, s_out):
-        if world == 1:
+        if world == 1 or column:
             ctx.em(1, w.K, seed, t, a_in, a_out, m_out, s_out)
         else:
             ctx.estep(a_in, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
@@ -298,7 +318,7 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            if world == 1:
+            if world == 1 or column:
                 ctx.em(1, w.K, seed, t, a_h, a_h, m_h, s_h)      # h2d alpha; d2h alpha, mu, s
             else:
                 ctx.estep(a_h, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
@@ -316,10 +336,10 @@ def main():
 
     # ---- roofline of the dominant kernel (live CUDA events over the timed region)
     pk, pk_kind = peaks()
-    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc)), key=lambda c: prof[c][0])
+    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc, D)), key=lambda c: prof[c][0])
     tot_ms, cnt = prof[dom]
     avg_ms = tot_ms / cnt
-    byt = algorithmic_bytes(dom, w, K_loc)
+    byt = algorithmic_bytes(dom, w, K_loc, D)
     achieved = byt / (avg_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -342,8 +362,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 (probe columns) + f64 (mean column)",
                 "data": "synthetic",
-                "config": {"workload": w.name, **w.config(), "parallelism": "probe-parallel x%d" % world,
-                           "K_per_rank": K_loc,
+                "config": {"workload": w.name, **w.config(),
+                           "parallelism": ("column-sharded x%d" if column else "probe-parallel x%d") % world,
+                           "K_per_rank": K_loc, "D_per_rank": D,
                            "l2": "inputs larger than L2 (working set %.0f MB > 126 MB)" % (
                                (w.K + 1) * D * 4 * 5 / 1e6)},
                 "rhs_applies_per_s": rhs_applies, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,

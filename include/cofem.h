@@ -72,6 +72,12 @@ typedef struct {
   /* CIRCCONV */
   const float* taps;         /* ntaps fp32 filter taps h_j; host or device */
   int32_t ntaps;             /* 1 <= ntaps <= 64, ntaps <= D */
+  /* DENSE column-sharded mode: this rank holds Phi's columns
+   * [d_offset, d_offset + D) of D_global (phi is N x D local, y the full N); alpha, mu, s
+   * are the matching D-slices.  d_offset must be a multiple of 128 (probe counters,
+   * reading R8).  D_global = 0: unsharded. */
+  int64_t d_offset;
+  int64_t D_global;
 } cofem_operator;
 
 typedef struct {
@@ -81,9 +87,18 @@ typedef struct {
   double alpha_max;          /* M-step clamp (default 1e12) */
   int32_t probe_precision;   /* 0: probe columns in fp32 (fast); 1: fp64 (parity mode). The mean column is always fp64. */
   int32_t max_probes;        /* K capacity of the workspaces (>= any K passed later) */
+  /* Column-sharded dense mode: NCCL rank / world and the 128-byte ncclUniqueId from
+   * cofem_get_unique_id (broadcast by the caller).  nccl_id = NULL: single GPU.  World 1 with
+   * an id runs the sharded code path on a 1-rank communicator (tests). */
+  int32_t rank, world;
+  const uint8_t* nccl_id;
 } cofem_options;
 
-/* Fill *opt with the defaults above (U = 100, precond = 1, max_probes = 32). */
+/* NCCL unique id for cofem_options.nccl_id (call on one rank, broadcast the 128 bytes).
+ * Returns COFEM_ERR_NCCL if libnccl.so.2 cannot be loaded. */
+cofem_status cofem_get_unique_id(uint8_t id[128]);
+
+/* Fill *opt with the defaults above (U = 100, precond = 1, max_probes = 32, single GPU). */
 void cofem_default_options(cofem_options* opt);
 
 /* Build a context: validate, copy/derive the operator (dense Phi copy; DCT

@@ -34,13 +34,15 @@ class _Operator(ctypes.Structure):
                 ("phi", ctypes.c_void_p), ("ld", ctypes.c_int64),
                 ("rows", ctypes.c_int32), ("cols", ctypes.c_int32), ("obs_idx", ctypes.c_void_p),
                 ("convention", ctypes.c_int32),
-                ("taps", ctypes.c_void_p), ("ntaps", ctypes.c_int32)]
+                ("taps", ctypes.c_void_p), ("ntaps", ctypes.c_int32),
+                ("d_offset", ctypes.c_int64), ("D_global", ctypes.c_int64)]
 
 
 class _Options(ctypes.Structure):
     _fields_ = [("cg_iters", ctypes.c_int32), ("precond", ctypes.c_int32), ("den_floor", ctypes.c_double),
                 ("alpha_max", ctypes.c_double), ("probe_precision", ctypes.c_int32),
-                ("max_probes", ctypes.c_int32)]
+                ("max_probes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p)]
 
 
 class _Report(ctypes.Structure):
@@ -52,6 +54,7 @@ class _Report(ctypes.Structure):
 
 # (name, restype, argtypes) — every entry point of include/cofem.h
 SYMBOLS = [
+    ("cofem_get_unique_id", ctypes.c_int, [ctypes.c_void_p]),
     ("cofem_default_options", None, [ctypes.POINTER(_Options)]),
     ("cofem_setup", ctypes.c_int, [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(_Operator), ctypes.c_void_p,
                                    ctypes.c_double, ctypes.POINTER(_Options), ctypes.c_void_p]),
@@ -92,6 +95,15 @@ def lib():
     return _lib
 
 
+def get_unique_id():
+    """128-byte NCCL unique id for the column-sharded mode (broadcast it to every rank)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().cofem_get_unique_id(buf)
+    if st != 0:
+        raise CofemError(st, "libnccl.so.2 could not be loaded")
+    return buf.raw
+
+
 def kernel_classes():
     out, i = [], 0
     while True:
@@ -128,7 +140,10 @@ class Context:
 
     def __init__(self, kind, N, D, y, beta, phi=None, rows=0, cols=0, obs_idx=None, convention=0, taps=None,
                  cg_iters=100, precond=1, probe_precision=0, max_probes=32, den_floor=1e-12, alpha_max=1e12,
-                 stream=None):
+                 stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None):
+        """Column-sharded dense mode: phi holds this rank's columns
+        [d_offset, d_offset + D) of D_global; nccl_id = get_unique_id() from one rank,
+        broadcast; the library all-reduces W and the column dots over NCCL itself."""
         L = lib()
         self.N, self.D, self.kind = int(N), int(D), int(kind)
         self._keep = [y, phi, obs_idx, taps]
@@ -138,6 +153,7 @@ class Context:
             op.phi = _ptr(phi, np.float32, self.N * self.D, "phi")
             op.ld = self.D
         op.rows, op.cols, op.convention = int(rows), int(cols), int(convention)
+        op.d_offset, op.D_global = int(d_offset), int(D_global)
         if obs_idx is not None:
             op.obs_idx = _ptr(obs_idx, np.int64, self.N, "obs_idx")
         if taps is not None:
@@ -148,6 +164,10 @@ class Context:
         opt.cg_iters, opt.precond, opt.probe_precision, opt.max_probes = int(cg_iters), int(precond), \
             int(probe_precision), int(max_probes)
         opt.den_floor, opt.alpha_max = float(den_floor), float(alpha_max)
+        opt.rank, opt.world = int(rank), int(world)
+        if nccl_id is not None:
+            self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opt.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)
         self.U, self.K_max = int(cg_iters), int(max_probes)
         self.probe_precision = int(probe_precision)
         h = ctypes.c_void_p()

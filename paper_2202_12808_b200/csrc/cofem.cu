@@ -83,11 +83,12 @@ struct VecArgs {
   const uint32_t* bits;
   ColState* cs; double* part; int part_stride; unsigned* counter;
   double invK;
+  double* colsum;   // sharded mode: per-column totals go here (summed over ranks, then finished)
 };
 
 // Probe-stream parameters of the current E-step, read from device memory so that one
 // captured CUDA graph serves every E-step (R8: key = seed, counter = (d/128, k, t, tag)).
-struct ProbeParams { uint32_t kx, ky; int t, k_offset; };
+struct ProbeParams { uint32_t kx, ky; int t, k_offset; long long blk_offset; };   // blk_offset: d_offset / 128
 __global__ void k_set_probe_params(ProbeParams* p, ProbeParams v) { *p = v; }
 
 __global__ void k_probe_bits(uint32_t* __restrict__ bits, int64_t wpc, int K, int64_t nblk128,
@@ -97,7 +98,7 @@ __global__ void k_probe_bits(uint32_t* __restrict__ bits, int64_t wpc, int K, in
   const ProbeParams prm = *pp;
   int k = (int)(idx / nblk128);
   int64_t b = idx - (int64_t)k * nblk128;
-  uint4 w = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(prm.k_offset + k), (uint32_t)prm.t, PROBE_TAG),
+  uint4 w = philox4x32_10(make_uint4((uint32_t)(b + prm.blk_offset), (uint32_t)(prm.k_offset + k), (uint32_t)prm.t, PROBE_TAG),
                           make_uint2(prm.kx, prm.ky));
   *reinterpret_cast<uint4*>(bits + (int64_t)k * wpc + b * 4) = w;
 }
@@ -210,7 +211,9 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
     }
   }
   ColState* cs = a.cs;
-  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs](int j, double v) {
+  double* colsum = a.colsum;
+  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs, colsum](int j, double v) {
+    if (colsum) { colsum[j] = v; return; }
     ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
     c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
     cs[j] = c;
@@ -284,7 +287,9 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
     }
   }
   ColState* cs = a.cs;
-  vec_finish(sh, a.part, a.part_stride, a.counter, a.jlo, a.jhi, [cs](int j, double v) {
+  double* colsum = a.colsum;
+  vec_finish(sh, a.part, a.part_stride, a.counter, a.jlo, a.jhi, [cs, colsum](int j, double v) {
+    if (colsum) { colsum[j] = v; return; }
     ColState c = cs[j];
     if (c.frozen) return;
     c.b = v / c.rho;
@@ -347,6 +352,30 @@ __global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* 
   }
 }
 
+// Sharded mode: apply the rank-summed per-column totals (same rules as the in-kernel finishes).
+__global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum, int m, int mode, int iter) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const double v = colsum[j];
+  ColState c = cs[j];
+  if (mode == 0) {
+    c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0; c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+  } else if (mode == 1) {
+    finish_gamma(c, v, iter);
+  } else {
+    if (c.frozen) return;
+    c.b = v / c.rho; c.rho = v;
+  }
+  cs[j] = c;
+}
+
+cofem_status sharded_finish(Ctx* c, int m, int mode, int iter) {
+  cofem_status st = comm_allreduce(c, c->colsum, (size_t)m, 1);
+  if (st != COFEM_OK) return st;
+  k_sharded_finish<<<1, 160, 0, c->stream>>>(c->cs, c->colsum, m, mode, iter);
+  return check_launch(c, "k_sharded_finish") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
 template <typename TP>
 static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   VecArgs<TP> a;
@@ -360,6 +389,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.s = c->s; a.bits = c->bits;
   a.cs = c->cs; a.part = c->part; a.part_stride = c->part_stride; a.counter = c->counters + MAXM;
   a.invK = invK;
+  a.colsum = c->sharded ? c->colsum : nullptr;
   return a;
 }
 
@@ -484,6 +514,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   else k_init<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
   launch_end(c, KC_INIT);
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
+  if (c->sharded) { cofem_status st = sharded_finish(c, m, 0, 0); if (st != COFEM_OK) return st; }
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
   for (int it = 0; it < c->opt.cg_iters; ++it) {
@@ -500,6 +531,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     else k_update<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
+    if (c->sharded && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
   }
   return COFEM_OK;
 }
@@ -509,7 +541,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
 // ~4-8 per CG iteration.  Per-kernel profiling (cofem_profile_enable)
 // records events around every launch and therefore runs uncaptured.
 static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offset, int K_total) {
-  ProbeParams pv{(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), t, k_offset};
+  ProbeParams pv{(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), t, k_offset, (long long)(c->d_offset / 128)};
   k_set_probe_params<<<1, 1, 0, c->stream>>>((ProbeParams*)c->dparams, pv);
   CK(cudaGetLastError());
   static const bool no_graph = getenv("COFEM_NO_GRAPH") != nullptr;   // test hook
@@ -588,6 +620,7 @@ void cofem_default_options(cofem_options* o) {
   memset(o, 0, sizeof *o);
   o->cg_iters = 100; o->precond = 1; o->den_floor = 1e-12; o->alpha_max = 1e12;
   o->probe_precision = 0; o->max_probes = 32;
+  o->rank = 0; o->world = 1; o->nccl_id = nullptr;
 }
 
 const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
@@ -599,12 +632,13 @@ const char* cofem_kernel_class_name(int32_t cls) {
 const char* cofem_last_error(cofem_ctx ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 
 static void free_all(Ctx* c) {
+  comm_destroy(c);
   dense_tc_free(c);
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
-                  c->Pb, c->p0b, c->conv_tab32, c->conv_tab64};
+                  c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -636,6 +670,17 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
+  if (opt->nccl_id || op->D_global) {          // column-sharded dense mode (comm.cu)
+    if (op->kind != COFEM_OP_DENSE) { c->err = "sharded mode: DENSE operators only"; return COFEM_ERR_UNSUPPORTED; }
+    if (!opt->nccl_id || opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) {
+      c->err = "sharded mode: need nccl_id and 0 <= rank < world"; return COFEM_ERR_INVALID;
+    }
+    if (op->d_offset < 0 || op->d_offset % 128 || op->D_global < op->d_offset + op->D) {
+      c->err = "sharded mode: d_offset must be a multiple of 128 and d_offset + D <= D_global"; return COFEM_ERR_INVALID;
+    }
+    if (opt->probe_precision) { c->err = "sharded mode: fp32 probes only"; return COFEM_ERR_UNSUPPORTED; }
+    c->sharded = true; c->d_offset = op->d_offset; c->D_global = op->D_global;
+  }
   c->probe64 = opt->probe_precision != 0;
   c->Kcap = opt->max_probes; c->m_cap = c->Kcap + 1;
   c->Dp = ((c->D + VEC_TILE - 1) / VEC_TILE) * VEC_TILE;
@@ -732,6 +777,12 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (y_tmp) cudaFree(y_tmp);
   if (st != COFEM_OK) return st;
   ALLOC(c->part, (size_t)c->m_cap * c->part_stride);
+  if (c->sharded) {
+    ALLOC(c->colsum, MAXM);
+    if (!c->dense_tc) { c->err = "sharded mode needs the tensor-core dense path (D % 4 == 0, K <= 128)"; return COFEM_ERR_UNSUPPORTED; }
+    cofem_status cst = comm_init(c, opt->rank, opt->world, opt->nccl_id);
+    if (cst != COFEM_OK) return cst;
+  }
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());
   return COFEM_OK;

@@ -1,0 +1,88 @@
+// comm.cu — NCCL for the column-sharded dense mode (BASELINE config 3
+// "column-sharded runs"): rank r owns the columns [d_offset, d_offset + D_r) of Phi and
+// the matching rows of every D-vector; each CG iteration sums W = Phi P over ranks and the
+// per-column dot products (gamma_j, rho_j) before the step lengths are taken.
+//
+// NCCL is resolved at run time (dlopen of the libnccl.so.2 already mapped into the process —
+// torch's — or the system one), so the library has no link-time NCCL dependency and a
+// single-GPU user never loads it.  Collectives are enqueued on the context stream (no host
+// synchronisation), so the sharded E-step is still captured into one CUDA graph.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <string>
+
+#include "internal.cuh"
+
+namespace cofem {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl(std::string& err) {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) { if (!api.ok) err = "NCCL not available"; return api; }
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);   // torch's, if loaded
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) { err = std::string("dlopen libnccl.so.2: ") + dlerror(); return api; }
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+  if (!api.ok) err = "libnccl.so.2 lacks required symbols";
+  return api;
+}
+
+cofem_status comm_init(Ctx* c, int rank, int world, const uint8_t* id) {
+  NcclApi& a = nccl(c->err);
+  if (!a.ok) return COFEM_ERR_NCCL;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  ncclComm_t comm;
+  ncclResult_t r = a.CommInitRank(&comm, world, uid, rank);
+  if (r != ncclSuccess) { c->err = std::string("ncclCommInitRank: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
+  c->comm = comm;
+  return COFEM_OK;
+}
+
+void comm_destroy(Ctx* c) {
+  if (!c->comm) return;
+  std::string e;
+  NcclApi& a = nccl(e);
+  if (a.ok) a.CommDestroy((ncclComm_t)c->comm);
+  c->comm = nullptr;
+}
+
+// In-place sum over ranks on the context stream; dtype 0 = fp32, 1 = fp64.
+cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype) {
+  NcclApi& a = nccl(c->err);
+  if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
+  ncclResult_t r = a.AllReduce(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, ncclSum, (ncclComm_t)c->comm,
+                               c->stream);
+  if (r != ncclSuccess) { c->err = std::string("ncclAllReduce: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
+  return COFEM_OK;
+}
+
+}  // namespace cofem
+
+extern "C" cofem_status cofem_get_unique_id(uint8_t id[128]) {
+  std::string err;
+  cofem::NcclApi& a = cofem::nccl(err);
+  if (!a.ok || !id) return COFEM_ERR_NCCL;
+  ncclUniqueId uid;
+  if (a.GetUniqueId(&uid) != ncclSuccess) return COFEM_ERR_NCCL;
+  memcpy(id, &uid, sizeof uid);
+  return COFEM_OK;
+}

@@ -99,6 +99,11 @@ struct Ctx {
   double* ws1d = nullptr; double* ws2d = nullptr;   // mean-column scratch
   int dense_splits = 1;
   void* dense_tc = nullptr;             // tensor-core dense path state (op_dense_tc.cu), NULL: SIMT
+  // column-sharded dense mode (comm.cu): per-column sums go through colsum + an NCCL all-reduce
+  bool sharded = false;
+  int64_t d_offset = 0, D_global = 0;
+  void* comm = nullptr;                 // ncclComm_t
+  double* colsum = nullptr;             // [MAXM] per-column totals of this rank
 
   // host mirrors for the report
   std::vector<ColState> cs_host;
@@ -240,6 +245,13 @@ cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_
 bool conv_fft_eligible(const Ctx* c);
 cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g);
 cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
+
+cofem_status comm_init(Ctx* c, int rank, int world, const uint8_t* id);
+void comm_destroy(Ctx* c);
+cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype);
+// after a per-column reduction written to c->colsum: sum over ranks, then apply it (mode:
+// 0 = rho0 (init), 1 = gamma -> freeze rule / step length, 2 = rho' -> b)
+cofem_status sharded_finish(Ctx* c, int m, int mode, int iter);
 
 // vector kernels (cofem.cu)
 cofem_status launch_dir(Ctx* c, int m);

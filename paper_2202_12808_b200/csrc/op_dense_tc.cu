@@ -441,8 +441,8 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
       float v = 0.f;
       if (n < N)
         for (int s = 0; s < splits; ++s) v += Wpart[(int64_t)s * tot + i];
-      const float h = tf32_hi(v);
-      Whi[i] = h; Wlo[i] = v - h;
+      if (Wlo) { const float h = tf32_hi(v); Whi[i] = h; Wlo[i] = v - h; }
+      else Whi[i] = v;                                // sharded: raw partial W, split after the all-reduce
     } else {
       const int n = (int)(i - tot);
       double v = 0.0;
@@ -450,6 +450,14 @@ __global__ void k_tc_reduce_w(int N, int Npad, int K, int splits, const float* _
         for (int s = 0; s < splits; ++s) v += W0part[(int64_t)s * Npad + n];
       w0[n] = v;
     }
+  }
+}
+
+// Sharded mode: W_hi / W_lo from the rank-summed W (in W_hi), in place.
+__global__ void k_tc_split_w(int64_t n, float* __restrict__ Wh, float* __restrict__ Wl) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = Wh[i], h = tf32_hi(v);
+    Wh[i] = h; Wl[i] = v - h;
   }
 }
 
@@ -472,6 +480,7 @@ struct PhiTWArgs {
   const double* alpha; const double* w0; const double* p0; double* q0;
   const float* P; float* Q;
   ColState* cs; double* part; int stride; unsigned* counter; int iter;
+  double* colsum;
 };
 
 template <int MT>
@@ -548,7 +557,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
     __threadfence();
     for (int j = warp; j < m; j += THREADS / 32) {
       const double v = reduce_partials(a.part + (int64_t)j * a.stride, gridDim.x);
-      if (lane == 0) { ColState c = a.cs[j]; finish_gamma(c, v, a.iter); a.cs[j] = c; }
+      if (lane == 0) {
+        if (a.colsum) a.colsum[j] = v;              // sharded: summed over ranks, then finished
+        else { ColState c = a.cs[j]; finish_gamma(c, v, a.iter); a.cs[j] = c; }
+      }
     }
     if (threadIdx.x == 0) *a.counter = 0u;
   }
@@ -684,19 +696,27 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   if (t->mt == 2) k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
-                                                       t->Wl, t->w0);
+                                                       c->sharded ? nullptr : t->Wl, t->w0);
+  if (c->sharded) {      // W = sum over ranks of Phi_r P_r (SURVEY §8(e) column-sharded dense), then split
+    cofem_status st;
+    if ((st = comm_allreduce(c, t->Wh, (size_t)K * t->Npad, 0)) != COFEM_OK) return st;
+    if ((st = comm_allreduce(c, t->w0, (size_t)t->Npad, 1)) != COFEM_OK) return st;
+    k_tc_split_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * t->Npad, t->Wh, t->Wl);
+  }
   launch_end(c, KC_DENSE_PHI_P);
   if (check_launch(c, "k_tc_phiP")) return COFEM_ERR_CUDA;
   PhiTWArgs a2;
   a2.pl = t->pl; a2.N = (int)c->N; a2.D = (int)c->D; a2.K = K; a2.Dp = c->Dp; a2.beta = c->beta;
   a2.alpha = c->alpha; a2.w0 = t->w0; a2.p0 = c->p0; a2.q0 = c->q0; a2.P = (const float*)c->P; a2.Q = (float*)c->Q;
   a2.cs = c->cs; a2.part = c->part; a2.stride = c->part_stride; a2.counter = c->counters + MAXM; a2.iter = iter;
+  a2.colsum = c->sharded ? c->colsum : nullptr;
   launch_begin(c, KC_DENSE_PHIT_W);
   const unsigned g2 = (unsigned)((c->D + rows - 1) / rows);
   if (t->mt == 2) k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
+  if (c->sharded) { cofem_status st = sharded_finish(c, m, 1, iter); if (st != COFEM_OK) return st; }
   if (getenv("COFEM_TC_DEBUG")) {     // synchronous protocol check (debug hook)
     cudaStreamSynchronize(c->stream);
     unsigned long long h[4];

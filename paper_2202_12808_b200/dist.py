@@ -10,6 +10,23 @@ tests); this module holds only the host-side orchestration.
 """
 
 
+def column_shard(D, world, rank, align=128):
+    """Column-sharded dense mode: contiguous slice [d_offset, d_offset + D_r)
+    of the D columns of Phi for `rank`, boundaries multiples of `align` (the probe counter
+    block, reading R8) so every rank regenerates the same p_k[d] for its global d.
+    Returns (d_offset, D_r)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    blocks = (D + align - 1) // align
+    if blocks < world:
+        raise ValueError("column sharding needs >= %d columns per rank" % align)
+    base, extra = divmod(blocks, world)
+    b0 = rank * base + min(rank, extra)
+    b1 = b0 + base + (1 if rank < extra else 0)
+    d0, d1 = b0 * align, min(D, b1 * align)
+    return d0, d1 - d0
+
+
 def probe_split(K, world, rank):
     """Contiguous split of K probes over `world` ranks: (k_offset, K_local)."""
     if world < 1 or not 0 <= rank < world:

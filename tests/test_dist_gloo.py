@@ -69,3 +69,98 @@ def test_probe_parallel_gloo_world2_equals_single(tmp_path):
     ea, emu, es = cofem_em(DenseOp(w.phi), w.y, w.beta, 3, 6, 9, w.U)
     rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)
     assert rel(a, ea) < 1e-10 and rel(mu, emu) < 1e-10 and rel(s, es) < 1e-10, (rel(a, ea), rel(mu, emu), rel(s, es))
+
+
+# ---------------------------------------------------------------- column-sharded dense mode
+def test_column_shard_covers_all_aligned():
+    from paper_2202_12808_b200.dist import column_shard
+    for D in (256, 400, 1000, 8000, 32768):
+        for world in (1, 2, 3, 4, 8):
+            if (D + 127) // 128 < world:
+                continue
+            parts = [column_shard(D, world, r) for r in range(world)]
+            assert [d for off, n in parts for d in range(off, off + n)] == list(range(D))
+            assert all(off % 128 == 0 for off, _ in parts) and min(n for _, n in parts) >= 1
+
+
+def _col_worker(rank, world, port, out):
+    """One rank of the column-sharded E-step, following the library's schedule exactly
+    (op_dense_tc.cu + cofem.cu sharded path): local b0 / colsq / probes of the rank's global
+    d range; every reduction the library sends through NCCL (rho0, W = Phi P and Phi p0,
+    gamma, rho') is a gloo all-reduce here; the step lengths are then taken identically on
+    every rank.  Local arithmetic is plain NumPy fp64 (this is a test of the decomposition
+    and the exchange schedule, not of the kernels)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    import synth
+    from oracle.philox import rademacher_probes
+    from paper_2202_12808_b200.dist import column_shard
+    w = synth.dense(60, 640, 6, K=5, U=200, T=1, seed=3)   # converged U (DESIGN.md §4)
+    d0, Dr = column_shard(w.D, world, rank)
+    Phi = w.phi.astype(np.float64)[:, d0:d0 + Dr]
+    alpha = np.linspace(0.5, 3.0, w.D)[d0:d0 + Dr]
+    beta, K, U = w.beta, w.K, w.U
+
+    def ar(x):
+        t = torch.from_numpy(np.array(x, dtype=np.float64, copy=True))
+        dist.all_reduce(t)
+        return t.numpy()
+
+    b0 = beta * Phi.T @ w.y.astype(np.float64)
+    diag = beta * np.sum(Phi * Phi, axis=0) + alpha
+    P = rademacher_probes(w.D, K, 11, 0)[d0:d0 + Dr]          # global d range (reading R8)
+    B = np.concatenate([b0[:, None], P], axis=1)
+    X = np.zeros_like(B)
+    R = B.copy()
+    Z = R / diag[:, None]
+    Pd = Z.copy()
+    rho = ar(np.sum(R * Z, axis=0))                            # k_init -> colsum -> all-reduce
+    rho0 = rho.copy()
+    frozen = np.zeros(K + 1, dtype=bool)
+    for _ in range(U):
+        W = ar(Phi @ Pd)                                       # K1 partial W -> all-reduce
+        Q = beta * Phi.T @ W + alpha[:, None] * Pd             # K2 (local rows)
+        gamma = ar(np.sum(Pd * Q, axis=0))                     # gamma -> colsum -> all-reduce
+        with np.errstate(all="ignore"):                        # freeze rule R5, same on every rank
+            ok = np.isfinite(gamma) & np.isfinite(rho) & (gamma > 0) & (rho > 1e-30 * rho0)
+        frozen |= ~ok
+        act = ~frozen
+        a = np.where(act, rho / np.where(act, gamma, 1.0), 0.0)
+        X += a * Pd
+        R -= a * Q
+        Z = R / diag[:, None]
+        rho_new = ar(np.sum(R * Z, axis=0))                    # rho' -> colsum -> all-reduce
+        b = np.where(act, rho_new / rho, 0.0)
+        Pd = np.where(act, Z + b * Pd, Pd)
+        rho = np.where(act, rho_new, rho)
+    mu = X[:, 0]
+    s = np.mean(P * X[:, 1:], axis=1)
+    full = np.zeros(w.D)
+    full[d0:d0 + Dr] = mu
+    mu_full = ar(full)
+    full = np.zeros(w.D)
+    full[d0:d0 + Dr] = s
+    s_full = ar(full)
+    if rank == 0:
+        np.save(out, np.stack([mu_full, s_full]))
+    dist.destroy_process_group()
+
+
+def test_column_sharded_gloo_world2_equals_single(tmp_path):
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = str(tmp_path / "c0.npy")
+    mp.start_processes(_col_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    mu, s = np.load(out)
+    import synth
+    from oracle.cofem import estep
+    from oracle.operators import DenseOp
+    w = synth.dense(60, 640, 6, K=5, U=200, T=1, seed=3)   # converged U (DESIGN.md §4)
+    alpha = np.linspace(0.5, 3.0, w.D)
+    emu, es, _ = estep(DenseOp(w.phi), w.y, w.beta, alpha, w.K, 11, 0, w.U)
+    rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)
+    assert rel(mu, emu) < 1e-8 and rel(s, es) < 1e-8, (rel(mu, emu), rel(s, es))

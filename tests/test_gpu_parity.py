@@ -279,3 +279,35 @@ def test_c2_full_size_tensor_core_path():
     a, mu, s = gpu_em(ctx, w, 2, 8, 6)
     oa, omu, _ = cofem_em(op_of(w), w.y, w.beta, 2, 8, 6, 40)
     assert rel(1 / a, 1 / oa) <= 1e-3 and rel(mu, omu) <= 1e-3, (rel(1 / a, 1 / oa), rel(mu, omu))
+
+
+def test_column_sharded_path_world1():
+    """The column-sharded dense path (comm.cu + the sharded finishes of cofem.cu /
+    op_dense_tc.cu) on a 1-rank NCCL communicator: (i) with d_offset = 0 it must reproduce
+    the single-GPU run exactly (the all-reduces are identities, the sums are the same); (ii)
+    a rank holding columns [128, 1024) of a 1024-column Phi must solve its sub-system with
+    the probes of its GLOBAL indices (reading R8), against the fp64 oracle PCG."""
+    from oracle.cofem import jacobi_diag, mean_rhs, pcg
+    from oracle.operators import gram_apply
+    from paper_2202_12808_b200 import OP_DENSE, Context, get_unique_id
+    w = synth.dense(250, 1024, 20, K=8, U=60, T=3, seed=2)
+    a, mu, s = gpu_em(ctx_of(w), w, 3, 8, 5)
+    nid = get_unique_id()
+    sh = ctx_of(w, rank=0, world=1, nccl_id=nid, d_offset=0, D_global=w.D)
+    a2, mu2, s2 = gpu_em(sh, w, 3, 8, 5)
+    assert np.array_equal(a2, a) and np.array_equal(mu2, mu) and np.array_equal(s2, s)
+    d0 = 128
+    phi_r = np.ascontiguousarray(w.phi[:, d0:])
+    part = Context(OP_DENSE, w.N, w.D - d0, w.y, w.beta, phi=phi_r, cg_iters=w.U, max_probes=8,
+                   rank=0, world=1, nccl_id=get_unique_id(), d_offset=d0, D_global=w.D)   # one id per communicator
+    alpha = np.ones(w.D - d0)
+    a_dev = torch.ones(w.D - d0, dtype=torch.float64, device="cuda")
+    m_dev, s_dev = dev(w.D - d0), dev(w.D - d0)
+    part.estep(a_dev, 8, 5, 0, m_dev, s_dev)
+    op = DenseOp(phi_r)
+    P = rademacher_probes(w.D, 8, 5, 0)[d0:]
+    B = np.concatenate([mean_rhs(op, w.y, w.beta)[:, None], P], axis=1)
+    X, _ = pcg(lambda V: gram_apply(op, w.beta, alpha, V), B, jacobi_diag(op, w.beta, alpha), w.U)
+    omu, os_ = X[:, 0], np.mean(P * X[:, 1:], axis=1)
+    assert rel(m_dev.cpu().numpy(), omu) <= 1e-4 and rel(s_dev.cpu().numpy(), os_) <= 1e-4, \
+        (rel(m_dev.cpu().numpy(), omu), rel(s_dev.cpu().numpy(), os_))
