@@ -48,6 +48,7 @@ constexpr int TM_A = 256;
 // (K = 64) into round-to-nearest fp32 register sums held by the splitter warps, with two TMEM
 // accumulator buffers so the MMAs of the next chunk overlap the promotion.
 constexpr int CH = 2;
+constexpr int PLAG = 3;                    // splitters promote chunk c once they reach step (c + PLAG) CH (protocol checked by simulation)
 
 // ---------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -297,8 +298,8 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       if (lane == 0) mbar_arrive(&bs.chunk_free[ab]);
     };
     for (int kt = g; kt < nk; kt += NGROUP) {
-      // promote the chunks two behind this step (their MMAs need no split work of ours anymore)
-      while (cdone < nch && (cdone + 2) * CH <= kt) promote(cdone++);
+      // promote the chunks PLAG behind this step (their MMAs need no split work of ours anymore)
+      while (cdone < nch && (cdone + PLAG) * CH <= kt) promote(cdone++);
       const int b = kt % NABU;
       mbar_wait(&bs.full[s], ph);
       if (kt >= NABU) mbar_wait(&bs.tfree[b], ((kt / NABU) - 1) & 1);
