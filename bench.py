@@ -220,9 +220,9 @@ def main():
     if column:
         # column-sharded dense Phi: rank r holds Phi[:, d0:d0+Dr] and the D-slices of
         # alpha, mu, s; the library all-reduces W and the column dots over NCCL inside the E-step
-        if w.kind != "dense":
-            raise SystemExit("--mode column needs a dense workload (C1-C3)")
-        from paper_2202_12808_b200 import OP_DENSE, get_unique_id
+        if w.kind not in ("dense", "circconv"):
+            raise SystemExit("--mode column needs a dense (C1-C3, column-sharded) or convolution (C5, D-sharded) workload")
+        from paper_2202_12808_b200 import OP_CIRCCONV, OP_DENSE, get_unique_id
         d0, Dr = column_shard(w.D, world, rank)
         nid = get_unique_id() if rank == 0 else bytes(128)
         if world > 1:
@@ -230,8 +230,14 @@ def main():
             torch.distributed.broadcast_object_list(box, src=0)
             nid = box[0]
         k_off, K_loc = 0, w.K
-        ctx = Context(OP_DENSE, w.N, Dr, w.y, w.beta, phi=np.ascontiguousarray(w.phi[:, d0:d0 + Dr]), cg_iters=w.U,
-                      max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0, D_global=w.D)
+        if w.kind == "dense":
+            ctx = Context(OP_DENSE, w.N, Dr, w.y, w.beta, phi=np.ascontiguousarray(w.phi[:, d0:d0 + Dr]),
+                          cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
+                          D_global=w.D)
+        else:   # D-sharded circular convolution: 64-sample halos exchanged with both ring neighbours
+            ctx = Context(OP_CIRCCONV, Dr, Dr, np.ascontiguousarray(w.y[d0:d0 + Dr]), w.beta, taps=w.taps,
+                          cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
+                          D_global=w.D)
         D = Dr
     else:
         k_off, K_loc = probe_split(w.K, world, rank)
@@ -363,7 +369,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32 (probe columns) + f64 (mean column)",
                 "data": "synthetic",
                 "config": {"workload": w.name, **w.config(),
-                           "parallelism": ("column-sharded x%d" if column else "probe-parallel x%d") % world,
+                           "parallelism": (("column-sharded x%d" if w.kind == "dense" else "D-sharded x%d") if column
+                                           else "probe-parallel x%d") % world,
                            "K_per_rank": K_loc, "D_per_rank": D,
                            "l2": "inputs larger than L2 (working set %.0f MB > 126 MB)" % (
                                (w.K + 1) * D * 4 * 5 / 1e6)},

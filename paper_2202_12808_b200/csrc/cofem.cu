@@ -495,6 +495,8 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
 }
 
 // Runs Alg. 1 lines 3-7 with alpha already in c->alpha.  No host sync inside.
+static cofem_status cg_loop_conv_sharded(Ctx* c, int K, double invK);
+
 // The device work of one E-step (probes .. end of the CG loop), enqueued on c->stream;
 // the probe parameters are already in c->dparams.
 static cofem_status estep_body(Ctx* c, int K, int K_total) {
@@ -516,6 +518,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
   if (c->sharded) { cofem_status st = sharded_finish(c, m, 0, 0); if (st != COFEM_OK) return st; }
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
+  if (c->fast_conv && c->sharded) return cg_loop_conv_sharded(c, K, invK);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
@@ -533,6 +536,30 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
     if (c->sharded && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
   }
+  return COFEM_OK;
+}
+
+// D-sharded convolution (BASELINE config 5): one stream (the NCCL calls must
+// be ordered); per CG iteration: halo exchange of r, p, 1/diag with both ring neighbours,
+// the FFT apply of the mean and the probe columns, the rank-sum of gamma, the update, the
+// rank-sum of rho'.
+static cofem_status cg_loop_conv_sharded(Ctx* c, int K, double invK) {
+  const int m = K + 1;
+  void* const P_entry = c->P; double* const p0_entry = c->p0;
+  for (int it = 0; it < c->opt.cg_iters; ++it) {
+    cofem_status st;
+    if ((st = conv_halo_exchange(c, K)) != COFEM_OK) return st;
+    if ((st = conv_fft_apply(c, 0, 1, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if ((st = conv_fft_apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if ((st = sharded_finish(c, m, 1, it)) != COFEM_OK) return st;
+    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->stream, KC_MEAN);
+    if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
+    else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
+    if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
+    if ((st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
+  }
+  if (c->P != P_entry) { c->Pb = c->P; c->P = P_entry; }
+  if (c->p0 != p0_entry) { c->p0b = c->p0; c->p0 = p0_entry; }
   return COFEM_OK;
 }
 
@@ -632,13 +659,19 @@ const char* cofem_kernel_class_name(int32_t cls) {
 const char* cofem_last_error(cofem_ctx ctx) { return ctx ? ctx->c.err.c_str() : g_err.c_str(); }
 
 static void free_all(Ctx* c) {
+  // the captured graph references NCCL work of the communicator: drain and drop it first
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->work) cudaStreamSynchronize(c->work);
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
   comm_destroy(c);
   dense_tc_free(c);
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
-                  c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum};
+                  c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
+                  c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -670,8 +703,8 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
-  if (opt->nccl_id || op->D_global) {          // column-sharded dense mode (comm.cu)
-    if (op->kind != COFEM_OP_DENSE) { c->err = "sharded mode: DENSE operators only"; return COFEM_ERR_UNSUPPORTED; }
+  if (opt->nccl_id || op->D_global) {          // column-sharded dense / D-sharded conv mode (comm.cu)
+    if (op->kind == COFEM_OP_DCT2_MASKED) { c->err = "sharded mode: DENSE or CIRCCONV operators only"; return COFEM_ERR_UNSUPPORTED; }
     if (!opt->nccl_id || opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) {
       c->err = "sharded mode: need nccl_id and 0 <= rank < world"; return COFEM_ERR_INVALID;
     }
@@ -680,6 +713,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
     }
     if (opt->probe_precision) { c->err = "sharded mode: fp32 probes only"; return COFEM_ERR_UNSUPPORTED; }
     c->sharded = true; c->d_offset = op->d_offset; c->D_global = op->D_global;
+    c->rank = opt->rank; c->world = opt->world;
   }
   c->probe64 = opt->probe_precision != 0;
   c->Kcap = opt->max_probes; c->m_cap = c->Kcap + 1;
@@ -711,6 +745,17 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
   c->part_stride = std::max(c->vec_grid, 1);
 
+  if (c->sharded) {     // the communicator first: the D-sharded conv setup exchanges y halos
+    cofem_status cst = comm_init(c, opt->rank, opt->world, opt->nccl_id);
+    if (cst != COFEM_OK) return cst;
+    if (c->kind == COFEM_OP_CIRCCONV) {
+      const size_t tp = c->probe64 ? 8 : 4;
+      char* p;
+      ALLOC(p, 2 * (size_t)c->Kcap * 192 * tp); c->halo_send = p;
+      ALLOC(p, 2 * (size_t)c->Kcap * 192 * tp); c->halo_recv = p;
+      ALLOC(c->halo_send0, 2 * 192); ALLOC(c->halo_recv0, 2 * 192);
+    }
+  }
   // y to device
   const float* y_dev = y;
   float* y_tmp = nullptr;
@@ -779,9 +824,12 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   ALLOC(c->part, (size_t)c->m_cap * c->part_stride);
   if (c->sharded) {
     ALLOC(c->colsum, MAXM);
-    if (!c->dense_tc) { c->err = "sharded mode needs the tensor-core dense path (D % 4 == 0, K <= 128)"; return COFEM_ERR_UNSUPPORTED; }
-    cofem_status cst = comm_init(c, opt->rank, opt->world, opt->nccl_id);
-    if (cst != COFEM_OK) return cst;
+    if (c->kind == COFEM_OP_DENSE && !c->dense_tc) {
+      c->err = "sharded mode needs the tensor-core dense path (D % 4 == 0, K <= 128)"; return COFEM_ERR_UNSUPPORTED;
+    }
+    if (c->kind == COFEM_OP_CIRCCONV && !c->fast_conv) {
+      c->err = "D-sharded convolution needs the FFT path (local D >= 2048, ntaps <= 64)"; return COFEM_ERR_UNSUPPORTED;
+    }
   }
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());

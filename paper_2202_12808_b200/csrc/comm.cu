@@ -22,7 +22,12 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -38,9 +43,15 @@ static NcclApi& nccl(std::string& err) {
   api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
   api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+  api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString && api.Send &&
+           api.Recv && api.GroupStart && api.GroupEnd;
   if (!api.ok) err = "libnccl.so.2 lacks required symbols";
   return api;
 }
@@ -61,7 +72,9 @@ void comm_destroy(Ctx* c) {
   if (!c->comm) return;
   std::string e;
   NcclApi& a = nccl(e);
-  if (a.ok) a.CommDestroy((ncclComm_t)c->comm);
+  // ncclCommAbort does not wait on peers (a rank being torn down must not block on the
+  // others' progress, e.g. at interpreter exit); fall back to ncclCommDestroy
+  if (a.ok) (a.CommAbort ? a.CommAbort : a.CommDestroy)((ncclComm_t)c->comm);
   c->comm = nullptr;
 }
 
@@ -72,6 +85,27 @@ cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype) {
   ncclResult_t r = a.AllReduce(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, ncclSum, (ncclComm_t)c->comm,
                                c->stream);
   if (r != ncclSuccess) { c->err = std::string("ncclAllReduce: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
+  return COFEM_OK;
+}
+
+// Ring halo exchange (D-sharded convolution): this rank's first block goes to the left
+// neighbour (it is that rank's right halo), its last block to the right neighbour; the
+// matching blocks arrive in recv_left / recv_right.  count elements of dtype per side.
+cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, void* recv_left, void* recv_right,
+                       size_t count, int dtype) {
+  NcclApi& a = nccl(c->err);
+  if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
+  const int left = (c->rank + c->world - 1) % c->world, right = (c->rank + 1) % c->world;
+  const ncclDataType_t t = dtype ? ncclFloat64 : ncclFloat32;
+  ncclComm_t cm = (ncclComm_t)c->comm;
+  ncclResult_t r = a.GroupStart();
+  if (r == ncclSuccess) r = a.Send(send_left, count, t, left, cm, c->stream);
+  if (r == ncclSuccess) r = a.Recv(recv_right, count, t, right, cm, c->stream);
+  if (r == ncclSuccess) r = a.Send(send_right, count, t, right, cm, c->stream);
+  if (r == ncclSuccess) r = a.Recv(recv_left, count, t, left, cm, c->stream);
+  ncclResult_t r2 = a.GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) { c->err = std::string("NCCL halo exchange: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
   return COFEM_OK;
 }
 

@@ -104,6 +104,10 @@ struct Ctx {
   int64_t d_offset = 0, D_global = 0;
   void* comm = nullptr;                 // ncclComm_t
   double* colsum = nullptr;             // [MAXM] per-column totals of this rank
+  int rank = 0, world = 1;
+  // D-sharded convolution (op_conv_fft.cu): per column [side][r | p | dinv][64] halo records
+  void* halo_send = nullptr; void* halo_recv = nullptr;        // probe precision, [K][2][3][64]
+  double* halo_send0 = nullptr; double* halo_recv0 = nullptr;  // mean column (fp64), [2][3][64]
 
   // host mirrors for the report
   std::vector<ColState> cs_host;
@@ -245,10 +249,13 @@ cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_
 bool conv_fft_eligible(const Ctx* c);
 cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g);
 cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
+cofem_status conv_halo_exchange(Ctx* c, int K);
 
 cofem_status comm_init(Ctx* c, int rank, int world, const uint8_t* id);
 void comm_destroy(Ctx* c);
 cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype);
+cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, void* recv_left, void* recv_right,
+                       size_t count, int dtype);
 // after a per-column reduction written to c->colsum: sum over ranks, then apply it (mode:
 // 0 = rho0 (init), 1 = gamma -> freeze rule / step length, 2 = rho' -> b)
 cofem_status sharded_finish(Ctx* c, int m, int mode, int iter);

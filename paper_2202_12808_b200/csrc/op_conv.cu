@@ -18,13 +18,14 @@ constexpr int CONV_TILE = CONV_THREADS * CONV_PER_THREAD;
 constexpr int CONV_MAXH = 63;
 
 // b0_i = beta (Phi^T y)_i = beta sum_j h_j y_{(i+j) mod D}  (Eq. 5), colsq_i = sum_j h_j^2
-__global__ void k_conv_setup(const float* __restrict__ h, int T, const float* __restrict__ y, int64_t D, double beta,
-                             double sumsq, double* __restrict__ b0, double* __restrict__ colsq) {
+__global__ void k_conv_setup(const float* __restrict__ h, int T, const float* __restrict__ y, int64_t D, int64_t Dwrap,
+                             double beta, double sumsq, double* __restrict__ b0, double* __restrict__ colsq) {
+  // Dwrap: period of y's indexing (D; D-sharded: D + 64, y extended by the right halo)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D; i += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int j = 0; j < T; ++j) {
       int64_t idx = i + j;
-      if (idx >= D) idx -= D;
+      if (idx >= Dwrap) idx -= Dwrap;
       acc += (double)h[j] * (double)y[idx];
     }
     b0[i] = beta * acc;
@@ -110,9 +111,30 @@ cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host) {
     double* gp; cudaMalloc(&gp, g.size() * 8); cudaMemcpy(gp, g.data(), g.size() * 8, cudaMemcpyHostToDevice);
     cudaFree(c->g32); c->g32 = reinterpret_cast<float*>(gp);
   }
+  const float* y_use = y_dev;
+  float* y_ext = nullptr;
+  int64_t Dwrap = c->D;
+  if (c->sharded) {   // D-sharded: b0_i needs y up to i + 63 -> the right neighbour's first 64 samples
+    if (c->D < 2048 || c->ntaps > 64) { c->err = "D-sharded convolution: local D >= 2048 and ntaps <= 64"; return COFEM_ERR_UNSUPPORTED; }
+    float* sbuf;
+    if (cudaMalloc(&y_ext, (c->D + 64) * sizeof(float)) != cudaSuccess || cudaMalloc(&sbuf, 128 * sizeof(float)) != cudaSuccess) {
+      c->err = "cudaMalloc y halo"; return COFEM_ERR_OOM;
+    }
+    cudaMemcpyAsync(y_ext, y_dev, c->D * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
+    cudaMemcpyAsync(sbuf, y_dev, 64 * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
+    cudaMemcpyAsync(sbuf + 64, y_dev + c->D - 64, 64 * sizeof(float), cudaMemcpyDeviceToDevice, c->stream);
+    float* left_unused;
+    cudaMalloc(&left_unused, 64 * sizeof(float));
+    cofem_status hs = comm_halo(c, sbuf, sbuf + 64, left_unused, y_ext + c->D, 64, 0);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(sbuf); cudaFree(left_unused);
+    if (hs != COFEM_OK) { cudaFree(y_ext); return hs; }
+    y_use = y_ext; Dwrap = c->D + 64;
+  }
   launch_begin(c, KC_SETUP);
-  k_conv_setup<<<c->num_sms * 8, 256, 0, c->stream>>>(c->taps, T, y_dev, c->D, c->beta, sumsq, c->b0, c->colsq);
+  k_conv_setup<<<c->num_sms * 8, 256, 0, c->stream>>>(c->taps, T, y_use, c->D, Dwrap, c->beta, sumsq, c->b0, c->colsq);
   launch_end(c, KC_SETUP);
+  if (y_ext) { cudaStreamSynchronize(c->stream); cudaFree(y_ext); }
   if (check_launch(c, "k_conv_setup")) return COFEM_ERR_CUDA;
   const int grid = (int)((c->D + CONV_TILE - 1) / CONV_TILE);
   c->part_stride = std::max(c->part_stride, grid);

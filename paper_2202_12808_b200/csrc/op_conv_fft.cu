@@ -38,6 +38,11 @@ struct ConvArgs {
   const void* P; void* Pn; const void* R; const void* dinvp; void* Q;
   const void* tab32; const void* tab64;
   ColState* cs; double* part; int stride; unsigned* counter; int iter;
+  // D-sharded mode: D is this rank's slice; samples outside [0, D) come from the received
+  // halo records [side][r | p | dinv][64] (side 0: the 64 before, 1: the 64 after), and
+  // per-column totals go to colsum (summed over ranks, then finished)
+  const void* halo; const double* halo0; double* colsum;
+  int64_t halo_side;   // elements between the side-0 and side-1 blocks of `halo` ([side][K][3][64])
 };
 
 template <typename T> struct CCol { const T* p; T* pn; const T* r; const T* dinv; const T* al; T* q; };
@@ -75,6 +80,14 @@ __global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int
     const int64_t o0 = blk * V, w0 = o0 - HALO;                         // outputs [o0, o0+V), window [w0, w0+1024)
     const int nvalid = (int)min((int64_t)V, a.D - o0);
     const bool fast = w0 >= 0 && w0 + L <= a.D;
+    const T* hal = nullptr;                                             // this column's halo records (sharded)
+    int64_t hside = 0;
+    if (a.halo) {
+      if constexpr (sizeof(T) == 8) {
+        if (j == 0) { hal = a.halo0; hside = 192; }
+        else { hal = (const T*)a.halo + (int64_t)(j - 1) * 192; hside = a.halo_side; }
+      } else { hal = (const T*)a.halo + (int64_t)(j - 1) * 192; hside = a.halo_side; }
+    }
     const T bb = (T)ci.b[jj];
     // ---- load the window as packed complex z[n] (n = ja + 64 r, jb + 64 r), fused direction update
     cplx<T> va[8], vb[8];
@@ -90,13 +103,29 @@ __global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int
           i0 = (w0 + 2 * n) % a.D; if (i0 < 0) i0 += a.D;
           i1 = i0 + 1 == a.D ? 0 : i0 + 1;
         }
-        if (fast && sizeof(T) == 4) {
-          const float2 v = *reinterpret_cast<const float2*>(c.p + i0);
-          x0 = (T)v.x; x1 = (T)v.y;
-        } else { x0 = c.p[i0]; x1 = c.p[i1]; }
-        if (dir) {                                                      // a6: p = M^-1 r + b p
-          x0 = c.dinv[i0] * c.r[i0] + bb * x0;
-          x1 = c.dinv[i1] * c.r[i1] + bb * x1;
+        if (!fast && hal) {                                             // sharded edge window: halo records
+          const int64_t wi = w0 + 2 * n;
+          T v2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t i = wi + e;
+            T pv, rv, dv;
+            if (i >= 0 && i < a.D) { pv = c.p[i]; rv = c.r[i]; dv = c.dinv[i]; }
+            else if (i < 0 && i >= -64) { const T* h = hal + (64 + i); rv = h[0]; pv = h[64]; dv = h[128]; }
+            else if (i >= a.D && i < a.D + 64) { const T* h = hal + hside + (i - a.D); rv = h[0]; pv = h[64]; dv = h[128]; }
+            else { pv = 0; rv = 0; dv = 0; }                          // beyond the halo: affects invalid outputs only
+            v2[e] = dir ? dv * rv + bb * pv : pv;
+          }
+          x0 = v2[0]; x1 = v2[1];
+        } else {
+          if (fast && sizeof(T) == 4) {
+            const float2 v = *reinterpret_cast<const float2*>(c.p + i0);
+            x0 = (T)v.x; x1 = (T)v.y;
+          } else { x0 = c.p[i0]; x1 = c.p[i1]; }
+          if (dir) {                                                    // a6: p = M^-1 r + b p
+            x0 = c.dinv[i0] * c.r[i0] + bb * x0;
+            x1 = c.dinv[i1] * c.r[i1] + bb * x1;
+          }
         }
         if (sl) vb[r] = {x0, x1}; else va[r] = {x0, x1};
       }
@@ -175,7 +204,10 @@ __global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int
   for (int jj = warp; jj < a.ncols; jj += NW) {
     const int j = j0 + jj;
     const double tot = reduce_partials(a.part + (int64_t)j * a.stride, gridDim.x);
-    if (lane == 0 && !ci.frozen[jj]) { ColState cc = a.cs[j]; finish_gamma(cc, tot, a.iter); a.cs[j] = cc; }
+    if (lane == 0) {
+      if (a.colsum) a.colsum[j] = tot;                                  // sharded: summed over ranks, then finished
+      else if (!ci.frozen[jj]) { ColState cc = a.cs[j]; finish_gamma(cc, tot, a.iter); a.cs[j] = cc; }
+    }
   }
   if (threadIdx.x == 0) *a.counter = 0u;
 }
@@ -215,6 +247,50 @@ template <typename T> static size_t smem_bytes() { return (size_t)NW * WREG * si
 
 }  // namespace cfft
 
+// Halo records of every column ([side][column][r | p | dinv][64]): side 0 = this rank's first
+// 64 samples (the left neighbour's right halo), side 1 = its last 64 (the right neighbour's
+// left halo).  Probe columns in probe precision, the mean column in its own fp64 buffer.
+template <typename T>
+__global__ void k_conv_pack_halo(int64_t D, int64_t Dp, const T* __restrict__ R, const T* __restrict__ P,
+                                 const T* __restrict__ dinv, T* __restrict__ out, int64_t side_stride,
+                                 const double* __restrict__ r0, const double* __restrict__ p0,
+                                 const double* __restrict__ dinv64, double* __restrict__ out0) {
+  const int j = blockIdx.x;                 // 0: mean column, 1..K probes
+  for (int t = threadIdx.x; t < 2 * 64; t += blockDim.x) {
+    const int side = t >> 6, e = t & 63;
+    const int64_t i = side ? D - 64 + e : e;
+    if (j == 0) {
+      double* o = out0 + side * 192 + e;
+      o[0] = r0[i]; o[64] = p0[i]; o[128] = dinv64[i];
+    } else {
+      T* o = out + side * side_stride + (int64_t)(j - 1) * 192 + e;
+      const int64_t b = (int64_t)(j - 1) * Dp + i;
+      o[0] = R[b]; o[64] = P[b]; o[128] = dinv[i];
+    }
+  }
+}
+
+// Pack and exchange the halo records of all K + 1 columns with both ring neighbours (one
+// NCCL group per precision), on the context stream.
+cofem_status conv_halo_exchange(Ctx* c, int K) {
+  const int64_t side = (int64_t)c->Kcap * 192;
+  if (c->probe64)
+    k_conv_pack_halo<double><<<K + 1, 128, 0, c->stream>>>(c->D, c->Dp, (const double*)c->R, (const double*)c->P,
+                                                           (const double*)c->dinvp, (double*)c->halo_send, side, c->r0,
+                                                           c->p0, c->dinv64, c->halo_send0);
+  else
+    k_conv_pack_halo<float><<<K + 1, 128, 0, c->stream>>>(c->D, c->Dp, (const float*)c->R, (const float*)c->P,
+                                                          (const float*)c->dinvp, (float*)c->halo_send, side, c->r0,
+                                                          c->p0, c->dinv64, c->halo_send0);
+  if (check_launch(c, "k_conv_pack_halo")) return COFEM_ERR_CUDA;
+  const size_t tp = c->probe64 ? 8 : 4;
+  char* sp = (char*)c->halo_send;
+  char* rp = (char*)c->halo_recv;
+  cofem_status st = comm_halo(c, sp, sp + side * tp, rp, rp + side * tp, (size_t)K * 192, c->probe64 ? 1 : 0);
+  if (st != COFEM_OK) return st;
+  return comm_halo(c, c->halo_send0, c->halo_send0 + 192, c->halo_recv0, c->halo_recv0 + 192, 192, 1);
+}
+
 bool conv_fft_eligible(const Ctx* c) { return c->D >= 2048 && c->ntaps <= 64 && !getenv("COFEM_CONV_DIRECT"); }
 
 cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g) {
@@ -243,6 +319,9 @@ cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStre
   a.tab32 = c->conv_tab32; a.tab64 = c->conv_tab64;
   a.cs = c->cs; a.part = c->part; a.stride = c->part_stride; a.iter = iter;
   a.counter = c->counters + MAXM + 2 + (j0 == 0 ? 1 : 0);
+  a.halo = c->sharded ? c->halo_recv : nullptr; a.halo0 = c->sharded ? c->halo_recv0 : nullptr;
+  a.halo_side = (int64_t)c->Kcap * 192;
+  a.colsum = c->sharded ? c->colsum : nullptr;
   const bool f64 = j0 == 0 || c->probe64;
   const void* fn = f64 ? (const void*)k_conv_fft<double> : (const void*)k_conv_fft<float>;
   const size_t sm = f64 ? smem_bytes<double>() : smem_bytes<float>();

@@ -164,3 +164,64 @@ def test_column_sharded_gloo_world2_equals_single(tmp_path):
     emu, es, _ = estep(DenseOp(w.phi), w.y, w.beta, alpha, w.K, 11, 0, w.U)
     rel = lambda x, y: np.linalg.norm(x - y) / np.linalg.norm(y)
     assert rel(mu, emu) < 1e-8 and rel(s, es) < 1e-8, (rel(mu, emu), rel(s, es))
+
+
+# ---------------------------------------------------------------- D-sharded convolution (halo exchange)
+def _halo_worker(rank, world, port, out):
+    """One rank of the D-sharded Gram apply q = beta g * p + alpha o p (g = autocorr(h), 127
+    taps) following comm_halo's ring schedule: send the first 64 samples to the left
+    neighbour and the last 64 to the right one, receive the right / left halos, convolve the
+    extended window, keep the rank's own outputs.  gloo point-to-point stands in for NCCL."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    import synth
+    from paper_2202_12808_b200.dist import column_shard
+    w = synth.circconv(3000, 64, 5, K=2, U=1, T=1, seed=5)
+    d0, Dl = column_shard(w.D, world, rank)
+    rng = np.random.default_rng(7)
+    p_full = rng.standard_normal(w.D)
+    alpha = rng.uniform(0.5, 2.0, w.D)
+    p = p_full[d0:d0 + Dl]
+    left, right = (rank - 1) % world, (rank + 1) % world
+    send_l, send_r = torch.from_numpy(p[:64].copy()), torch.from_numpy(p[-64:].copy())
+    recv_l, recv_r = torch.zeros(64, dtype=torch.float64), torch.zeros(64, dtype=torch.float64)
+    reqs = [dist.isend(send_l, left), dist.isend(send_r, right), dist.irecv(recv_r, right), dist.irecv(recv_l, left)]
+    for r in reqs:
+        r.wait()
+    ext = np.concatenate([recv_l.numpy(), p, recv_r.numpy()])      # samples d0-64 .. d0+Dl+63
+    h = w.taps.astype(np.float64)
+    g = np.correlate(h, h, mode="full")                             # g_l, l = -63 .. 63
+    H = len(h) - 1
+    q = np.array([np.dot(g, ext[64 + i - H:64 + i + H + 1]) for i in range(Dl)])
+    q = w.beta * q + alpha[d0:d0 + Dl] * p
+    gam = torch.tensor([np.dot(p, q)])
+    dist.all_reduce(gam)                                           # gamma = p^T q over ranks
+    full = torch.zeros(w.D, dtype=torch.float64)
+    full[d0:d0 + Dl] = torch.from_numpy(q)
+    dist.all_reduce(full)
+    if rank == 0:
+        np.save(out, np.concatenate([full.numpy(), gam.numpy()]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_d_sharded_conv_halo_gloo(tmp_path, world):
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = str(tmp_path / "h0.npy")
+    mp.start_processes(_halo_worker, args=(world, port, out), nprocs=world, join=True, start_method="spawn")
+    res = np.load(out)
+    q, gam = res[:-1], res[-1]
+    import synth
+    from oracle.operators import CircConvOp, gram_apply
+    w = synth.circconv(3000, 64, 5, K=2, U=1, T=1, seed=5)
+    rng = np.random.default_rng(7)
+    p = rng.standard_normal(w.D)
+    alpha = rng.uniform(0.5, 2.0, w.D)
+    ref = gram_apply(CircConvOp(w.taps, w.D), w.beta, alpha, p[:, None])[:, 0]
+    assert np.linalg.norm(q - ref) / np.linalg.norm(ref) < 1e-12
+    assert abs(gam - p @ ref) / abs(p @ ref) < 1e-12

@@ -311,3 +311,38 @@ def test_column_sharded_path_world1():
     omu, os_ = X[:, 0], np.mean(P * X[:, 1:], axis=1)
     assert rel(m_dev.cpu().numpy(), omu) <= 1e-4 and rel(s_dev.cpu().numpy(), os_) <= 1e-4, \
         (rel(m_dev.cpu().numpy(), omu), rel(s_dev.cpu().numpy(), os_))
+
+
+def test_d_sharded_conv_path_world1():
+    """D-sharded convolution (halo exchange through NCCL send/recv with both ring neighbours,
+    rank sums of gamma / rho') on a 1-rank communicator: the ring closes on itself, so the
+    rank must reproduce the single-GPU circular convolution (identical up to FFT rounding in
+    the edge windows); a rank holding samples [128, D) must solve its own circular sub-system
+    with globally indexed probes (reading R8)."""
+    from oracle.cofem import jacobi_diag, mean_rhs, pcg
+    from oracle.operators import gram_apply
+    from paper_2202_12808_b200 import OP_CIRCCONV, Context, get_unique_id
+    w = synth.circconv(20000, 64, 20, K=8, U=150, T=3, seed=4)
+    mu, s = gpu_estep(ctx_of(w), w, np.ones(w.D), 8, 5, 0)
+    sh = ctx_of(w, rank=0, world=1, nccl_id=get_unique_id(), d_offset=0, D_global=w.D)
+    mu2, s2 = gpu_estep(sh, w, np.ones(w.D), 8, 5, 0)
+    assert rel(mu2, mu) <= 1e-6 and rel(s2, s) <= 1e-5, (rel(mu2, mu), rel(s2, s))
+    a, m_, s_ = gpu_em(ctx_of(w), w, 2, 8, 6)
+    a2, m2, s2_ = gpu_em(sh, w, 2, 8, 6)
+    assert rel(1 / a2, 1 / a) <= 1e-4 and rel(m2, m_) <= 1e-4
+    d0 = 128
+    Dl = w.D - d0
+    y_r = np.ascontiguousarray(w.y[d0:])
+    part = Context(OP_CIRCCONV, Dl, Dl, y_r, w.beta, taps=w.taps, cg_iters=w.U, max_probes=8,
+                   rank=0, world=1, nccl_id=get_unique_id(), d_offset=d0, D_global=w.D)
+    a_dev = torch.ones(Dl, dtype=torch.float64, device="cuda")
+    m_dev, s_dev = dev(Dl), dev(Dl)
+    part.estep(a_dev, 8, 5, 0, m_dev, s_dev)
+    op = CircConvOp(w.taps, Dl)
+    alpha = np.ones(Dl)
+    P = rademacher_probes(w.D, 8, 5, 0)[d0:]
+    B = np.concatenate([mean_rhs(op, y_r, w.beta)[:, None], P], axis=1)
+    X, _ = pcg(lambda V: gram_apply(op, w.beta, alpha, V), B, jacobi_diag(op, w.beta, alpha), w.U)
+    omu, os_ = X[:, 0], np.mean(P * X[:, 1:], axis=1)
+    assert rel(m_dev.cpu().numpy(), omu) <= 1e-4 and rel(s_dev.cpu().numpy(), os_) <= 1e-4, \
+        (rel(m_dev.cpu().numpy(), omu), rel(s_dev.cpu().numpy(), os_))
