@@ -70,11 +70,14 @@ __global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int
   const int64_t nblk = (a.D + V - 1) / V;
   const int64_t ngrp = (nblk + NW - 1) / NW;
   T* reg = sm + warp * WREG;
+  // work items column-fastest: the CTAs in flight cover a narrow range of block groups over
+  // all columns, so the shared 1/diag and alpha windows (64 MB each at D = 2^24) are read
+  // from HBM about once per apply instead of once per column (L2 hits for the others)
   for (int64_t w = blockIdx.x; w < (int64_t)a.ncols * ngrp; w += gridDim.x) {
-    const int jj = (int)(w / ngrp);
+    const int jj = (int)(w % a.ncols);
     if (ci.frozen[jj]) continue;                                        // CTA-uniform
     const int j = j0 + jj;
-    const int64_t blk = (w % ngrp) * NW + warp;
+    const int64_t blk = (w / a.ncols) * NW + warp;
     if (blk >= nblk) continue;                                          // warp-uniform
     const CCol<T> c = ccol<T>(a, j);
     const int64_t o0 = blk * V, w0 = o0 - HALO;                         // outputs [o0, o0+V), window [w0, w0+1024)
