@@ -47,7 +47,7 @@ typedef enum {
   COFEM_OK = 0,
   COFEM_ERR_INVALID = 1,     /* bad argument / dimension mismatch */
   COFEM_ERR_CUDA = 2,        /* CUDA runtime error */
-  COFEM_ERR_NCCL = 3,        /* reserved (collectives are done by the caller's process group) */
+  COFEM_ERR_NCCL = 3,        /* NCCL unavailable or a library-owned collective failed (sharded modes) */
   COFEM_ERR_NUMERIC = 4,     /* NaN/Inf in the CG recurrence */
   COFEM_ERR_OOM = 5,         /* device allocation failed */
   COFEM_ERR_UNSUPPORTED = 6  /* valid but not implemented (e.g. DCT grid not a power of two) */

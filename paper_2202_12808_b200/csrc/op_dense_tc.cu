@@ -44,13 +44,31 @@ constexpr int TMEM_COLS = 512;             // [0, 256) two accumulator buffers; 
 constexpr int TM_A = 256;
 // The tensor core's fp32 accumulation rounds toward zero, so its error grows linearly with the
 // number of accumulated MMAs (measured: 3xTF32 apply error 6e-5 at N = 8192 with one TMEM
-// accumulator, tools/tc_error_probe.py).  The accumulator is therefore promoted every CH K steps
-// (K = 64) into round-to-nearest fp32 register sums held by the splitter warps, with two TMEM
-// accumulator buffers so the MMAs of the next chunk overlap the promotion.
-constexpr int CH = 2;
-constexpr int PLAG = 3;                    // splitters promote chunk c once they reach step (c + PLAG) CH (protocol checked by simulation)
+// accumulator, tools/tc_error_probe.py).  The accumulator is therefore promoted every pair of
+// K steps (K = 64) into round-to-nearest fp32 register sums held by the splitter warps, with
+// NACC TMEM accumulator buffers so the MMAs of the next pairs overlap the promotion.
+//
+// Pair protocol.  The single MMA-issuing thread is the serial bottleneck of this kernel (each
+// tcgen05.mma costs ~45 issue cycles, a commit ~44, an mbarrier wait ~90; tools/mma_rate.cu,
+// tools/tc_trace.py), so it works on PAIRS of K steps: one split_done wait, 16 MMAs (fused)
+// and ONE commit (pair_done) per pair; pair_done frees the pair's smem stages (producer), its
+// TMEM A buffers (splitters, two pairs later) and is the chunk-complete signal (promotion).
+#ifdef COFEM_TC_EXP_NOSLEEP
+constexpr int SPLIT_SLEEP = 0;
+#else
+constexpr int SPLIT_SLEEP = 40;            // ns between the splitters' barrier polls
+#endif
+constexpr int PLAG = 2;                    // splitters promote pair c at the top of pair c + PLAG (right when its
+                                           // A buffers free up); deadlock-free for 2 <= PLAG < NACC + 3
 
 // ---------------------------------------------------------------- PTX wrappers
+#ifdef COFEM_TC_EXP_TRACE   // timing experiment: clock64 of pipeline events in CTA (0, 0) of k_tc_phiTW
+__device__ long long g_tc_trace[1024][10];
+#define TC_TRACE(kt, ev) \
+  { if (MN && blockIdx.x == 0 && blockIdx.y == 0 && (kt) < 1024) g_tc_trace[kt][ev] = clock64(); }
+#else
+#define TC_TRACE(kt, ev) {}
+#endif
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -66,7 +84,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 // g_tc_stuck and ends the thread instead of hanging the GPU (the host reports it as
 // COFEM_ERR_CUDA with the record).
 __device__ unsigned long long g_tc_stuck[4];
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+// sleep_ns > 0: back off between polls (the splitter warps share issue slots with the
+// single-thread MMA issuer, whose instruction chain must not be starved by spinning).
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int sleep_ns = 0) {
   for (long long spin = 0;; ++spin) {
     uint32_t done;
     asm volatile(
@@ -75,6 +95,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "r"(su32(b)), "r"(parity)
         : "memory");
     if (done) return;
+    if (sleep_ns) __nanosleep(sleep_ns);
     if (spin > (1ll << 24)) {
       if (atomicCAS(&g_tc_stuck[0], 0ull, 1ull) == 0ull) {
         g_tc_stuck[1] = ((unsigned long long)blockIdx.x << 32) | (blockIdx.y << 16) | (threadIdx.x >> 5);
@@ -104,6 +125,22 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// Warp-converged forms: all 32 lanes execute them with warp-uniform operands and elect.sync
+// picks the issuing lane inside the asm block, so ptxas emits a predicated UTCHMMA instead of
+// an ELECT loop per instruction (measured 34 vs 70 cycles per N = 64 MMA, tools/mma_rate.cu).
+__device__ __forceinline__ void mma_ts_e(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(su32(bar))
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -161,12 +198,29 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int bn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-// hi = x rounded to the nearest tf32 (cvt.rna), so lo = x - hi is exact and |lo| <= 2^-12 |x|.
+// hi = x rounded to the nearest tf32 (cvt.rna), so lo = x - hi is exact and |lo| <= 2^-11 |x|.
+// The same rounding (to nearest, ties away) on the integer pipe: add half a tf32 ulp to the
+// magnitude bits and clear the 13 low bits (finite x; the splitters' hot loop avoids the
+// conversion unit, which the fp64 mean-column F2F already keeps busy).
+__device__ __forceinline__ float tf32_hi_alu(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+
+// Kernel modes.  0: bn <= 64, fused N = 2 bn MMAs, 2 accumulator buffers of 128 columns;
+// 1: bn <= 64, three N = bn MMAs per K = 8, 4 buffers of 64 columns (the MMA of pair p waits for
+// the promotion of pair p - 4: never on the critical path); 2: bn <= 128, unfused, 2 x 128.
+// Pipeline depth: 6 stages of <= 33 KB (bn <= 64) or 4 of <= 49 KB (bn <= 128).
+__host__ __device__ constexpr int stages_of(int mode) { return mode == 2 ? 4 : 6; }
+__host__ __device__ constexpr int nacc_of(int mode) { return mode == 1 ? 4 : 2; }
+
+// Accumulator columns promoted (and written by the epilogue) per splitter group: the bn <= 64
+// logical columns split evenly over the 4 groups (128 / 4 in mode 2).
+__host__ __device__ constexpr int cpg_of(int mode) { return mode == 2 ? 32 : 16; }
 
 // Shared-memory plan (dynamic, 1024-aligned):
 // STAGES x [A: MT tiles x 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64 (1 KB)]
@@ -180,18 +234,22 @@ struct Plan {
 
 constexpr int MAXMT = 2;
 struct Bars {
-  uint64_t full[8], empty[8], split_done[NAB], tfree[NAB], chunk_full[2], chunk_free[2];
+  uint64_t full[8], split_done[2], pair_done[4], chunk_free[4];
   uint32_t tmem_base;
   double red[NSPLIT][MAXM];        // epilogue per-warp column partials
-  double mean[NSPLIT][MAXMT][32];  // mean-column partials of the groups
+  uint64_t mean_free[8];           // stage s's mean-column reads done (producer waits before reuse)
+  double mean[NSPLIT][32];         // mean-column partials of the groups
   int last;
 };
 
-// TMEM columns: accumulator of M-tile t at t * ACCW (ACCW = 64 when MT = 2, else 128);
-// A buffer b of M-tile t at TM_A + (b * MT + t) * 64 (hi 32 | lo 32).  NAB buffers
-// are cycled (nab = 6 / MT).
-template <int MT> struct TmemPlan {
-  static constexpr int ACCW = MT == 2 ? 64 : 128;
+// TMEM columns: NACC accumulator buffers (one per in-flight promotion chunk), buffer ab of
+// M-tile t at (ab MT + t) ACCW; A buffer b of M-tile t at TM_A + (b MT + t) 64 (hi 32 | lo 32),
+// NAB / MT buffers cycled.  NACC = 4 (bn <= 64, MT = 1): the MMAs of chunk c + 4 wait for the
+// promotion of chunk c, so the promotion latency never stalls the tensor core.  NACC = 2:
+// 128-column buffers (bn up to 128, or the fused N = 2 bn MMA; COFEM_TC_FUSE).
+template <int MT, int NACC> struct TmemPlan {
+  static_assert(NACC * MT * (MT == 2 || NACC == 4 ? 64 : 128) <= TM_A, "TMEM accumulator budget");
+  static constexpr int ACCW = (MT == 2 || NACC == 4) ? 64 : 128;
   static constexpr int NABU = NAB / MT;
   static constexpr int CPG = ACCW / NGROUP;        // accumulator columns promoted by each splitter group
   static __device__ __forceinline__ uint32_t acc(int ab, int t) { return (ab * MT + t) * ACCW; }
@@ -204,168 +262,204 @@ template <int MT> struct TmemPlan {
 // with the 128-B swizzle (k_tc_phiP, A = Phi, row m = n).  mean_w: the fp64 mean-column
 // operand along K (w0 for phiTW, p0 for phiP).  Returns, for a splitter thread, its fp64
 // mean-column accumulators of row m of each tile (acc0[t]).
-template <bool MN, int MT>
+// Row m's 8 K-values [8h, 8h + 8) of a stage's A tile.  MN: [32 n][128 d] dense, a warp reads
+// 128 contiguous bytes per n (conflict-free); else row m of 128 B with logical 16-B chunk c at
+// physical chunk c ^ (m & 7) (SWIZZLE_128B).
+template <bool MN>
+__device__ __forceinline__ void load_row8(const unsigned char* a, int m, int h, float (&x)[8]) {
+  if (MN) {
+    const float* col = reinterpret_cast<const float*>(a) + m;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = col[(8 * h + i) * BM];
+  } else {
+    const unsigned char* rowp = a + m * 128;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int c = 2 * h + cc;
+      const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
+      x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
+    }
+  }
+}
+
+template <bool MN, int MODE>
 __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUtensorMap* mA, const CUtensorMap* mBh,
                          const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
-                         double (&acc0)[MT], float (&sum)[MT][TmemPlan<MT>::CPG]) {
-  using TP = TmemPlan<MT>;
-  constexpr int NABU = TP::NABU, CPG = TP::CPG;
+                         double (&acc0)[1], float (&sum)[1][cpg_of(MODE)]) {
+  constexpr int NACC = nacc_of(MODE), S = stages_of(MODE);      // compile-time: no integer division on the MMA thread's path
+  using TP = TmemPlan<1, NACC>;
+  constexpr int CPG = cpg_of(MODE);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
-  const int nch = (nk + CH - 1) / CH;
+  const int np = (nk + 1) >> 1;                     // K-step pairs (= promotion chunks)
+  constexpr bool fuse = MODE == 0;
+  acc0[0] = 0.0;
 #pragma unroll
-  for (int t = 0; t < MT; ++t) {
-    acc0[t] = 0.0;
-#pragma unroll
-    for (int i = 0; i < CPG; ++i) sum[t][i] = 0.f;
-  }
+  for (int i = 0; i < CPG; ++i) sum[0][i] = 0.f;
   if (warp == 0) {
     if (lane == 0) {                                  // ---- TMA producer
-      const uint32_t bytes = MT * BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
-      int s = 0;
-      uint32_t ph = 0;
+#ifdef COFEM_TC_EXP_NOTMA
+      const uint32_t bytes = 0;
+#else
+      const uint32_t bytes = BM * BK * 4 + 2 * pl.bn * 128 + BK * 8;
+#endif
       for (int kt = 0; kt < nk; ++kt) {
-        if (kt >= pl.stages) mbar_wait(&bs.empty[s], ph ^ 1);
+        const int s = kt % S;
+        if (kt >= S && !(kt & 1)) {                   // stages of pair (kt - S) / 2 free once its MMAs retired
+          const int q = (kt - S) >> 1;
+          mbar_wait(&bs.pair_done[q & 3], (q >> 2) & 1);
+        }
+        if (kt >= S) mbar_wait(&bs.mean_free[s], ((kt / S) - 1) & 1);
+        TC_TRACE(kt, 8)
         mbar_expect_tx(&bs.full[s], bytes);
         const int kc = k0 + kt * BK;
-#pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          if (MN) tma_load_2d(sm + pl.a_off(s, t), mA, &bs.full[s], row0 + BM * t, kc);
-          else tma_load_2d(sm + pl.a_off(s, t), mA, &bs.full[s], kc, row0 + BM * t);
-        }
+#ifdef COFEM_TC_EXP_NOTMA
+        if (kc >= 0) continue;
+#endif
+        if (MN) tma_load_2d(sm + pl.a_off(s, 0), mA, &bs.full[s], row0, kc);
+        else tma_load_2d(sm + pl.a_off(s, 0), mA, &bs.full[s], kc, row0);
         tma_load_2d(sm + pl.bhi_off(s), mBh, &bs.full[s], kc, 0);
         tma_load_2d(sm + pl.blo_off(s), mBl, &bs.full[s], kc, 0);
         bulk_load(sm + pl.w_off(s), mean_w + kc, BK * 8, &bs.full[s]);
-        if (++s == pl.stages) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {                                  // ---- MMA issuer
+    {                                                 // ---- MMA issuer (whole warp, one lane elected per instruction)
       const uint32_t idesc = idesc_tf32(pl.bn);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int kt = 0; kt < nk; ++kt) {
-        const int b = kt % NABU, c = kt / CH, ab = c & 1, kin = kt % CH;
-        if (kin == 0 && c >= 2) mbar_wait(&bs.chunk_free[ab], ((c >> 1) - 1) & 1);   // promoted by the splitters
-        mbar_wait(&bs.full[s], ph);
-        mbar_wait(&bs.split_done[b], (kt / NABU) & 1);
+      // B_hi and B_lo are adjacent K-major row blocks of the stage, so when the accumulator has
+      // room for 2 bn columns one N = 2 bn MMA forms A_hi [B_hi | B_lo] (hi.hi in columns
+      // [0, bn), hi.lo in [bn, 2 bn), summed at promotion) and one N = bn MMA adds A_lo B_hi:
+      // 2 instructions and 2 A-operand reads per K = 8 instead of 3.
+      const uint32_t idesc2 = idesc_tf32(2 * pl.bn);
+      for (int p = 0; p < np; ++p) {
+        const int ab = p % NACC;
+        if (p >= NACC) mbar_wait(&bs.chunk_free[ab], ((p / NACC) - 1) & 1);   // chunk p - NACC promoted
+        if (lane == 0) TC_TRACE(p, 0)
+        mbar_wait(&bs.split_done[p & 1], (p >> 1) & 1);   // both steps split (hence both stages loaded)
+        if (lane == 0) TC_TRACE(p, 2)
         fence_after();
-        const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
+        const uint32_t d = tmem + TP::acc(ab, 0);
 #pragma unroll
-        for (int t = 0; t < MT; ++t) {
-          const uint32_t d = tmem + TP::acc(ab, t), ahi = tmem + TP::abuf(b, t), alo = ahi + 32;
+        for (int h = 0; h < 2; ++h) {
+          const int kt = 2 * p + h;
+          if (kt >= nk) break;
+          const int s = kt % S;
+          const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
+          const uint32_t ahi = tmem + TP::abuf(kt & 3, 0), alo = ahi + 32;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {        // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
-            const uint64_t dbh = desc_k_sw128(bh + kk * 32), dbl = desc_k_sw128(bl + kk * 32);
-            mma_ts(d, ahi + kk * 8, dbh, idesc, (kin | kk) != 0);
-            mma_ts(d, ahi + kk * 8, dbl, idesc, 1);
-            mma_ts(d, alo + kk * 8, dbh, idesc, 1);
+            const uint64_t dbh = desc_k_sw128(bh + kk * 32);
+            if (fuse) {
+              mma_ts_e(d, ahi + kk * 8, dbh, idesc2, (h | kk) != 0);
+            } else {
+              mma_ts_e(d, ahi + kk * 8, dbh, idesc, (h | kk) != 0);
+              mma_ts_e(d, ahi + kk * 8, desc_k_sw128(bl + kk * 32), idesc, 1);
+            }
+            mma_ts_e(d, alo + kk * 8, dbh, idesc, 1);
           }
         }
-        mma_commit(&bs.empty[s]);                       // smem stage reusable once these MMAs retire
-        mma_commit(&bs.tfree[b]);                       // TMEM A buffers b reusable
-        if (kin == CH - 1 || kt == nk - 1) mma_commit(&bs.chunk_full[ab]);   // chunk c accumulated
-        if (++s == pl.stages) { s = 0; ph ^= 1; }
+        mma_commit_e(&bs.pair_done[p & 3]);             // stages, A buffers and chunk p: all released here
+        if (lane == 0) TC_TRACE(p, 3)
       }
     }
   } else {                                            // ---- splitters / promoters (warps 2 .. 2 + NSPLIT)
-    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m of
-    // every M-tile for the K steps kt = g (mod NGROUP), so NGROUP steps are split concurrently,
-    // and it promotes accumulator columns [g CPG, (g+1) CPG) of row m after every chunk.
+    // warp -> TMEM lane quarter q = warp % 4 (hardware rule) and group g: it owns row m for
+    // the K steps kt = g (mod NGROUP) -- step h = g & 1 of the pairs p = g >> 1 (mod 2), into
+    // TMEM A buffer kt % 4 -- and promotes accumulator columns [g CPG, (g+1) CPG) of row m.
     const int wi = warp - 2, q = warp & 3, g = wi >> 2, m = 32 * q + lane;
     const uint32_t lane_addr = tmem + ((uint32_t)(32 * q) << 16);
-    double acc[MT][2];                                // independent DFMA chains (fixed-order sums below)
-#pragma unroll
-    for (int t = 0; t < MT; ++t) acc[t][0] = acc[t][1] = 0.0;
-    int s = g % pl.stages;
-    uint32_t ph = (g / pl.stages) & 1;
-    int cdone = 0;                                    // chunks promoted so far
-    auto promote = [&](int c) {                       // chunk c: TMEM accumulator -> register sums (RN)
-      const int ab = c & 1;
-      mbar_wait(&bs.chunk_full[ab], (c >> 1) & 1);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};             // independent DFMA chains (fixed-order sums below)
+    int cdone = 0;
+    auto promote = [&](int c) {                       // chunk (pair) c: TMEM accumulator -> register sums (RN)
+      const int ab = c % NACC;
+      mbar_wait(&bs.pair_done[c & 3], (c >> 2) & 1, SPLIT_SLEEP);
+      if (q == 0 && lane == 0) TC_TRACE(4 * c + g, 7)
       fence_after();
 #pragma unroll
-      for (int t = 0; t < MT; ++t)
+      for (int cc = 0; cc < CPG; cc += 16) {
+        if (g * CPG + cc >= pl.bn) continue;           // columns past bn carry nothing
+#ifdef COFEM_TC_EXP_NOPROMO
+        if (cc >= 0) continue;
+#endif
+        float v[16];
+        tmem_ld16(lane_addr + TP::acc(ab, 0) + g * CPG + cc, v);
+        if (fuse) {                                   // + the hi.lo half of the N = 2 bn product
+          float u[16];
+          tmem_ld16(lane_addr + TP::acc(ab, 0) + pl.bn + g * CPG + cc, u);
 #pragma unroll
-        for (int cc = 0; cc < CPG; cc += 16) {
-          float v[16];
-          tmem_ld16(lane_addr + TP::acc(ab, t) + g * CPG + cc, v);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) sum[t][cc + i] += v[i];
+          for (int i = 0; i < 16; ++i) v[i] += u[i];
         }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sum[0][cc + i] += v[i];
+      }
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bs.chunk_free[ab]);
     };
-    for (int kt = g; kt < nk; kt += NGROUP) {
-      // promote the chunks PLAG behind this step (their MMAs need no split work of ours anymore)
-      while (cdone < nch && (cdone + PLAG) * CH <= kt) promote(cdone++);
-      const int b = kt % NABU;
-      mbar_wait(&bs.full[s], ph);
-      if (kt >= NABU) mbar_wait(&bs.tfree[b], ((kt / NABU) - 1) & 1);
-      const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s));
-#pragma unroll
-      for (int t = 0; t < MT; ++t) {
-        const unsigned char* a = sm + pl.a_off(s, t);
+    const int nk2 = 2 * np;                           // an odd nk leaves the second half of the last pair empty
+    for (int kt = g; kt < nk2; kt += NGROUP) {
+      // promote the chunks PLAG pairs behind this step (their MMAs need no split work of ours anymore)
+      while (cdone < np && 2 * (cdone + PLAG) <= kt) promote(cdone++);
+      const int p = kt >> 1;
+      if (kt < nk) {
+        const int s = kt % S;
+        if (p >= 2) mbar_wait(&bs.pair_done[(p - 2) & 3], ((p - 2) >> 2) & 1, SPLIT_SLEEP);   // A buffer free
+        if (q == 0 && lane == 0) TC_TRACE(kt, 5)
+        mbar_wait(&bs.full[s], (kt / S) & 1, SPLIT_SLEEP);
+        if (q == 0 && lane == 0) TC_TRACE(kt, 4)
+        const unsigned char* a = sm + pl.a_off(s, 0);
+        const uint32_t buf = TP::abuf(kt & 3, 0);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           float x[8];
-          if (MN) {   // [32 n][128 d] dense: a warp reads 128 contiguous bytes per n (conflict-free)
-            const float* col = reinterpret_cast<const float*>(a) + m;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) x[i] = col[(8 * h + i) * BM];
-          } else {    // row m of 128 B; logical 16-B chunk c at physical chunk c ^ (m & 7)
-            const unsigned char* rowp = a + m * 128;
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-              const int c = 2 * h + cc;
-              const float4 v = *reinterpret_cast<const float4*>(rowp + ((c ^ (m & 7)) << 4));
-              x[4 * cc] = v.x; x[4 * cc + 1] = v.y; x[4 * cc + 2] = v.z; x[4 * cc + 3] = v.w;
-            }
-          }
+          load_row8<MN>(a, m, h, x);
           float hi[8], lo[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            hi[i] = tf32_hi(x[i]);
+            hi[i] = tf32_hi_alu(x[i]);
             lo[i] = x[i] - hi[i];
-#ifndef COFEM_TC_EXP_NOMEAN
-            acc[t][i & 1] = fma((double)x[i], w[8 * h + i], acc[t][i & 1]);   // mean column, fp64 (R10)
-#endif
           }
-          tmem_st8(lane_addr + TP::abuf(b, t) + 8 * h, hi);
-          tmem_st8(lane_addr + TP::abuf(b, t) + 32 + 8 * h, lo);
+          tmem_st8(lane_addr + buf + 8 * h, hi);
+          tmem_st8(lane_addr + buf + 32 + 8 * h, lo);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bs.empty[s]);       // this warp has consumed its reads of the smem stage
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bs.split_done[b]);
-      s += NGROUP;
-      while (s >= pl.stages) { s -= pl.stages; ph ^= 1; }
+      if (lane == 0) mbar_arrive(&bs.split_done[p & 1]);
+      if (q == 0 && lane == 0) TC_TRACE(kt, 6)
+      if (kt < nk) {   // fp64 mean column (R10) after the MMA's operands are out: off the critical path
+        const int s = kt % S;
+        const double* w = reinterpret_cast<const double*>(sm + pl.w_off(s));
+        const unsigned char* a = sm + pl.a_off(s, 0);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float x[8];
+          load_row8<MN>(a, m, h, x);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i & 3] = fma((double)x[i], w[8 * h + i], acc[i & 3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bs.mean_free[s]);
+      }
     }
-    while (cdone < nch) promote(cdone++);
+    while (cdone < np) promote(cdone++);
     // combine the groups' partial sums of row m in fixed order (g = 0 .. NGROUP-1)
-#pragma unroll
-    for (int t = 0; t < MT; ++t) bs.mean[wi][t][lane] = acc[t][0] + acc[t][1];
+    bs.mean[wi][lane] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * NSPLIT));
+    double v = 0.0;
 #pragma unroll
-    for (int t = 0; t < MT; ++t) {
-      double v = 0.0;
-#pragma unroll
-      for (int gg = 0; gg < NGROUP; ++gg) v += bs.mean[4 * gg + (wi & 3)][t][lane];
-      acc0[t] = v;
-    }
+    for (int gg = 0; gg < NGROUP; ++gg) v += bs.mean[4 * gg + (wi & 3)][lane];
+    acc0[0] = v;
   }
 }
 
 __device__ void setup_cta(Bars& bs, int stages) {
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.empty[s], 1 + 4); }
-    for (int b = 0; b < NAB; ++b) { mbar_init(&bs.split_done[b], 4); mbar_init(&bs.tfree[b], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&bs.chunk_full[b], 1); mbar_init(&bs.chunk_free[b], NSPLIT); }
+    for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.mean_free[s], 4); }
+    for (int b = 0; b < 2; ++b) mbar_init(&bs.split_done[b], 8);      // 2 groups x 4 warps per pair
+    for (int b = 0; b < 4; ++b) { mbar_init(&bs.pair_done[b], 1); mbar_init(&bs.chunk_free[b], NSPLIT); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -397,10 +491,11 @@ struct PhiPArgs {
   int Npad;
 };
 
-template <int MT>
+template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ CUtensorMap mA,
                                                         const __grid_constant__ CUtensorMap mBh,
                                                         const __grid_constant__ CUtensorMap mBl, PhiPArgs a) {
+  constexpr int MT = 1;
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   setup_cta(bs, a.pl.stages);
@@ -408,11 +503,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ 
   const int k0 = split * a.kchunk, k1 = min(a.D, k0 + a.kchunk);
   const int nk = (k1 - k0 + BK - 1) / BK;
   double acc0[MT];
-  float sum[MT][TmemPlan<MT>::CPG];
-  mainloop<false, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, acc0, sum);
+  float sum[MT][cpg_of(MODE)];
+  mainloop<false, MODE>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, k0, nk, a.p0, acc0, sum);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= 2) {
-    constexpr int CPG = TmemPlan<MT>::CPG;
+    constexpr int CPG = cpg_of(MODE);
     const int q = warp & 3, g = (warp - 2) >> 2;
     float* wp = a.Wpart + (size_t)split * a.K * a.Npad;
 #pragma unroll
@@ -484,10 +579,11 @@ struct PhiTWArgs {
   double* colsum;
 };
 
-template <int MT>
+template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__ CUtensorMap mA,
                                                          const __grid_constant__ CUtensorMap mBh,
                                                          const __grid_constant__ CUtensorMap mBl, PhiTWArgs a) {
+  constexpr int MT = 1;
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
@@ -495,12 +591,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
   const int row0 = blockIdx.x * BM * MT;
   const int nk = (a.N + BK - 1) / BK;
   double acc0[MT];
-  float sum[MT][TmemPlan<MT>::CPG];
-  mainloop<true, MT>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0, sum);
+  float sum[MT][cpg_of(MODE)];
+  mainloop<true, MODE>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0, sum);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.K + 1;
   if (warp >= 2) {
-    constexpr int CPG = TmemPlan<MT>::CPG;
+    constexpr int CPG = cpg_of(MODE);
     const int wi = warp - 2, q = warp & 3, g = wi >> 2;
     if (g == 0) {     // mean column (fp64): q0 = beta (Phi^T w0)_d + alpha_d p0_d
       double gm = 0.0;
@@ -600,11 +696,11 @@ static bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t ro
          CUDA_SUCCESS;
 }
 
-static Plan plan_for(int bn, int mt) {
+static Plan plan_for(int bn, int mt, int mode) {
   Plan p;
   p.bn = bn; p.mt = mt;
   p.stage_bytes = mt * BM * BK * 4 + 2 * bn * 128 + 1024;   // + 32 fp64 mean operands, padded to keep 1024-B alignment
-  p.stages = std::min(8, (int)((226 * 1024 - sizeof(Bars)) / p.stage_bytes));
+  p.stages = stages_of(mode);                                // even: whole pairs
   return p;
 }
 static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes + sizeof(Bars); }
@@ -616,6 +712,7 @@ struct DenseTC {
   float *Ph, *Pl, *Wh, *Wl, *Wpart;
   double *W0part, *w0;
   int bn, mt, splits, kchunk, Npad;
+  int mode;
   tc::Plan pl;
 };
 
@@ -639,11 +736,10 @@ cofem_status dense_tc_setup(Ctx* c) {
   memset(t, 0, sizeof *t);
   c->dense_tc = t;
   t->bn = std::max(16, (c->Kcap + 15) / 16 * 16);
-  // 256-row CTAs share each B tile when K <= 64 and the K2 grid still fills the SMs
-  // MT = 2 (256-row CTAs sharing B tiles) hangs with the chunked-promotion protocol (two
-  // TMEM A buffers); it stays off until that is resolved.
-  t->mt = (getenv("COFEM_TC_MT2") && t->bn <= 64) ? 2 : 1;
-  t->pl = plan_for(t->bn, t->mt);
+  t->mt = 1;                                      // one 128-row M-tile per CTA (pair protocol)
+  t->mode = t->bn > 64 ? 2 : getenv("COFEM_TC_FUSE") ? 0 : 1;   // env: timing comparison hook
+  t->pl = plan_for(t->bn, t->mt, t->mode);
+  if (smem_of(t->pl) > 227 * 1024) { c->err = "dense tc: shared-memory plan too large"; return COFEM_ERR_INVALID; }
   t->Npad = (int)((c->N + 31) / 32 * 32);
   const int rows = BM * t->mt;
   const int mtiles = (int)((c->N + rows - 1) / rows);
@@ -674,8 +770,10 @@ cofem_status dense_tc_setup(Ctx* c) {
             make_map(&t->wll, t->Wl, t->Npad, c->Kcap, t->Npad, BK, t->bn);
   if (!ok) { c->err = "cuTensorMapEncodeTiled failed"; return COFEM_ERR_CUDA; }
   const int sm = (int)smem_of(t->pl);
+  cudaFuncSetAttribute(k_tc_phiP<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_tc_phiP<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_tc_phiP<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_tc_phiTW<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_tc_phiTW<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   cudaFuncSetAttribute(k_tc_phiTW<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
@@ -694,8 +792,9 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
   a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
   const dim3 g1((unsigned)((c->N + rows - 1) / rows), t->splits);
-  if (t->mt == 2) k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
-  else k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  if (t->mode == 0) k_tc_phiP<0><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  else if (t->mode == 1) k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  else k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
                                                        c->sharded ? nullptr : t->Wl, t->w0);
   if (c->sharded) {      // W = sum over ranks of Phi_r P_r (SURVEY §8(e) column-sharded dense), then split
@@ -713,8 +812,9 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   a2.colsum = c->sharded ? c->colsum : nullptr;
   launch_begin(c, KC_DENSE_PHIT_W);
   const unsigned g2 = (unsigned)((c->D + rows - 1) / rows);
-  if (t->mt == 2) k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
-  else k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  if (t->mode == 0) k_tc_phiTW<0><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  else if (t->mode == 1) k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  else k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
   if (c->sharded) { cofem_status st = sharded_finish(c, m, 1, iter); if (st != COFEM_OK) return st; }
@@ -732,3 +832,9 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
 }
 
 }  // namespace cofem
+
+#ifdef COFEM_TC_EXP_TRACE
+extern "C" int cofem_tc_trace_dump(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, cofem::tc::g_tc_trace, sizeof(cofem::tc::g_tc_trace));
+}
+#endif
