@@ -24,7 +24,7 @@ def launches(path):
     hd = rows[h]
     ki, vi, ui = hd.index("Kernel Name"), hd.index("Metric Value"), hd.index("Metric Unit")
     agg = collections.defaultdict(lambda: [0, 0.0])
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
     for r in rows[h + 1:]:
         if len(r) <= vi:
             continue
