@@ -281,6 +281,33 @@ def test_c2_full_size_tensor_core_path():
     assert rel(1 / a, 1 / oa) <= 1e-3 and rel(mu, omu) <= 1e-3, (rel(1 / a, 1 / oa), rel(mu, omu))
 
 
+def test_c3_full_size_mean_residual_and_sampled_parity():
+    """Config 3 at full size (8192 x 32768 dense, 1 GiB fp32 Phi, K = 64, U = 300: the bench
+    launch configuration, tcgen05 3xTF32 path).  The oracle cannot run this E-step in
+    seconds, so the properties any correct E-step has are checked instead (Eq. 5-7):
+    (i) mu = x0 solves A x = b0 = beta Phi^T y to the CG's convergence (fp64 mean column);
+    (ii) sampled parity: the K = 1 E-step (probe 1 of the same Philox stream) against the
+    fp64 oracle E-step at the full U, the north_star bar (1e-4 on mu and s)."""
+    from oracle.cofem import mean_rhs
+    w = synth.preset("C3")
+    op = DenseOp(w.phi)
+    ones = np.ones(w.D)
+    b0 = mean_rhs(op, w.y, w.beta)
+
+    def A(x):
+        return w.beta * op.apply_T(op.apply(x[:, None]))[:, 0] + x
+
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, ones, w.K, 0, 0)
+    assert np.all(np.isfinite(s)) and np.all(s > 0)          # diag(A^-1) > 0 (A is SPD)
+    assert rel(A(mu), b0) <= 1e-8, rel(A(mu), b0)
+    ctx1 = ctx_of(w, max_probes=1)
+    mu1, s1 = gpu_estep(ctx1, w, ones, 1, 0, 0)
+    assert rel(mu1, mu) <= 1e-12                              # the mean column ignores K
+    omu, os_, _ = estep(op, w.y, w.beta, ones, 1, 0, 0, w.U)  # sampled: probe 1 only, full U
+    assert rel(mu1, omu) <= 1e-4 and rel(s1, os_) <= 1e-4, (rel(mu1, omu), rel(s1, os_))
+
+
 def test_column_sharded_path_world1():
     """The column-sharded dense path (comm.cu + the sharded finishes of cofem.cu /
     op_dense_tc.cu) on a 1-rank NCCL communicator: (i) with d_offset = 0 it must reproduce
