@@ -234,7 +234,7 @@ struct Plan {
 
 constexpr int MAXMT = 2;
 struct Bars {
-  uint64_t full[8], split_done[2], pair_done[4], chunk_free[4];
+  uint64_t full[8], split_done[4], pair_done[4], chunk_free[4];   // 4 phases apart: no parity aliasing
   uint32_t tmem_base;
   double red[NSPLIT][MAXM];        // epilogue per-warp column partials
   uint64_t mean_free[8];           // stage s's mean-column reads done (producer waits before reuse)
@@ -335,7 +335,7 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
         const int ab = p % NACC;
         if (p >= NACC) mbar_wait(&bs.chunk_free[ab], ((p / NACC) - 1) & 1);   // chunk p - NACC promoted
         if (lane == 0) TC_TRACE(p, 0)
-        mbar_wait(&bs.split_done[p & 1], (p >> 1) & 1);   // both steps split (hence both stages loaded)
+        mbar_wait(&bs.split_done[p & 3], (p >> 2) & 1);   // both steps split (hence both stages loaded)
         if (lane == 0) TC_TRACE(p, 2)
         fence_after();
         const uint32_t d = tmem + TP::acc(ab, 0);
@@ -426,7 +426,7 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       }
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bs.split_done[p & 1]);
+      if (lane == 0) mbar_arrive(&bs.split_done[p & 3]);
       if (q == 0 && lane == 0) TC_TRACE(kt, 6)
       if (kt < nk) {   // fp64 mean column (R10) after the MMA's operands are out: off the critical path
         const int s = kt % S;
@@ -458,7 +458,7 @@ __device__ void setup_cta(Bars& bs, int stages) {
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { mbar_init(&bs.full[s], 1); mbar_init(&bs.mean_free[s], 4); }
-    for (int b = 0; b < 2; ++b) mbar_init(&bs.split_done[b], 8);      // 2 groups x 4 warps per pair
+    for (int b = 0; b < 4; ++b) mbar_init(&bs.split_done[b], 8);      // 2 groups x 4 warps per pair
     for (int b = 0; b < 4; ++b) { mbar_init(&bs.pair_done[b], 1); mbar_init(&bs.chunk_free[b], NSPLIT); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
