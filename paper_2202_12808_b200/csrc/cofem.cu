@@ -478,10 +478,13 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   cudaStream_t ms = serial ? c->stream : c->side;
   CK(cudaEventRecord(c->ev_fork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  static const bool no_mean = getenv("COFEM_EXP_NO_MEAN") != nullptr;   // timing experiment only (results invalid)
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
-    if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
-    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
+    if (!no_mean) {
+      if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
+      update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
+    }
     if ((st = apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
     if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);

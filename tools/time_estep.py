@@ -1,0 +1,33 @@
+"""Time E-steps at a fixed alpha so that runs with different library settings follow identical
+CG trajectories (frozen columns are skipped, so the cost of an E-step depends on alpha):
+    python tools/time_estep.py C4 5 [alpha.pt]
+alpha.pt: if it exists it is loaded, else alpha after 3 EM iterations is computed and saved
+(the steady-state regime of bench.py; alpha = 1 freezes columns early and is unrepresentative)."""
+import os
+import sys
+import torch
+sys.path.insert(0, "/root/repo")
+import synth
+from paper_2202_12808_b200 import Context
+
+w = synth.preset(sys.argv[1] if len(sys.argv) > 1 else "C4")
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+ctx = Context.from_workload(w, max_probes=w.K)
+alpha = torch.ones(w.D, dtype=torch.float64, device="cuda")
+mu, s = torch.empty_like(alpha), torch.empty_like(alpha)
+ap = sys.argv[3] if len(sys.argv) > 3 else None
+if ap and os.path.exists(ap):
+    alpha = torch.load(ap).cuda()
+elif ap:
+    ctx.em(3, w.K, 0, 0, None, alpha, mu, s)
+    torch.save(alpha.cpu(), ap)
+for t in range(2):
+    ctx.estep(alpha, w.K, 0, t, mu, s)
+torch.cuda.synchronize()
+ms = []
+for t in range(reps):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); ctx.estep(alpha, w.K, 0, 2 + t, mu, s); b.record()
+    torch.cuda.synchronize()
+    ms.append(a.elapsed_time(b))
+print("%s E-step at fixed alpha: median %.2f ms (min %.2f) over %d" % (w.name, sorted(ms)[len(ms) // 2], min(ms), reps))
