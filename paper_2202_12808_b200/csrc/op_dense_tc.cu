@@ -53,10 +53,10 @@ constexpr int TM_A = 256;
 // tools/tc_trace.py), so it works on PAIRS of K steps: one split_done wait, 16 MMAs (fused)
 // and ONE commit (pair_done) per pair; pair_done frees the pair's smem stages (producer), its
 // TMEM A buffers (splitters, two pairs later) and is the chunk-complete signal (promotion).
-#ifdef COFEM_TC_EXP_NOSLEEP
-constexpr int SPLIT_SLEEP = 0;
-#else
+#ifdef COFEM_TC_EXP_SLEEP
 constexpr int SPLIT_SLEEP = 40;            // ns between the splitters' barrier polls
+#else
+constexpr int SPLIT_SLEEP = 0;             // spinning on try_wait measured 2 % faster on C3 than a 40 ns back-off
 #endif
 constexpr int PLAG = 2;                    // splitters promote pair c at the top of pair c + PLAG (right when its
                                            // A buffers free up); deadlock-free for 2 <= PLAG < NACC + 3
