@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=1, help="EM iterations of the per-kernel profiled pass")
+    ap.add_argument("--rtol", type=float, default=0.0,
+                    help="NEXT-1: the paper's CG stopping rule eps (per-column freezing, U stays the cap); "
+                         "0 = the BASELINE fixed-U contract")
     return ap.parse_args()
 
 
@@ -242,15 +245,15 @@ def main():
         if w.kind == "dense":
             ctx = Context(OP_DENSE, w.N, Dr, w.y, w.beta, phi=np.ascontiguousarray(w.phi[:, d0:d0 + Dr]),
                           cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
-                          D_global=w.D)
+                          D_global=w.D, cg_rtol=args.rtol)
         else:   # D-sharded circular convolution: 64-sample halos exchanged with both ring neighbours
             ctx = Context(OP_CIRCCONV, Dr, Dr, np.ascontiguousarray(w.y[d0:d0 + Dr]), w.beta, taps=w.taps,
                           cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
-                          D_global=w.D)
+                          D_global=w.D, cg_rtol=args.rtol)
         D = Dr
     else:
         k_off, K_loc = probe_split(w.K, world, rank)
-        ctx = Context.from_workload(w, max_probes=K_loc)
+        ctx = Context.from_workload(w, max_probes=K_loc, cg_rtol=args.rtol)
         D = w.D
     alpha = torch.ones(D, dtype=torch.float64, device=dev)
     mu = torch.empty_like(alpha)
@@ -402,7 +405,7 @@ def main():
                 "config": {"workload": w.name, **w.config(),
                            "parallelism": (("column-sharded x%d" if w.kind == "dense" else "D-sharded x%d") if column
                                            else "probe-parallel x%d") % world,
-                           "K_per_rank": K_loc, "D_per_rank": D,
+                           "K_per_rank": K_loc, "D_per_rank": D, **({"cg_rtol": args.rtol} if args.rtol > 0 else {}),
                            "l2": ("inputs larger than L2 (working set %.0f MB > 126 MB)" % ws_mb if flush is None
                                   else "working set %.1f MB fits in L2: 256 MB flush write before every timed "
                                        "EM iteration, outside its events" % ws_mb)},

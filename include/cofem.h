@@ -92,6 +92,12 @@ typedef struct {
    * an id runs the sharded code path on a 1-rank communicator (tests). */
   int32_t rank, world;
   const uint8_t* nccl_id;
+  /* NEXT-1, the paper's stopping rule ("||A X - B||_F / ||B||_F < eps"), reading R19:
+   * cg_rtol = eps > 0 freezes column j once rho_j <= eps^2 rho_j(0), rho = r^T M^-1 r (with
+   * precond = 0 exactly ||r_j|| <= eps ||b_j||); when every column has frozen the Frobenius
+   * criterion holds and the remaining iterations launch but do no column work.  U stays the cap.
+   * 0 (default): fixed U iterations (BASELINE north_star, R5).  Must be in [0, 1). */
+  double cg_rtol;
 } cofem_options;
 
 /* NCCL unique id for cofem_options.nccl_id (call on one rank, broadcast the 128 bytes).

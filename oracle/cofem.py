@@ -19,6 +19,11 @@ Readings of silent/ambiguous passages:
   R6  Jacobi preconditioner z = r / (beta colsq + alpha) (BASELINE.json); the
       paper's plain CG is precond=False
   R7  M-step floor 1e-12 and clamp 1e12
+  R19 (NEXT-1) the paper's stopping rule ||A X - B||_F / ||B||_F < eps applied per
+      column ("columns that individually converge are frozen"): rtol = eps > 0
+      raises the R5 threshold to tau = eps^2, i.e. freeze column j once
+      rho_j <= eps^2 rho_j(0) with rho = r^T M^-1 r (plain CG: ||r_j|| <= eps ||b_j||); once
+      every column is frozen the Frobenius criterion holds.  rtol = 0: fixed U (R5).
   R9  Algorithm 1 returns alpha after the last M-step and mu, s of the last E-step
 """
 import numpy as np
@@ -103,7 +108,12 @@ def jacobi_diag(op, beta, alpha):
     return beta * op.colsq() + alpha
 
 
-def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=False):
+def tau_of(rtol):
+    """Freeze threshold of R5 / R19: max(1e-30, rtol^2)."""
+    return max(FREEZE_TAU, float(rtol) ** 2)
+
+
+def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=False, rtol=0.0):
     """Simplified E-step (Alg. 1 lines 3-7; Eq. 6-7).
 
     B = [b0 | p_1 .. p_K]  (R2),  X = LinearSolver(A, B) (P:136),
@@ -115,7 +125,7 @@ def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=
     diag = jacobi_diag(op, beta, alpha)
     Pk = rademacher_probes(op.D, K, seed, t, k_offset)
     B = np.concatenate([b0[:, None], Pk], axis=1)
-    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), B, diag, U, precond)
+    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), B, diag, U, precond, tau=tau_of(rtol))
     if rep.nonfinite.any():
         raise FloatingPointError("numerical breakdown in column %d" % int(np.argmax(rep.nonfinite)))
     mu = X[:, 0]
@@ -131,14 +141,14 @@ def mstep(mu, s, den_floor=DEN_FLOOR, alpha_max=ALPHA_MAX):
     return np.minimum(1.0 / den, alpha_max)
 
 
-def cofem_em(op, y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True, trace=None):
+def cofem_em(op, y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True, trace=None, rtol=0.0):
     """Algorithm 1: alpha <- 1; for t in 1..T: E-step with fresh probes
     (probe counter t0 + t), M-step.  Returns (alpha_T, mu, s) where mu, s are
     from the last E-step (R9)."""
     alpha = np.ones(op.D) if alpha_init is None else np.asarray(alpha_init, dtype=np.float64).copy()
     mu = s = None
     for t in range(t0, t0 + T):
-        mu, s, _ = estep(op, y, beta, alpha, K, seed, t, U, precond)
+        mu, s, _ = estep(op, y, beta, alpha, K, seed, t, U, precond, rtol=rtol)
         alpha = mstep(mu, s)
         if trace is not None:
             trace.append((alpha.copy(), mu.copy(), s.copy()))

@@ -42,7 +42,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("cg_iters", ctypes.c_int32), ("precond", ctypes.c_int32), ("den_floor", ctypes.c_double),
                 ("alpha_max", ctypes.c_double), ("probe_precision", ctypes.c_int32),
                 ("max_probes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("cg_rtol", ctypes.c_double)]
 
 
 class _Report(ctypes.Structure):
@@ -140,7 +140,7 @@ class Context:
 
     def __init__(self, kind, N, D, y, beta, phi=None, rows=0, cols=0, obs_idx=None, convention=0, taps=None,
                  cg_iters=100, precond=1, probe_precision=0, max_probes=32, den_floor=1e-12, alpha_max=1e12,
-                 stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None):
+                 stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None, cg_rtol=0.0):
         """Column-sharded dense mode: phi holds this rank's columns
         [d_offset, d_offset + D) of D_global; nccl_id = get_unique_id() from one rank,
         broadcast; the library all-reduces W and the column dots over NCCL itself."""
@@ -165,6 +165,7 @@ class Context:
             int(probe_precision), int(max_probes)
         opt.den_floor, opt.alpha_max = float(den_floor), float(alpha_max)
         opt.rank, opt.world = int(rank), int(world)
+        opt.cg_rtol = float(cg_rtol)
         if nccl_id is not None:
             self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opt.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)

@@ -84,6 +84,7 @@ struct VecArgs {
   ColState* cs; double* part; int part_stride; unsigned* counter;
   double invK;
   double* colsum;   // sharded mode: per-column totals go here (summed over ranks, then finished)
+  double tau;       // freeze threshold on rho / rho0 (ColState::tau)
 };
 
 // Probe-stream parameters of the current E-step, read from device memory so that one
@@ -212,10 +213,11 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
   }
   ColState* cs = a.cs;
   double* colsum = a.colsum;
-  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs, colsum](int j, double v) {
+  const double tau = a.tau;
+  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs, colsum, tau](int j, double v) {
     if (colsum) { colsum[j] = v; return; }
     ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
-    c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+    c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0; c.tau = tau;
     cs[j] = c;
   });
 }
@@ -353,13 +355,14 @@ __global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* 
 }
 
 // Sharded mode: apply the rank-summed per-column totals (same rules as the in-kernel finishes).
-__global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum, int m, int mode, int iter) {
+__global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum, int m, int mode, int iter, double tau) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   const double v = colsum[j];
   ColState c = cs[j];
   if (mode == 0) {
     c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0; c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+    c.tau = tau;
   } else if (mode == 1) {
     finish_gamma(c, v, iter);
   } else {
@@ -372,7 +375,7 @@ __global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum
 cofem_status sharded_finish(Ctx* c, int m, int mode, int iter) {
   cofem_status st = comm_allreduce(c, c->colsum, (size_t)m, 1);
   if (st != COFEM_OK) return st;
-  k_sharded_finish<<<1, 160, 0, c->stream>>>(c->cs, c->colsum, m, mode, iter);
+  k_sharded_finish<<<1, 160, 0, c->stream>>>(c->cs, c->colsum, m, mode, iter, c->freeze_tau);
   return check_launch(c, "k_sharded_finish") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
@@ -390,6 +393,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.cs = c->cs; a.part = c->part; a.part_stride = c->part_stride; a.counter = c->counters + MAXM;
   a.invK = invK;
   a.colsum = c->sharded ? c->colsum : nullptr;
+  a.tau = c->freeze_tau;
   return a;
 }
 
@@ -651,6 +655,7 @@ void cofem_default_options(cofem_options* o) {
   o->cg_iters = 100; o->precond = 1; o->den_floor = 1e-12; o->alpha_max = 1e12;
   o->probe_precision = 0; o->max_probes = 32;
   o->rank = 0; o->world = 1; o->nccl_id = nullptr;
+  o->cg_rtol = 0.0;
 }
 
 const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
@@ -703,9 +708,11 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (!(beta > 0.0) || !isfinite(beta)) { c->err = "beta must be > 0"; return COFEM_ERR_INVALID; }
   if (op->D < 1 || op->N < 1) { c->err = "N, D must be >= 1"; return COFEM_ERR_INVALID; }
   if (opt->cg_iters < 1) { c->err = "cg_iters must be >= 1"; return COFEM_ERR_INVALID; }
+  if (!(opt->cg_rtol >= 0.0 && opt->cg_rtol < 1.0)) { c->err = "cg_rtol must be in [0, 1)"; return COFEM_ERR_INVALID; }
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
+  c->freeze_tau = std::max(FREEZE_TAU, opt->cg_rtol * opt->cg_rtol);
   if (opt->nccl_id || op->D_global) {          // column-sharded dense / D-sharded conv mode (comm.cu)
     if (op->kind == COFEM_OP_DCT2_MASKED) { c->err = "sharded mode: DENSE or CIRCCONV operators only"; return COFEM_ERR_UNSUPPORTED; }
     if (!opt->nccl_id || opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) {
@@ -905,7 +912,7 @@ __global__ void k_reset_cols(ColState* cs, int m) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   ColState c; c.rho = 1.0; c.rho0 = 1.0; c.gamma = 0; c.a = 0; c.b = 0;
-  c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0;
+  c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0; c.tau = FREEZE_TAU;
   cs[j] = c;
 }
 

@@ -32,6 +32,7 @@ struct ColState {
   int frozen_at;    // iteration index, -1 if never
   int nonfinite;    // the freeze was caused by NaN/Inf
   int pad;
+  double tau;       // freeze when !(rho > tau rho0): FREEZE_TAU (R5) or cg_rtol^2 (reading R19)
 };
 
 template <typename T> struct cplx { T x, y; };
@@ -39,6 +40,7 @@ template <typename T> struct cplx { T x, y; };
 // ---------------------------------------------------------------- context
 struct Ctx {
   int kind = 0;
+  double freeze_tau = FREEZE_TAU;   // max(FREEZE_TAU, cg_rtol^2)
   int64_t N = 0, D = 0, Dp = 0;        // Dp: D padded to a multiple of VEC_TILE (zero padding)
   double beta = 0;
   cofem_options opt{};
@@ -167,7 +169,7 @@ __device__ __forceinline__ void finish_gamma(ColState& c, double gamma, int iter
   if (c.frozen) return;
   c.gamma = gamma;
   bool finite = isfinite(gamma) && isfinite(c.rho);
-  bool ok = finite && (gamma > 0.0) && (c.rho > FREEZE_TAU * c.rho0);
+  bool ok = finite && (gamma > 0.0) && (c.rho > c.tau * c.rho0);
   if (!ok) {
     c.frozen = 1; c.frozen_at = iter; c.nonfinite = finite ? 0 : 1; c.a = 0.0;
   } else {

@@ -5,7 +5,7 @@ import pytest
 
 import synth
 from oracle import closed_forms as cf
-from oracle.cofem import cofem_em, estep, mstep, pcg, support
+from oracle.cofem import cofem_em, estep, mstep, pcg, support, tau_of
 from oracle.exact import dense_phi, exact_em, exact_posterior, log_evidence
 from oracle.operators import CircConvOp, DCT2MaskedOp, DenseOp
 from oracle.philox import rademacher_probes
@@ -74,6 +74,52 @@ def test_pcg_freeze_rules():
     # non-finite operator output flags the column
     X, rep = pcg(lambda V: V * np.nan, np.ones((3, 2)), np.ones(3), U=3)
     assert rep.nonfinite.all()
+
+
+# ---------------------------------------------------------------- eps stopping (NEXT-1, reading R19)
+def test_eps_stopping_identity_one_step():
+    """SPEC S:109 with a tolerance: A = I converges in one step; every column freezes at i = 1."""
+    B = np.random.default_rng(1).standard_normal((9, 3))
+    X, rep = pcg(lambda V: V, B, np.ones(9), U=10, precond=False, tau=tau_of(1e-8))
+    assert np.array_equal(X, B) and np.all(rep.frozen_at == 1) and rep.iters_run == 2
+
+
+@pytest.mark.parametrize("precond", [False, True])
+def test_eps_stopping_first_iteration_meeting_the_criterion(precond):
+    """Each column stops at the first iteration where rho <= eps^2 rho0 (plain CG: the recursive
+    ||r_j|| <= eps ||b_j||); its iterate equals the fixed-U iterate with U = that iteration count,
+    one iteration earlier the criterion did not hold, and at the end the paper's Frobenius
+    criterion ||AX - B||_F / ||B||_F < eps holds (checked with the true residual)."""
+    rng = np.random.default_rng(7)
+    D, eps = 40, 1e-6
+    M = rng.standard_normal((D, D))
+    A = M.T @ M + np.eye(D)
+    B = rng.standard_normal((D, 4)) * np.array([1e-3, 1.0, 1e3, 5.0])      # very different column scales
+    diag = np.diag(A).copy()
+    X, rep = pcg(lambda V: A @ V, B, diag, U=4 * D, precond=precond, tau=tau_of(eps))
+    assert np.all(rep.frozen_at > 0) and np.all(rep.frozen_at < 4 * D) and not rep.nonfinite.any()
+    minv = 1.0 / diag if precond else np.ones(D)
+    for j in range(4):
+        u = int(rep.frozen_at[j])
+        Xu, _ = pcg(lambda V: A @ V, B[:, [j]], diag, U=u, precond=precond)
+        assert rel(Xu[:, 0], X[:, j]) < 1e-7        # same recurrence; BLAS order differs with the block width, amplified by kappa
+        Xp, _ = pcg(lambda V: A @ V, B[:, [j]], diag, U=u - 1, precond=precond)
+        r_now, r_prev = B[:, j] - A @ X[:, j], B[:, j] - A @ Xp[:, 0]
+        rho0 = B[:, j] @ (minv * B[:, j])
+        assert r_now @ (minv * r_now) <= eps ** 2 * rho0 * 1.01
+        assert r_prev @ (minv * r_prev) > eps ** 2 * rho0 * 0.99
+    if not precond:
+        assert np.linalg.norm(A @ X - B) / np.linalg.norm(B) < eps
+
+
+def test_eps_zero_is_the_fixed_u_run():
+    rng = np.random.default_rng(2)
+    M = rng.standard_normal((20, 20))
+    A = M.T @ M + np.eye(20)
+    B = rng.standard_normal((20, 3))
+    X0, _ = pcg(lambda V: A @ V, B, np.diag(A).copy(), U=15)
+    X1, _ = pcg(lambda V: A @ V, B, np.diag(A).copy(), U=15, tau=tau_of(0.0))
+    assert np.array_equal(X0, X1) and tau_of(0.0) == 1e-30 and tau_of(1e-3) == 1e-6
 
 
 # ---------------------------------------------------------------- E/M-step
