@@ -11,6 +11,8 @@ import synth
 from paper_2202_12808_b200 import Context
 
 w = synth.preset(sys.argv[1] if len(sys.argv) > 1 else "C4")
+if os.environ.get("TIME_K"):          # emulate one rank of a probe-parallel run (K / world probes)
+    w.K = int(os.environ["TIME_K"])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 ctx = Context.from_workload(w, max_probes=w.K)
 alpha = torch.ones(w.D, dtype=torch.float64, device="cuda")
