@@ -126,6 +126,17 @@ def algorithmic_bytes(cls, w, K_local, D_local=None):
     return None
 
 
+def mean_cost(w):
+    """Effective cost of the fp64 mean system in probe columns, for probe_split_owner.  It runs
+    on a side stream concurrently with the probes, so its cost is the extra time it adds to a
+    rank, measured with tools/time_estep.py (C4 fixed alpha, per-rank E-step): +2.3 ms at 16
+    probes, +3.4 ms at 5, alone 9.7 ms vs ~2 ms per probe column -> ~2 probe columns.  Dense: the
+    mean column rides in every rank's tensor-core kernels anyway (no saving, cost 0)."""
+    if w.kind == "dense":
+        return 0.0
+    return 2.0 if w.kind == "circconv" or (w.rows, w.cols) == (1024, 1024) else 1.0
+
+
 def working_set_bytes(w, K_local, D_local):
     """Bytes one E-step keeps touching: ~5 fp32 vectors per probe column (r, p, q, x, z) plus
     the operator's own storage (dense Phi; the DCT mask and conv taps are negligible)."""
@@ -221,7 +232,7 @@ def main():
 
     import synth
     from paper_2202_12808_b200 import Context
-    from paper_2202_12808_b200.dist import column_shard, probe_split
+    from paper_2202_12808_b200.dist import column_shard, probe_split_owner
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -252,7 +263,9 @@ def main():
                           D_global=w.D, cg_rtol=args.rtol)
         D = Dr
     else:
-        k_off, K_loc = probe_split(w.K, world, rank)
+        # rank 0 owns the mean system (fewer probes), the others run cofem_estep_probes and get mu
+        # by broadcast; mean_cost = its cost in probe columns, measured per operator
+        k_off, K_loc, owns_mean = probe_split_owner(w.K, world, rank, mean_cost(w))
         ctx = Context.from_workload(w, max_probes=K_loc, cg_rtol=args.rtol)
         D = w.D
     alpha = torch.ones(D, dtype=torch.float64, device=dev)
@@ -260,12 +273,19 @@ def main():
     s = torch.empty_like(alpha)
     seed = args.seed
 
+    def probe_estep(a_in, t):
+        if owns_mean:
+            ctx.estep(a_in, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
+        else:
+            ctx.estep_probes(a_in, K_loc, seed, t, s, k_offset=k_off, K_total=w.K)
+        torch.distributed.all_reduce(s)
+        torch.distributed.broadcast(mu, src=0)
+
     def step(t, a_in, a_out, m_out, s_out):
         if world == 1 or column:
             ctx.em(1, w.K, seed, t, a_in, a_out, m_out, s_out)
         else:
-            ctx.estep(a_in, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
-            torch.distributed.all_reduce(s)
+            probe_estep(a_in, t)
             ctx.mstep(mu, s, alpha)
             if a_out is not alpha:
                 a_out.copy_(alpha)
@@ -361,8 +381,7 @@ def main():
             if world == 1 or column:
                 ctx.em(1, w.K, seed, t, a_h, a_h, m_h, s_h)      # h2d alpha; d2h alpha, mu, s
             else:
-                ctx.estep(a_h, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
-                torch.distributed.all_reduce(s)
+                probe_estep(a_h, t)
                 ctx.mstep(mu, s, a_h)
                 m_h.copy_(mu); s_h.copy_(s)
             t += 1
@@ -404,7 +423,8 @@ def main():
                 "data": "synthetic",
                 "config": {"workload": w.name, **w.config(),
                            "parallelism": (("column-sharded x%d" if w.kind == "dense" else "D-sharded x%d") if column
-                                           else "probe-parallel x%d") % world,
+                                           else "probe-parallel x%d" + (", rank 0 owns the mean system"
+                                                                         if world > 1 else "")) % world,
                            "K_per_rank": K_loc, "D_per_rank": D, **({"cg_rtol": args.rtol} if args.rtol > 0 else {}),
                            "l2": ("inputs larger than L2 (working set %.0f MB > 126 MB)" % ws_mb if flush is None
                                   else "working set %.1f MB fits in L2: 256 MB flush write before every timed "

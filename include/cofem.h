@@ -132,6 +132,13 @@ cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* 
 cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
                          int32_t k_offset, int32_t K_total, double* mu, double* s);
 
+/* The same E-step for the probe columns only (probe-parallel ranks that do not own the mean
+ * system): column 0 (b0 = beta Phi^T y) is frozen at once and none of its work is
+ * launched; s is this rank's partial sum as in cofem_estep; mu is not computed (the owner rank
+ * broadcasts it).  Arguments and errors as cofem_estep. */
+cofem_status cofem_estep_probes(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
+                                int32_t k_offset, int32_t K_total, double* s);
+
 /* One batched Gram apply (the CG matrix-matrix product of §3.2; Eq. 7):
  *   q0 = A x0,  Q_k = A X_k  (k < K),   A = beta Phi^T Phi + diag(alpha),
  * through exactly the kernels the E-step uses (mean column in fp64; probe columns in

@@ -61,6 +61,8 @@ SYMBOLS = [
     ("cofem_estep", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
                                    ctypes.c_void_p]),
+    ("cofem_estep_probes", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]),
     ("cofem_mstep", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_apply", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
@@ -202,6 +204,14 @@ class Context:
         self._check(lib().cofem_estep(self._h, _ptr(alpha, np.float64, D, "alpha"), int(K), int(seed), int(t),
                                       int(k_offset), int(K if K_total is None else K_total),
                                       _ptr(mu, np.float64, D, "mu"), _ptr(s, np.float64, D, "s")))
+
+    def estep_probes(self, alpha, K, seed, t, s, k_offset=0, K_total=None):
+        """E-step for the probe columns only (the mean system is owned by another rank): s = this
+        call's partial (1/K_total) sum; mu is not computed."""
+        D = self.D
+        self._check(lib().cofem_estep_probes(self._h, _ptr(alpha, np.float64, D, "alpha"), int(K), int(seed),
+                                             int(t), int(k_offset), int(K if K_total is None else K_total),
+                                             _ptr(s, np.float64, D, "s")))
 
     def apply(self, alpha, x0, X, q0, Q, gamma=None):
         """One Gram apply q0 = A x0, Q_k = A X_k (A = beta Phi^T Phi + diag alpha, Eq. 7) through the

@@ -354,6 +354,11 @@ __global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* 
   }
 }
 
+// cofem_estep_probes: the mean system (column 0) is solved by another rank; freeze it at once.
+__global__ void k_freeze_col0(ColState* cs) {
+  if (threadIdx.x == 0) { cs[0].frozen = 1; cs[0].frozen_at = 0; }
+}
+
 // Sharded mode: apply the rank-summed per-column totals (same rules as the in-kernel finishes).
 __global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum, int m, int mode, int iter, double tau) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -485,7 +490,7 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   static const bool no_mean = getenv("COFEM_EXP_NO_MEAN") != nullptr;   // timing experiment only (results invalid)
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
-    if (!no_mean) {
+    if (!no_mean && !c->skip_mean) {
       if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
       update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
     }
@@ -524,6 +529,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   launch_end(c, KC_INIT);
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
   if (c->sharded) { cofem_status st = sharded_finish(c, m, 0, 0); if (st != COFEM_OK) return st; }
+  if (c->skip_mean) k_freeze_col0<<<1, 32, 0, c->stream>>>(c->cs);   // every kernel skips a frozen column
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
   if (c->fast_conv && c->sharded) return cg_loop_conv_sharded(c, K, invK);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
@@ -585,7 +591,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   CK(cudaStreamWaitEvent(c->work, c->ev_in, 0));
   c->stream = c->work;
   cofem_status st = COFEM_OK;
-  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total) {
+  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total || c->graph_skip != (int)c->skip_mean) {
     if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
     const int64_t l0 = c->launches;
     cudaGraph_t g = nullptr;
@@ -604,7 +610,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
       if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
       return st;
     }
-    c->graph_K = K; c->graph_Kt = K_total;
+    c->graph_K = K; c->graph_Kt = K_total; c->graph_skip = (int)c->skip_mean;
   }
   cudaError_t e = cudaGraphLaunch(c->graph_exec, c->work);
   c->launches += c->graph_launches;
@@ -895,6 +901,16 @@ cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t
   if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
   ctx->c.err.clear();
   return estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, mu, s);
+}
+
+cofem_status cofem_estep_probes(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
+                                int32_t k_offset, int32_t K_total, double* s) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  ctx->c.err.clear();
+  ctx->c.skip_mean = true;
+  const cofem_status st = estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, nullptr, s);
+  ctx->c.skip_mean = false;
+  return st;
 }
 
 __global__ void k_apply_prep(int64_t D, int64_t Dp, double beta, int precond, const double* __restrict__ alpha,

@@ -63,7 +63,8 @@ struct Ctx {
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   void* dparams = nullptr;              // device ProbeParams of the current E-step
   cudaGraphExec_t graph_exec = nullptr; // captured E-step (cofem.cu estep_device)
-  int graph_K = -1, graph_Kt = -1;
+  int graph_K = -1, graph_Kt = -1, graph_skip = -1;
+  bool skip_mean = false;          // cofem_estep_probes: column 0 frozen from the start (mean owned elsewhere)
   int64_t graph_launches = 0;
   void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu
   void* dct_tab64 = nullptr;            // (double)

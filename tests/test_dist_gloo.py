@@ -11,7 +11,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2202_12808_b200.dist import em_probe_parallel, probe_split
+from paper_2202_12808_b200.dist import em_probe_parallel, probe_split, probe_split_owner
 
 
 def test_probe_split_covers_all():
@@ -24,7 +24,19 @@ def test_probe_split_covers_all():
         probe_split(2, 4, 0)
 
 
-def _worker(rank, world, port, out):
+def test_probe_split_owner_covers_all_and_balances():
+    for K in (2, 7, 16, 32, 33):
+        for world in range(1, min(K, 8) + 1):
+            for cost in (0.0, 1.0, 6.5, 40.0):
+                parts = [probe_split_owner(K, world, r, cost) for r in range(world)]
+                ks = [k for off, n, _ in parts for k in range(off, off + n)]
+                assert ks == list(range(K)) and min(n for _, n, _ in parts) >= 1
+                assert [o for _, _, o in parts] == [True] + [False] * (world - 1)
+    # C4 at 8 GPUs: the owner of a 6.5-probe mean system gets 1 probe, the others 4-5
+    assert [n for _, n, _ in (probe_split_owner(32, 8, r, 6.5) for r in range(8))] == [1, 5, 5, 5, 4, 4, 4, 4]
+
+
+def _worker(rank, world, port, out, mean_cost=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import torch
@@ -47,21 +59,33 @@ def _worker(rank, world, port, out):
     def mstep_fn(mu, s, alpha):
         alpha[:] = mstep(mu, s)
 
+    def estep_probes_fn(alpha, K_local, seed, t, s, k_offset, K_total):
+        _, s_loc, _ = estep(op, w.y, w.beta, alpha, K_local, seed, t, w.U, k_offset=k_offset)
+        s[:] = s_loc * K_local / K_total
+
+    def broadcast(mu):
+        dist.broadcast(torch.from_numpy(mu), src=0)
+
     alpha, mu, s = np.ones(w.D), np.zeros(w.D), np.zeros(w.D)
-    em_probe_parallel(estep_fn, mstep_fn, allreduce, 3, 6, 9, rank, world, alpha, mu, s)
-    if rank == 0:
-        np.save(out, np.stack([alpha, mu, s]))
+    if rank > 0 and mean_cost is not None:
+        mu[:] = np.nan                              # never computed here: must arrive by broadcast
+    em_probe_parallel(estep_fn, mstep_fn, allreduce, 3, 6, 9, rank, world, alpha, mu, s,
+                      mean_cost=mean_cost, estep_probes=estep_probes_fn, broadcast=broadcast)
+    np.save(out + ".%d.npy" % rank, np.stack([alpha, mu, s]))
     dist.destroy_process_group()
 
 
-def test_probe_parallel_gloo_world2_equals_single(tmp_path):
+@pytest.mark.parametrize("world,mean_cost", [(2, None), (2, 1.5), (3, 2.0)])
+def test_probe_parallel_gloo_world2_equals_single(tmp_path, world, mean_cost):
     import socket
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    out = str(tmp_path / "r0.npy")
-    mp.start_processes(_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
-    a, mu, s = np.load(out)
+    out = str(tmp_path / "r")
+    mp.start_processes(_worker, args=(world, port, out, mean_cost), nprocs=world, join=True, start_method="spawn")
+    for r in range(1, world):                      # every rank ends with the same alpha, mu, s
+        assert np.array_equal(np.load(out + ".%d.npy" % r), np.load(out + ".0.npy"))
+    a, mu, s = np.load(out + ".0.npy")
     import synth
     from oracle.cofem import cofem_em
     from oracle.operators import DenseOp

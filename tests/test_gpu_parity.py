@@ -222,6 +222,24 @@ def test_probe_parallel_partial_s_sums_to_full():
     assert rel(np.sum(parts, axis=0), s) < 1e-12
 
 
+@pytest.mark.parametrize("w", [SMALL[0], SMALL[2], SMALL[5],
+                               synth.dct(1024, 1024, 262144, 400, K=4, U=8, T=1, seed=1)], ids=lambda w: w.name)
+def test_estep_probes_equals_estep_s(w):
+    """cofem_estep_probes (probe-parallel ranks that do not own the mean system): the same s,
+    bit for bit, as the full E-step (the columns are independent, R3), column 0 frozen at 0."""
+    ctx = ctx_of(w)
+    a = torch.ones(w.D, dtype=torch.float64, device="cuda")
+    mu, s = dev(w.D), dev(w.D)
+    ctx.estep(a, w.K, 2, 1, mu, s, k_offset=3, K_total=w.K + 5)
+    s2 = dev(w.D)
+    ctx.estep_probes(a, w.K, 2, 1, s2, k_offset=3, K_total=w.K + 5)
+    assert torch.equal(s, s2)
+    assert ctx.report()["frozen_at"][0] == 0
+    mu3, s3 = dev(w.D), dev(w.D)                   # and the graph of the full E-step is rebuilt after
+    ctx.estep(a, w.K, 2, 1, mu3, s3, k_offset=3, K_total=w.K + 5)
+    assert torch.equal(mu3, mu) and torch.equal(s3, s)
+
+
 # ------------------------------------------------------------ full-size checks (bench launch config)
 def test_c4_full_estep1_closed_form():
     """Config 4 at full size (1024 x 1024, N = 2^18, K = 32, U = 200): E-step 1 vs the

@@ -29,7 +29,12 @@ torch.cuda.synchronize()
 ms = []
 for t in range(reps):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); ctx.estep(alpha, w.K, 0, 2 + t, mu, s); b.record()
+    a.record()
+    if os.environ.get("TIME_PROBES_ONLY"):     # a probe-parallel rank that does not own the mean system
+        ctx.estep_probes(alpha, w.K, 0, 2 + t, s)
+    else:
+        ctx.estep(alpha, w.K, 0, 2 + t, mu, s)
+    b.record()
     torch.cuda.synchronize()
     ms.append(a.elapsed_time(b))
 print("%s E-step at fixed alpha: median %.2f ms (min %.2f) over %d" % (w.name, sorted(ms)[len(ms) // 2], min(ms), reps))
