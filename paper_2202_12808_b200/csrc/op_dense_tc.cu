@@ -4,27 +4,25 @@
 // (Eq. 7; batched "matrix-matrix" CG apply, §3.2; BASELINE north_star:
 // "tcgen05/TMA tiles with a 3xTF32 split").
 //
-// 3xTF32: every fp32 operand x is split into hi = x with its 13 low mantissa bits cleared
-// (exactly a tf32 value) and lo = x - hi (exact in fp32), and C = A_hi B_hi + A_hi B_lo +
-// A_lo B_hi on kind::tf32 MMAs with fp32 accumulation in TMEM; the dropped A_lo B_lo term is
-// <= 2^-22 |A||B| per product (DESIGN.md §7 error budget).
+// 3xTF32: every fp32 operand x is split into hi = x rounded to tf32 and lo = x - hi (exact in
+// fp32), and C = A_hi B_hi + A_hi B_lo + A_lo B_hi on kind::tf32 MMAs with fp32 accumulation
+// in TMEM; the dropped A_lo B_lo term is <= 2^-22 |A||B| per product.
 //
-// Per CTA (one 128-row output tile; 6 warps):
-//   warp 0      TMA producer: Phi tile (16 KB) + B_hi, B_lo tiles (K-major, SWIZZLE_128B) per
-//               32-wide K step into a STAGES-deep shared-memory ring (mbarrier complete_tx)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (A from TMEM, B from smem)
-//   warps 2-5   "splitters": each thread owns one output row m; per K step it reads its row
-//               of the Phi tile from shared memory (this is where Phi^T's transposition
-//               happens for k_tc_phiTW: the tile is MN-major in smem, the row is gathered
-//               across the swizzled 128-B lines), writes A_hi / A_lo into TMEM
-//               (tcgen05.st, double-buffered), and accumulates the fp64 mean column
-//               (column 0 of B = [b0 | p_1..p_K], reading R2; fp64 per DESIGN.md R10)
-//               in a register with DFMA; after the last step they are the epilogue
-//               (tcgen05.ld of the fp32 accumulator -> q, gamma partials / W partials).
+// Per CTA (one 128-row output tile; 18 warps):
+//   warp 0      TMA producer: Phi tile (16 KB) + B_hi, B_lo tiles (K-major, SWIZZLE_128B) + 32
+//               fp64 mean-column operands per 32-wide K step into a 6-stage smem ring
+//   warp 1      TMEM allocator + tcgen05.mma issuer (whole warp, elect.sync per instruction;
+//               A from TMEM, B from smem), one wait and one commit per PAIR of K steps
+//   warps 2-17  "splitters", 4 groups x one warp per TMEM lane quarter: each thread owns one
+//               output row m; group g splits the K steps kt = g (mod 4): reads its row of the
+//               Phi tile from smem (Phi^T's transposition happens here for k_tc_phiTW: the
+//               tile is MN-major in smem), writes A_hi / A_lo into TMEM (tcgen05.st), then
+//               accumulates the fp64 mean column (column 0 of B = [b0 | p_1..p_K], R2, R10)
+//               with DFMA; they promote the round-toward-zero TMEM accumulator into RN fp32
+//               register sums every pair and run the epilogue (q, gamma partials / W partials).
 // The probe B operand's hi/lo split is done once per apply in global memory (B is
-// O((N + D) K), Phi is O(N D)); a CTA covers MT = 2 M-tiles (256 rows) when K <= 64 so
-// each B tile loaded from L2 feeds two accumulators.  Only the probe columns use the tensor cores; parity
-// mode (fp64 probes) keeps the SIMT path (op_dense.cu).
+// O((N + D) K), Phi is O(N D)).  Only the probe columns use the tensor cores; parity mode
+// (fp64 probes) keeps the SIMT path (op_dense.cu).  Measured design notes: DESIGN.md §7.2.
 #include <cuda.h>
 #include <stdio.h>
 
