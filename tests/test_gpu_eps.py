@@ -105,3 +105,23 @@ def test_eps_full_em_bars_c1():
     a, m = ao.cpu().numpy(), mu.cpu().numpy()
     assert rel(1 / a, 1 / oa) <= 1e-3 and rel(m, omu) <= 1e-3, (rel(1 / a, 1 / oa), rel(m, omu))
     assert np.array_equal(support(m), support(omu))
+
+
+def test_eps_through_the_sharded_finishes_world1():
+    """The eps rule reaches the sharded modes' freeze (k_sharded_finish carries tau): on a
+    1-rank communicator the column-sharded dense and the D-sharded conv runs equal the
+    single-GPU runs with the same cg_rtol."""
+    from paper_2202_12808_b200 import Context, get_unique_id
+    for w, eps in ((synth.dense(250, 1024, 20, K=8, U=200, T=1, seed=2), 1e-4),
+                   (synth.circconv(20000, 64, 20, K=8, U=600, T=1, seed=4), 1e-3)):
+        base = Context.from_workload(w, cg_rtol=eps)
+        sh = Context.from_workload(w, cg_rtol=eps, rank=0, world=1, nccl_id=get_unique_id(), d_offset=0,
+                                   D_global=w.D)
+        out = []
+        for c in (base, sh):
+            a = torch.ones(w.D, dtype=torch.float64, device="cuda")
+            mu, s = torch.empty_like(a), torch.empty_like(a)
+            c.estep(a, w.K, 5, 0, mu, s)
+            out.append((mu.cpu().numpy(), s.cpu().numpy(), c.report()["frozen_at"]))
+        assert out[0][2] == out[1][2] and min(out[1][2]) >= 0, (out[0][2], out[1][2])
+        assert rel(out[1][0], out[0][0]) <= 1e-6 and rel(out[1][1], out[0][1]) <= 1e-5
