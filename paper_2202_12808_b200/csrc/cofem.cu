@@ -85,6 +85,9 @@ struct VecArgs {
   double invK;
   double* colsum;   // sharded mode: per-column totals go here (summed over ranks, then finished)
   double tau;       // freeze threshold on rho / rho0 (ColState::tau)
+  int uchunks;      // k_update: probe columns split into uchunks chunks per D tile (1 = all in one item)
+  int mean_grid;    // k_update: CTAs [0, mean_grid) update the mean column, tile stride mean_grid
+  double* s_part; unsigned* tile_cnt;
 };
 
 // Probe-stream parameters of the current E-step, read from device memory so that one
@@ -237,9 +240,14 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
   __syncthreads();
   const int64_t ntiles = a.Dp / VEC_TILE;
   const int klo = a.jlo > 0 ? a.jlo - 1 : 0, khi = a.jhi - 1;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
-    if (a.jlo == 0 && sh.act[0]) {
+  // work item = (D tile, chunk of the probe columns); uchunks > 1 only when D is small
+  const int ncol = khi - klo, csz = ncol > 0 ? (ncol + a.uchunks - 1) / a.uchunks : 1;
+  const int nch = ncol > 0 ? (ncol + csz - 1) / csz : 1;
+  // the fp64 mean column over the tiles with the vec_grid stride, whatever the chunking: its
+  // rho' partials (and so mu) do not depend on K or max_probes
+  if (a.jlo == 0 && sh.act[0] && blockIdx.x < a.mean_grid) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += a.mean_grid) {
+      const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
       const double a0 = sh.a[0];
       double x[8], r[8], p[8], q[8], dv[8], acc = 0.0;
       ld8(a.x0 + d0, x); ld8(a.r0 + d0, r); ld8(a.p0 + d0, p); ld8(a.q0 + d0, q); ld8(a.dinv64 + d0, dv);
@@ -253,11 +261,17 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
       acc = warp_sum(acc);
       if (lane == 0) sh.red[warp][0] += acc;
     }
+  }
+  for (int64_t item = blockIdx.x; item < ntiles * nch; item += gridDim.x) {
+    const int64_t tile = item / nch;
+    const int chunk = (int)(item % nch);
+    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
     TP dp[8];
     ld8(a.dinvp + d0, dp);
     double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool any = false;
-    for (int k = klo; k < khi; ++k) {
+    const int k1 = min(khi, klo + (chunk + 1) * csz);
+    for (int k = klo + chunk * csz; k < k1; ++k) {
       if (!sh.act[k + 1]) continue;
       any = true;
       const double ak = sh.a[k + 1];
@@ -280,12 +294,34 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
       acc = warp_sum(acc);
       if (lane == 0) sh.red[warp][k + 1] += acc;
     }
-    if (any) {
-      double sv[8];
-      ld8(a.s + d0, sv);
+    if (nch == 1) {
+      if (any) {
+        double sv[8];
+        ld8(a.s + d0, sv);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sv[e] += sacc[e];
-      st8(a.s + d0, sv);
+        for (int e = 0; e < 8; ++e) sv[e] += sacc[e];
+        st8(a.s + d0, sv);
+      }
+    } else {   // chunk partials; the tile's last chunk adds them to s in chunk order (deterministic)
+      st8(a.s_part + (int64_t)chunk * a.Dp + d0, sacc);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) sh.last = atomicAdd(a.tile_cnt + tile, 1u) == (unsigned)nch - 1;
+      __syncthreads();
+      if (sh.last) {
+        __threadfence();
+        double sv[8];
+        ld8(a.s + d0, sv);
+        for (int ch = 0; ch < nch; ++ch) {
+          double pv[8];
+          ld8(a.s_part + (int64_t)ch * a.Dp + d0, pv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sv[e] += pv[e];
+        }
+        st8(a.s + d0, sv);
+        if (threadIdx.x == 0) a.tile_cnt[tile] = 0u;
+      }
+      __syncthreads();
     }
   }
   ColState* cs = a.cs;
@@ -399,6 +435,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.invK = invK;
   a.colsum = c->sharded ? c->colsum : nullptr;
   a.tau = c->freeze_tau;
+  a.uchunks = c->upd_chunks; a.s_part = c->s_part; a.tile_cnt = c->tile_cnt; a.mean_grid = c->vec_grid;
   return a;
 }
 
@@ -472,7 +509,7 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
   VecArgs<TP> a = vec_args<TP>(c, K, invK);
   a.jlo = jlo; a.jhi = jhi; a.counter = counter;
   launch_begin(c, cls, st);
-  k_update<TP><<<c->vec_grid, VEC_THREADS, 0, st>>>(a);
+  k_update<TP><<<jlo == 0 && jhi == 1 ? c->vec_grid : c->upd_grid, VEC_THREADS, 0, st>>>(a);
   launch_end(c, cls, st);
 }
 
@@ -543,8 +580,8 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     }
     if (st != COFEM_OK) return st;
     launch_begin(c, KC_UPDATE);
-    if (c->probe64) k_update<double><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
-    else k_update<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
+    if (c->probe64) k_update<double><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
+    else k_update<float><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
     if (c->sharded && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
@@ -685,7 +722,7 @@ static void free_all(Ctx* c) {
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
-                  c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0};
+                  c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -759,7 +796,16 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   ALLOC(c->cs, c->m_cap);
   ALLOC(c->counters, MAXM + 4);   // [0, MAXM): per column; MAXM..: per-launch tickets
   c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
-  c->part_stride = std::max(c->vec_grid, 1);
+  {   // k_update: with fewer D tiles than 2 per SM, split the probe columns into chunks as well
+    const int64_t ntiles = Dp / VEC_TILE;
+    int ch = 1;
+    if (ntiles < 2 * c->num_sms && c->Kcap > 1 && !getenv("COFEM_UPD_NOCHUNK"))
+      ch = (int)std::min<int64_t>(c->Kcap, (2 * c->num_sms + ntiles - 1) / ntiles);
+    c->upd_chunks = ch;
+    c->upd_grid = (int)std::min<int64_t>(ntiles * ch, (int64_t)c->num_sms * 4);
+    if (ch > 1) { ALLOC(c->s_part, (size_t)ch * Dp); ALLOC(c->tile_cnt, (size_t)ntiles); }   // zeroed
+  }
+  c->part_stride = std::max(std::max(c->vec_grid, c->upd_grid), 1);
 
   if (c->sharded) {     // the communicator first: the D-sharded conv setup exchanges y halos
     cofem_status cst = comm_init(c, opt->rank, opt->world, opt->nccl_id);

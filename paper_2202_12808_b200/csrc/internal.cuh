@@ -41,6 +41,10 @@ template <typename T> struct cplx { T x, y; };
 struct Ctx {
   int kind = 0;
   double freeze_tau = FREEZE_TAU;   // max(FREEZE_TAU, cg_rtol^2)
+  // k_update over (D tile x probe-column chunk) when the D tiles alone underfill the SMs
+  int upd_chunks = 1, upd_grid = 0;
+  double* s_part = nullptr;          // [upd_chunks][Dp] partial s of each chunk
+  unsigned* tile_cnt = nullptr;      // [D tiles] arrival tickets (last chunk sums s_part in order)
   int64_t N = 0, D = 0, Dp = 0;        // Dp: D padded to a multiple of VEC_TILE (zero padding)
   double beta = 0;
   cofem_options opt{};
