@@ -454,9 +454,9 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const size_t sm = smem_bytes<T>();
   // persistent grids at full occupancy (measured best: tools/sweep_slots.sh)
   static const int slots_env = getenv("COFEM_1K_SLOTS") ? atoi(getenv("COFEM_1K_SLOTS")) : -1;   // tuning hook
-  // the concurrent fp64 mean column is confined to a fraction of the SMs (COFEM_1K_MEAN_SMS,
-  // default half: tools/time_estep.py at fixed alpha, K = 32 / 16 / 8 / 4 probes per GPU:
-  // equal at K = 32, 5-7 % faster than a quarter at K <= 8, where the mean path is critical)
+  // the concurrent fp64 mean column is confined to a fraction of the SMs (COFEM_1K_MEAN_SMS):
+  // a quarter with >= 16 probe columns (bench C4: 15.35 vs 15.27 EM it/s for half), half below
+  // (tools/time_estep.py, 4-8 probes per GPU: 5-7 % faster, the mean path is critical there)
   static const int mean_sms_env = getenv("COFEM_1K_MEAN_SMS") ? atoi(getenv("COFEM_1K_MEAN_SMS")) : -1;
   auto grid_of = [&](const void* fn) {
     const int items = ncols * Work<T>::NTILE;
@@ -466,7 +466,7 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
     const int per_sm = slots_env > 0 ? std::min(slots_env, occ) : occ;
     int g = std::min(std::min(c->num_sms * per_sm, items), c->part_stride);
     if (j0 == 0 && c->fast1k) {
-      const int msms = mean_sms_env > 0 ? mean_sms_env : std::max(1, c->num_sms / 2);
+      const int msms = mean_sms_env > 0 ? mean_sms_env : std::max(1, c->num_sms / (c->Kcap >= 16 ? 4 : 2));
       if (mean_sms_env != 0) g = std::min(g, msms * per_sm);
     }
     return g;
