@@ -60,6 +60,7 @@ cudaError_t check_launch(Ctx* c, const char* what) {
 static void prof_collect(Ctx* c) {
   if (c->prof_recs.empty()) return;
   if (c->side) cudaStreamSynchronize(c->side);
+  for (int g = 1; g < Ctx::MAXG; ++g) if (c->gstream[g]) cudaStreamSynchronize(c->gstream[g]);
   cudaStreamSynchronize(c->stream);
   for (auto& r : c->prof_recs) {
     float ms = 0; cudaEventElapsedTime(&ms, r.a, r.b);
@@ -390,6 +391,11 @@ __global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* 
   }
 }
 
+__global__ void k_add_vec(int64_t n, double* __restrict__ a, const double* __restrict__ b) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += b[i];
+}
+
 // cofem_estep_probes: the mean system (column 0) is solved by another rank; freeze it at once.
 __global__ void k_freeze_col0(ColState* cs) {
   if (threadIdx.x == 0) { cs[0].frozen = 1; cs[0].frozen_at = 0; }
@@ -505,9 +511,11 @@ static cofem_status validate_alpha(Ctx* c, const double* alpha_dev) {
 // columns on the main stream; the columns are independent (reading R3), so the two
 // chains only join at the end of the E-step.
 template <typename TP>
-static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned* counter, cudaStream_t st, int cls) {
+static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned* counter, cudaStream_t st, int cls,
+                         double* s_acc = nullptr) {
   VecArgs<TP> a = vec_args<TP>(c, K, invK);
   a.jlo = jlo; a.jhi = jhi; a.counter = counter;
+  if (s_acc) a.s = s_acc;
   launch_begin(c, cls, st);
   k_update<TP><<<jlo == 0 && jhi == 1 ? c->vec_grid : c->upd_grid, VEC_THREADS, 0, st>>>(a);
   launch_end(c, cls, st);
@@ -522,8 +530,27 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   void* const P_entry = c->P; double* const p0_entry = c->p0;
   static const bool serial = getenv("COFEM_1K_SERIAL") != nullptr;   // tuning hook: mean column on the main stream
   cudaStream_t ms = serial ? c->stream : c->side;
+  // fast DCT path: the probe columns run as G independent groups on G streams, so that one
+  // group's issue-bound column pass overlaps another's bandwidth-bound passes (C4 fixed-alpha
+  // E-step: G = 1 62.7 ms, G = 2 58.3 ms, 57.6 with each probe launch on ~80 % of the SMs;
+  // G = 3 59.7, G = 4 61.6)
+  static const int groups_env = getenv("COFEM_PROBE_GROUPS") ? atoi(getenv("COFEM_PROBE_GROUPS")) : 2;
+  int G = c->fast1k ? std::max(1, std::min(Ctx::MAXG, groups_env)) : 1;
+  static const int gmin_env = getenv("COFEM_GROUP_MIN") ? atoi(getenv("COFEM_GROUP_MIN")) : -1;   // tuning hook
+  const int gmin = gmin_env > 0 ? gmin_env : 2;      // measured: groups of >= 2 columns help at every K
+  while (G > 1 && ((m - 1) / G < gmin || !c->gs[G - 1])) --G;
+  c->probe_groups = G;
+  int gj[Ctx::MAXG + 1];
+  for (int g = 0; g <= G; ++g) gj[g] = 1 + (int)((int64_t)(m - 1) * g / G);
   CK(cudaEventRecord(c->ev_fork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  for (int g = 1; g < G; ++g) {
+    CK(cudaMemsetAsync(c->gs[g], 0, c->Dp * sizeof(double), c->stream));
+  }
+  if (G > 1) {
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    for (int g = 1; g < G; ++g) CK(cudaStreamWaitEvent(c->gstream[g], c->ev_fork, 0));
+  }
   static const bool no_mean = getenv("COFEM_EXP_NO_MEAN") != nullptr;   // timing experiment only (results invalid)
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
@@ -531,13 +558,25 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
       if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
       update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
     }
-    if ((st = apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
-    if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
-    else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
+    for (int g = 0; g < G; ++g) {
+      cudaStream_t gst = g ? c->gstream[g] : c->stream;
+      unsigned* tk = g ? c->counters + 3 * MAXM + gj[g] : c->counters + MAXM;   // per-group tickets
+      if ((st = apply(c, gj[g], gj[g + 1], it, it > 0, gst)) != COFEM_OK) return st;
+      if (c->probe64) update_range<double>(c, K, invK, gj[g], gj[g + 1], tk, gst, KC_UPDATE, g ? c->gs[g] : nullptr);
+      else update_range<float>(c, K, invK, gj[g], gj[g + 1], tk, gst, KC_UPDATE, g ? c->gs[g] : nullptr);
+    }
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
   }
   CK(cudaEventRecord(c->ev_join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  for (int g = 1; g < G; ++g) {
+    CK(cudaEventRecord(c->gjoin[g], c->gstream[g]));
+    CK(cudaStreamWaitEvent(c->stream, c->gjoin[g], 0));
+  }
+  for (int g = 1; g < G; ++g) {   // s = s_0 + s_1 + ... in group order (deterministic)
+    k_add_vec<<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(c->Dp, c->s, c->gs[g]);
+    if (check_launch(c, "k_add_vec")) return COFEM_ERR_CUDA;
+  }
   if (c->P != P_entry) { c->Pb = c->P; c->P = P_entry; }
   if (c->p0 != p0_entry) { c->p0b = c->p0; c->p0 = p0_entry; }
   return COFEM_OK;
@@ -722,7 +761,8 @@ static void free_all(Ctx* c) {
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
-                  c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt};
+                  c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt,
+                  c->gs[1], c->gs[2], c->gs[3]};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -731,6 +771,10 @@ static void free_all(Ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
+  for (int g = 1; g < Ctx::MAXG; ++g) {
+    if (c->gstream[g]) cudaStreamDestroy(c->gstream[g]);
+    if (c->gjoin[g]) cudaEventDestroy(c->gjoin[g]);
+  }
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->work) cudaStreamDestroy(c->work);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -777,6 +821,10 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  for (int g = 1; g < Ctx::MAXG; ++g) {
+    CK(cudaStreamCreateWithFlags(&c->gstream[g], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->gjoin[g], cudaEventDisableTiming));
+  }
   CK(cudaStreamCreateWithFlags(&c->work, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
@@ -794,7 +842,8 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   { char* p; ALLOC(p, (size_t)c->Kcap * Dp * tp); c->Q = p; }
   ALLOC(c->bits, (size_t)c->Kcap * (Dp / 32));
   ALLOC(c->cs, c->m_cap);
-  ALLOC(c->counters, MAXM + 4);   // [0, MAXM): per column; MAXM..: per-launch tickets
+  ALLOC(c->counters, 4 * MAXM);   // [0, MAXM): per column; [MAXM, MAXM + 4): per-launch tickets; probe groups
+                                  // g >= 1 of the fast DCT path: [2 MAXM + j0) DCT, [3 MAXM + j0) update
   c->vec_grid = (int)std::min<int64_t>(Dp / VEC_TILE, (int64_t)c->num_sms * 4);
   {   // k_update: with fewer D tiles than 2 per SM, split the probe columns into chunks as well
     const int64_t ntiles = Dp / VEC_TILE;

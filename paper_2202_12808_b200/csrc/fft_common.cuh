@@ -72,6 +72,7 @@ struct DctArgs {
   DctTab<float> tr32, tc32;  // rows-length / cols-length tables
   DctTab<double> tr64, tc64;
   ColState* cs; double* part; int stride; unsigned* counters; int iter;
+  unsigned* ticket;   // this launch's last-CTA ticket (distinct per concurrently running column group)
 };
 
 template <typename T> __device__ __forceinline__ DctCol<T> col_of(const DctArgs& a, int j) {

@@ -63,6 +63,12 @@ struct Ctx {
   bool fast1k = false;                  // DCT2 1024 x 1024: fast path, mean column on `side`
   cudaStream_t side = nullptr;          // second stream (mean column of the fast DCT path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // fast DCT path: probe-column groups 1..3 on their own streams with their own s accumulators
+  static constexpr int MAXG = 4;
+  int probe_groups = 1;                 // groups of the E-step being enqueued (launch sizing)
+  cudaStream_t gstream[MAXG] = {};
+  cudaEvent_t gjoin[MAXG] = {};
+  double* gs[MAXG] = {};
   cudaStream_t work = nullptr;          // capturable stream the E-step graph runs on
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   void* dparams = nullptr;              // device ProbeParams of the current E-step

@@ -441,6 +441,8 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   if (st == COFEM_OK && dct1k_eligible(c) && !getenv("COFEM_DCT_GENERIC")) {   // env: test hook for the generic path
     st = dct1k_setup(c);
     c->fast1k = st == COFEM_OK;
+    for (int g = 1; c->fast1k && g < Ctx::MAXG; ++g)      // probe groups' s accumulators (cofem.cu)
+      if (cudaMalloc(&c->gs[g], c->Dp * sizeof(double)) != cudaSuccess) { c->gs[g] = nullptr; cudaGetLastError(); break; }
   }
   return st;
 }
@@ -458,6 +460,7 @@ DctArgs dct_args(Ctx* c, int m, int iter) {
   a.tr32 = tab_at(b32, c->rows); a.tc32 = tab_at(b32 + lr, c->cols);
   a.tr64 = tab_at(b64, c->rows); a.tc64 = tab_at(b64 + lr, c->cols);
   a.cs = c->cs; a.part = c->part; a.stride = c->part_stride; a.counters = c->counters; a.iter = iter;
+  a.ticket = c->counters + MAXM + 2;
   a.maskL = c->maskL; a.alphap = c->alphap; a.tab1k32 = c->tab1k32; a.tab1k64 = c->tab1k64;
   return a;
 }

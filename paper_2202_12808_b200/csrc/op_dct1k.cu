@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   __threadfence();
   __syncthreads();
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(a.counters + MAXM + 2 + (j0 == 0 ? 1 : 0), 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
       ColState cc = a.cs[j]; finish_gamma(cc, tot, a.iter); a.cs[j] = cc;
     }
   }
-  if (threadIdx.x == 0) a.counters[MAXM + 2 + (j0 == 0 ? 1 : 0)] = 0u;
+  if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
 template <typename T>
@@ -449,6 +449,7 @@ template <typename T>
 static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st) {
   using namespace d1k;
   DctArgs a = dct_args(c, j1, iter);
+  a.ticket = j0 == 0 ? c->counters + MAXM + 3 : j0 == 1 ? c->counters + MAXM + 2 : c->counters + 2 * MAXM + j0;
   constexpr int RT = Geo<T>::RT;
   const int ncols = j1 - j0;
   const size_t sm = smem_bytes<T>();
@@ -469,6 +470,11 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
       const int msms = mean_sms_env > 0 ? mean_sms_env : std::max(1, c->num_sms / (c->Kcap >= 16 ? 4 : 2));
       if (mean_sms_env != 0) g = std::min(g, msms * per_sm);
     }
+    // with concurrent probe groups each probe launch takes ~80 % of the SMs (C4: 120 of 148 best,
+    // 16.70 vs 16.51 EM it/s uncapped; tools/time_estep.py sweep 74..148)
+    static const int group_sms_env = getenv("COFEM_1K_GROUP_SMS") ? atoi(getenv("COFEM_1K_GROUP_SMS")) : -1;
+    const int gsms = group_sms_env >= 0 ? group_sms_env : (c->probe_groups > 1 ? (c->num_sms * 120) / 148 : 0);
+    if (j0 > 0 && gsms > 0) g = std::min(g, gsms * per_sm);
     return g;
   };
   const dim3 blk(RT * 32);
