@@ -455,9 +455,10 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const size_t sm = smem_bytes<T>();
   // persistent grids at full occupancy (measured best: tools/sweep_slots.sh)
   static const int slots_env = getenv("COFEM_1K_SLOTS") ? atoi(getenv("COFEM_1K_SLOTS")) : -1;   // tuning hook
-  // the concurrent fp64 mean column is confined to a fraction of the SMs (COFEM_1K_MEAN_SMS):
-  // a quarter with >= 16 probe columns (bench C4: 15.35 vs 15.27 EM it/s for half), half below
-  // (tools/time_estep.py, 4-8 probes per GPU: 5-7 % faster, the mean path is critical there)
+  // the concurrent fp64 mean column is confined to a fraction of the SMs (COFEM_1K_MEAN_SMS),
+  // shrinking as the probe work grows (tools/time_estep.py, C4 at a fixed alpha, with the
+  // concurrent probe groups): an eighth at >= 32 probes (57.3 vs 57.5 ms for a quarter), a
+  // quarter at >= 16 (33.1 vs 33.3 for an eighth), half below (21.1 vs 24.0 at 8 probes)
   static const int mean_sms_env = getenv("COFEM_1K_MEAN_SMS") ? atoi(getenv("COFEM_1K_MEAN_SMS")) : -1;
   auto grid_of = [&](const void* fn) {
     const int items = ncols * Work<T>::NTILE;
@@ -467,7 +468,8 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
     const int per_sm = slots_env > 0 ? std::min(slots_env, occ) : occ;
     int g = std::min(std::min(c->num_sms * per_sm, items), c->part_stride);
     if (j0 == 0 && c->fast1k) {
-      const int msms = mean_sms_env > 0 ? mean_sms_env : std::max(1, c->num_sms / (c->Kcap >= 16 ? 4 : 2));
+      const int msms = mean_sms_env > 0 ? mean_sms_env
+                                        : std::max(1, c->num_sms / (c->Kcap >= 32 ? 8 : c->Kcap >= 16 ? 4 : 2));
       if (mean_sms_env != 0) g = std::min(g, msms * per_sm);
     }
     // with concurrent probe groups each probe launch takes ~80 % of the SMs (C4: 120 of 148 best,
