@@ -392,6 +392,7 @@ def main():
     p1.record()
     barrier()
     prof_ms = p0.elapsed_time(p1)
+    busy = {c: ctx.profile_busy(c) for c in classes}
     prof = {c: ctx.profile_read(c) for c in classes}
     ctx.profile_enable([])
 
@@ -424,20 +425,44 @@ def main():
 
     # ---- roofline of the dominant kernel (live CUDA events over the timed region)
     pk, pk_kind = peaks()
-    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc, D)), key=lambda c: prof[c][0])
+    # dominant = the HBM-bound class with the largest busy time (union of its launch intervals:
+    # concurrent probe groups count once); dct_cols is issue-bound (two FFTs per 8 B/element,
+    # DESIGN §7.1) and has no HBM roofline; the whole-step HBM roofline is roofline.step
+    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc, D) and c != "dct_cols"),
+              key=lambda c: busy[c] if busy[c] > 0 else prof[c][0])
     tot_ms, cnt = prof[dom]
     avg_ms = tot_ms / cnt
-    byt = algorithmic_bytes(dom, w, K_loc, D)
-    achieved = byt / (avg_ms / 1000.0) / 1e9
+    # the probe columns may run as G concurrent groups (1024^2 DCT path): a launch then covers
+    # K / G columns (G = launches per CG iteration of the class), and the G launches of one
+    # iteration overlap: achieved = the class's bytes over its busy time (union of intervals)
+    groups = max(1, int(round(cnt / float(w.U * args.prof_steps))))
+    byt = algorithmic_bytes(dom, w, K_loc / groups, D)
+    busy_ms = busy[dom] if busy[dom] > 0 else tot_ms
+    achieved = byt * cnt / (busy_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
     share = {c: round(prof[c][0] / prof_ms, 4) for c in classes if prof[c][1] > 0}
+    busy_share = {c: round(busy[c] / prof_ms, 4) for c in classes if prof[c][1] > 0}
+    # whole-step view (the classes run concurrently on the DCT path): every class's algorithmic
+    # bytes per EM iteration over the device-timed step time
+    step_bytes = 0.0
+    for c in classes:
+        b_c = algorithmic_bytes(c, w, K_loc, D) if prof[c][1] > 0 else None
+        if b_c:
+            g_c = max(1, int(round(prof[c][1] / float(w.U * args.prof_steps))))
+            step_bytes += algorithmic_bytes(c, w, K_loc / g_c, D) * prof[c][1] / args.prof_steps
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_kind,
             "algorithmic_bytes_per_launch": byt, "avg_launch_ms": avg_ms, "launches": cnt,
-            "share_of_step": share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
+            "columns_per_launch": K_loc / groups, "busy_ms": busy_ms,
+            "achieved_def": "algorithmic bytes per launch x launches / busy time (union of launch intervals)",
+            "step": {"algorithmic_bytes": step_bytes, "achieved": step_bytes / (ms / args.steps / 1000.0) / 1e9,
+                     "frac": step_bytes / (ms / args.steps / 1000.0) / 1e9 / pk["hbm_gbs"],
+                     "def": "all classes' algorithmic bytes per EM iteration / device-timed ms_per_step "
+                            "(probe classes; the fp64 mean column is not counted)"},
+            "share_of_step": share, "busy_share_of_step": busy_share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
             args.prof_steps}
 
     cpu = None

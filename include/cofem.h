@@ -182,6 +182,10 @@ cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out);
  * i, the summed milliseconds and launch count since the last reset. */
 cofem_status cofem_profile_enable(cofem_ctx ctx, uint32_t mask);
 cofem_status cofem_profile_read(cofem_ctx ctx, int32_t cls, double* total_ms, int64_t* count, int32_t reset);
+/* Busy time of class i since its last reset: the measure of the union of its launch intervals, so
+ * launches of the class that ran concurrently (probe-column groups on separate streams) count
+ * once.  <= total_ms.  Reset together with cofem_profile_read(..., reset = 1). */
+cofem_status cofem_profile_busy(cofem_ctx ctx, int32_t cls, double* busy_ms);
 const char* cofem_kernel_class_name(int32_t cls);   /* NULL past the last class */
 
 const char* cofem_last_error(cofem_ctx ctx);        /* message of the last failing call ("" if none); ctx may be NULL */

@@ -70,6 +70,7 @@ SYMBOLS = [
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_last_report", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_Report)]),
     ("cofem_profile_enable", ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32]),
+    ("cofem_profile_busy", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     ("cofem_profile_read", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
                                           ctypes.POINTER(ctypes.c_int64), ctypes.c_int32]),
     ("cofem_kernel_class_name", ctypes.c_char_p, [ctypes.c_int32]),
@@ -259,6 +260,12 @@ class Context:
         ms, cnt = ctypes.c_double(), ctypes.c_int64()
         self._check(lib().cofem_profile_read(self._h, idx, ctypes.byref(ms), ctypes.byref(cnt), int(reset)))
         return ms.value, cnt.value
+
+    def profile_busy(self, cls):
+        """Union of the class's launch intervals in ms (concurrent launches counted once)."""
+        ms = ctypes.c_double()
+        self._check(lib().cofem_profile_busy(self._h, kernel_classes().index(cls), ctypes.byref(ms)))
+        return ms.value
 
     @property
     def launches(self):

@@ -62,11 +62,26 @@ static void prof_collect(Ctx* c) {
   if (c->side) cudaStreamSynchronize(c->side);
   for (int g = 1; g < Ctx::MAXG; ++g) if (c->gstream[g]) cudaStreamSynchronize(c->gstream[g]);
   cudaStreamSynchronize(c->stream);
+  std::vector<std::vector<std::pair<float, float>>> iv(KC_COUNT);
+  const cudaEvent_t ref = c->prof_recs.front().a;
   for (auto& r : c->prof_recs) {
     float ms = 0; cudaEventElapsedTime(&ms, r.a, r.b);
     c->prof_ms[r.cls] += ms; c->prof_cnt[r.cls] += 1;
-    c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b);
+    float t0 = 0; cudaEventElapsedTime(&t0, ref, r.a);        // may be negative (other streams)
+    iv[r.cls].push_back({t0, t0 + ms});
   }
+  for (int k = 0; k < KC_COUNT; ++k) {   // busy time = measure of the union of the intervals
+    auto& v = iv[k];
+    std::sort(v.begin(), v.end());
+    double busy = 0; float lo = 0, hi = 0; bool open = false;
+    for (auto& x : v) {
+      if (!open || x.first > hi) { if (open) busy += hi - lo; lo = x.first; hi = x.second; open = true; }
+      else hi = std::max(hi, x.second);
+    }
+    if (open) busy += hi - lo;
+    c->prof_busy[k] += busy;
+  }
+  for (auto& r : c->prof_recs) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
   c->prof_recs.clear();
 }
 
@@ -1159,7 +1174,14 @@ cofem_status cofem_profile_read(cofem_ctx ctx, int32_t cls, double* total_ms, in
   prof_collect(c);
   if (total_ms) *total_ms = c->prof_ms[cls];
   if (count) *count = c->prof_cnt[cls];
-  if (reset) { c->prof_ms[cls] = 0; c->prof_cnt[cls] = 0; }
+  if (reset) { c->prof_ms[cls] = 0; c->prof_cnt[cls] = 0; c->prof_busy[cls] = 0; }
+  return COFEM_OK;
+}
+
+cofem_status cofem_profile_busy(cofem_ctx ctx, int32_t cls, double* busy_ms) {
+  if (!ctx || cls < 0 || cls >= KC_COUNT || !busy_ms) { g_err = "bad argument"; return COFEM_ERR_INVALID; }
+  prof_collect(&ctx->c);
+  *busy_ms = ctx->c.prof_busy[cls];
   return COFEM_OK;
 }
 

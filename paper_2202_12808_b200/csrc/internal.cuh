@@ -139,6 +139,7 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_pool;
   double prof_ms[KC_COUNT] = {0};
   int64_t prof_cnt[KC_COUNT] = {0};
+  double prof_busy[KC_COUNT] = {0};    // union of the class's launch intervals (concurrent launches once)
 
   std::string err;
 };
