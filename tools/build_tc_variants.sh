@@ -4,7 +4,7 @@ set -e
 cd "$(dirname "$0")/.."
 python -c "from paper_2202_12808_b200 import build; build.build()"
 B=paper_2202_12808_b200/_build
-for v in ${VARIANTS:-NOTMA NOMMA NOSPLIT NOPROMO}; do
+for v in ${VARIANTS:-NOTMA NOPROMO TRACE}; do
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
     -I include $(echo $v | sed 's/^/-DCOFEM_TC_EXP_/; s/+/ -DCOFEM_TC_EXP_/g') -c paper_2202_12808_b200/csrc/op_dense_tc.cu -o /tmp/tc_$v.o
   objs=$(ls $B/*.o | grep -v op_dense_tc.o)
