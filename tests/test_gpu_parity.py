@@ -407,3 +407,13 @@ def test_full_em_recovers_the_sparse_signal(name, nrmse_max):
     true_sup = np.nonzero(z)[0]
     found = np.abs(mu) > 1e-3 * np.abs(mu).max()
     assert found[true_sup].mean() >= 0.95
+
+
+def test_c4_full_size_bitwise_deterministic():
+    """Config 4 at full size with the concurrent streams of the fast path (two probe groups and
+    the fp64 mean column): every reduction is fixed-order, so two runs agree bit for bit."""
+    w = synth.preset("C4")
+    r1 = gpu_em(ctx_of(w), w, 2, w.K, 4)
+    r2 = gpu_em(ctx_of(w), w, 2, w.K, 4)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
