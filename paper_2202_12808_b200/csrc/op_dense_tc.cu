@@ -4,9 +4,11 @@
 // (Eq. 7; batched "matrix-matrix" CG apply, §3.2; BASELINE north_star:
 // "tcgen05/TMA tiles with a 3xTF32 split").
 //
-// 3xTF32: every fp32 operand x is split into hi = x rounded to tf32 and lo = x - hi (exact in
-// fp32), and C = A_hi B_hi + A_hi B_lo + A_lo B_hi on kind::tf32 MMAs with fp32 accumulation
-// in TMEM; the dropped A_lo B_lo term is <= 2^-22 |A||B| per product.
+// 3xTF32: C = A_hi B_hi + A_hi B_lo + A_lo B_hi on kind::tf32 MMAs with fp32 accumulation in
+// TMEM.  B (the probe block, small) is split once per apply with hi = round-to-nearest tf32; A
+// (Phi) is written to TMEM as is — the tensor core reads only the tf32 bits of an fp32 operand
+// (truncation, tools/tf32_semantics.cu) — with lo = x - trunc(x) (exact, |lo| < 2^-10 |x|); the
+// dropped A_lo B_lo term is <= 2^-21 |A||B| per product.
 //
 // Per CTA (one 128-row output tile; 18 warps):
 //   warp 0      TMA producer: Phi tile (16 KB) + B_hi, B_lo tiles (K-major, SWIZZLE_128B) + 32
@@ -16,7 +18,7 @@
 //   warps 2-17  "splitters", 4 groups x one warp per TMEM lane quarter: each thread owns one
 //               output row m; group g splits the K steps kt = g (mod 4): reads its row of the
 //               Phi tile from smem (Phi^T's transposition happens here for k_tc_phiTW: the
-//               tile is MN-major in smem), writes A_hi / A_lo into TMEM (tcgen05.st), then
+//               tile is MN-major in smem), writes x and lo = x - trunc(x) into TMEM, then
 //               accumulates the fp64 mean column (column 0 of B = [b0 | p_1..p_K], R2, R10)
 //               with DFMA; they promote the round-toward-zero TMEM accumulator into RN fp32
 //               register sums every pair and run the epilogue (q, gamma partials / W partials).
@@ -411,13 +413,22 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
         for (int h = 0; h < 4; ++h) {
           float x[8];
           load_row8<MN>(a, m, h, x);
-          float hi[8], lo[8];
+          float lo[8];
+#ifdef COFEM_TC_EXP_RNHI
+          float hi[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             hi[i] = tf32_hi_alu(x[i]);
             lo[i] = x[i] - hi[i];
           }
           tmem_st8(lane_addr + buf + 8 * h, hi);
+#else
+          // A_hi = x itself: the tensor core reads only its tf32 bits (truncation, measured by
+          // tools/tf32_semantics.cu), so lo = x - trunc(x) is exact and no rounding is needed
+#pragma unroll
+          for (int i = 0; i < 8; ++i) lo[i] = x[i] - __uint_as_float(__float_as_uint(x[i]) & 0xFFFFE000u);
+          tmem_st8(lane_addr + buf + 8 * h, x);
+#endif
           tmem_st8(lane_addr + buf + 32 + 8 * h, lo);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
