@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--prof-steps", type=int, default=1, help="EM iterations of the per-kernel profiled pass")
+    ap.add_argument("--prof-steps", type=int, default=0,
+                    help="EM iterations of the per-kernel profiled pass (0 = all timed iterations)")
     ap.add_argument("--rtol", type=float, default=0.0,
                     help="NEXT-1: the paper's CG stopping rule eps (per-column freezing, U stays the cap); "
                          "0 = the BASELINE fixed-U contract")
@@ -146,13 +147,36 @@ def algorithmic_bytes(cls, w, K_local, D_local=None):
         return D * (16 * K + 16 + 4) + D * K // 8 + (0 if fast else D * 56)
     if cls == "pcg_direction":     # r, p read, p write (+dinv)
         return D * (12 * K + 24 + 12)
-    if cls == "conv_apply":        # p read, q write, alpha once
-        return D * (8 * K + 16 + 8)
+    if cls == "conv_apply":        # r, p read, p (direction, other buffer), q write; dinv, alpha once
+        return D * (16 * K + 8)
     if cls == "dense_phiT_w":      # Phi once, p read, q write, alpha
         return w.N * D * 4 + D * (8 * K + 16 + 8)
     if cls == "dense_phi_p":
         return w.N * D * 4 + D * (4 * K + 8)
     return None
+
+
+def active_bytes(cls, w, K_local, D_local, groups, frozen):
+    """Algorithmic bytes class `cls` moved over the profiled E-steps, counting only the work
+    the kernels execute: a column frozen at CG iteration F (R5, report frozen_at) is applied in
+    iterations 0..F and updated (and, on the dense path, given a new direction) in 0..F-1; the
+    per-column bytes count per active column-iteration and the arrays shared by a launch's
+    columns once per launch with an active column (launch g of an iteration covers the probe
+    columns [gj[g], gj[g+1]), gj[g] = 1 + K g / G, as cg_loop_split).  Returns (bytes, executed
+    fraction of the U x K column-iterations)."""
+    U, K = w.U, K_local
+    shared = algorithmic_bytes(cls, w, 0, D_local)
+    per_col = algorithmic_bytes(cls, w, 1, D_local) - shared
+    lag = 0 if cls in ("pcg_update", "pcg_direction") else 1
+    gj = [1 + (K * g) // groups for g in range(groups + 1)]
+    tot, colit = 0.0, 0
+    for fz in frozen:
+        act = [U if f < 0 else min(f + lag, U) for f in fz[1:K + 1]]
+        colit += sum(act)
+        tot += per_col * sum(act)
+        for g in range(groups):
+            tot += shared * max(act[gj[g] - 1:gj[g + 1] - 1], default=0)
+    return tot, colit / float(max(1, U * K * len(frozen)))
 
 
 def mean_cost(w):
@@ -383,15 +407,22 @@ def main():
         ctx.profile_read(c, reset=True)
     t = t_timed
     alpha.copy_(alpha_timed)
+    if args.prof_steps <= 0:
+        args.prof_steps = args.steps
     barrier()
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record()
+    # after each replayed E-step the report gives every column's freeze iteration (R5): a frozen
+    # column does no work in the remaining CG iterations, so the algorithmic bytes below count
+    # the column-iterations actually executed, not U x K
+    prof_ms, frozen = 0.0, []
     for _ in range(args.prof_steps):
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
         step(t, alpha, alpha, mu, s)
+        p1.record()
+        barrier()
+        prof_ms += p0.elapsed_time(p1)
+        frozen.append(ctx.report()["frozen_at"])
         t += 1
-    p1.record()
-    barrier()
-    prof_ms = p0.elapsed_time(p1)
     busy = {c: ctx.profile_busy(c) for c in classes}
     prof = {c: ctx.profile_read(c) for c in classes}
     ctx.profile_enable([])
@@ -434,11 +465,14 @@ def main():
     avg_ms = tot_ms / cnt
     # the probe columns may run as G concurrent groups (1024^2 DCT path): a launch then covers
     # K / G columns (G = launches per CG iteration of the class), and the G launches of one
-    # iteration overlap: achieved = the class's bytes over its busy time (union of intervals)
+    # iteration overlap: achieved = the class's executed bytes over its busy time (union of
+    # intervals).  Executed bytes: per-column bytes x active column-iterations + the shared
+    # arrays once per launch that has an active column (active_bytes)
     groups = max(1, int(round(cnt / float(w.U * args.prof_steps))))
     byt = algorithmic_bytes(dom, w, K_loc / groups, D)
     busy_ms = busy[dom] if busy[dom] > 0 else tot_ms
-    achieved = byt * cnt / (busy_ms / 1000.0) / 1e9
+    dom_bytes, work_frac = active_bytes(dom, w, K_loc, D, groups, frozen)
+    achieved = dom_bytes / (busy_ms / 1000.0) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -452,15 +486,17 @@ def main():
         b_c = algorithmic_bytes(c, w, K_loc, D) if prof[c][1] > 0 else None
         if b_c:
             g_c = max(1, int(round(prof[c][1] / float(w.U * args.prof_steps))))
-            step_bytes += algorithmic_bytes(c, w, K_loc / g_c, D) * prof[c][1] / args.prof_steps
+            step_bytes += active_bytes(c, w, K_loc, D, g_c, frozen)[0] / args.prof_steps
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk_kind,
             "algorithmic_bytes_per_launch": byt, "avg_launch_ms": avg_ms, "launches": cnt,
             "columns_per_launch": K_loc / groups, "busy_ms": busy_ms,
-            "achieved_def": "algorithmic bytes per launch x launches / busy time (union of launch intervals)",
+            "work_fraction": work_frac,
+            "achieved_def": "algorithmic bytes of the column-iterations executed (frozen columns, R5, do no "
+                            "work; work_fraction = executed / (U x K)) / busy time (union of launch intervals)",
             "step": {"algorithmic_bytes": step_bytes, "achieved": step_bytes / (ms / args.steps / 1000.0) / 1e9,
                      "frac": step_bytes / (ms / args.steps / 1000.0) / 1e9 / pk["hbm_gbs"],
-                     "def": "all classes' algorithmic bytes per EM iteration / device-timed ms_per_step "
+                     "def": "all classes' executed algorithmic bytes per EM iteration / device-timed ms_per_step "
                             "(probe classes; the fp64 mean column is not counted)"},
             "share_of_step": share, "busy_share_of_step": busy_share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
             args.prof_steps}

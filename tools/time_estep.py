@@ -14,6 +14,8 @@ w = synth.preset(sys.argv[1] if len(sys.argv) > 1 else "C4")
 if os.environ.get("TIME_K"):          # emulate one rank of a probe-parallel run (K / world probes)
     w.K = int(os.environ["TIME_K"])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+if os.environ.get("TIME_U"):          # CG iterations per E-step (use with an existing alpha file)
+    w.U = int(os.environ["TIME_U"])
 ctx = Context.from_workload(w, max_probes=w.K)
 alpha = torch.ones(w.D, dtype=torch.float64, device="cuda")
 mu, s = torch.empty_like(alpha), torch.empty_like(alpha)
@@ -37,4 +39,6 @@ for t in range(reps):
     b.record()
     torch.cuda.synchronize()
     ms.append(a.elapsed_time(b))
-print("%s E-step at fixed alpha: median %.2f ms (min %.2f) over %d" % (w.name, sorted(ms)[len(ms) // 2], min(ms), reps))
+fz = ctx.report()["frozen_at"]
+print("%s E-step at fixed alpha (U = %d): median %.2f ms (min %.2f) over %d; frozen_at max %d, mean %.1f, mean column %d" % (
+    w.name, w.U, sorted(ms)[len(ms) // 2], min(ms), reps, max(fz), sum(fz) / len(fz), fz[0]))
