@@ -147,7 +147,44 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
   const DctCol<T> c = col_of<T>(a, j);
   const int64_t rb = (int64_t)(row0 + warp) * L;
   T A[8], B[8], C[8], E[8];
-  {
+  if constexpr (sizeof(T) == 4) {
+    // fp32: the row moves as 16-byte vectors (lane l: elements 4 l + 128 i), the direction
+    // update a6 is elementwise there, and the warp's exchange region turns the row into the
+    // canonical per-lane positions (8 LDG.128 per array instead of 32 scalar loads)
+    float4* __restrict__ pr = reinterpret_cast<float4*>(c.p + rb);
+    const float4* __restrict__ rr = reinterpret_cast<const float4*>(c.r + rb);
+    const float4* __restrict__ dv = reinterpret_cast<const float4*>(c.dinv + rb);
+    float4* r4 = reinterpret_cast<float4*>(sm + warp * WREG);
+    const float bb = (float)bcoef;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 pv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pv[i] = pr[lane + 32 * (4 * h + i)];
+      if (dir) {
+        float4 rv[4], dd[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { rv[i] = rr[lane + 32 * (4 * h + i)]; dd[i] = dv[lane + 32 * (4 * h + i)]; }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {    // a6: p = M^-1 r + b p
+          pv[i].x = dd[i].x * rv[i].x + bb * pv[i].x; pv[i].y = dd[i].y * rv[i].y + bb * pv[i].y;
+          pv[i].z = dd[i].z * rv[i].z + bb * pv[i].z; pv[i].w = dd[i].w * rv[i].w + bb * pv[i].w;
+          pr[lane + 32 * (4 * h + i)] = pv[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) r4[lane + 32 * (4 * h + i)] = pv[i];
+    }
+    __syncwarp();
+    const T* reg = sm + warp * WREG;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int o[4];
+      canon(lane, r, o);
+      A[r] = reg[o[0]]; B[r] = reg[o[1]]; C[r] = reg[o[2]]; E[r] = reg[o[3]];
+    }
+    __syncwarp();                    // fft512 reuses the region
+  } else {
     T* __restrict__ pr = c.p + rb;
     const T* __restrict__ rr = c.r + rb;
     const T* __restrict__ dv = c.dinv + rb;
@@ -327,11 +364,45 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
   fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   T A[8], B[8], C[8], E[8];
   post_all<T>(lane, va, vb, A, B, C, E, tb);
+  double g = 0.0;
+  if constexpr (sizeof(T) == 4) {
+    // fp32: canonical values -> the warp's exchange region -> 16-byte vectors (lane l: elements
+    // 4 l + 128 i), so p, alpha and q move as LDG/STG.128
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int o[4];
+      canon(lane, r, o);
+      reg[o[0]] = A[r]; reg[o[1]] = B[r]; reg[o[2]] = C[r]; reg[o[3]] = E[r];
+    }
+    __syncwarp();
+    const float4* r4 = reinterpret_cast<const float4*>(reg);
+    const float4* __restrict__ pp = reinterpret_cast<const float4*>(c.p + rb);
+    const float4* __restrict__ al = reinterpret_cast<const float4*>(alpha_of<T>(a, j) + rb);
+    float4* __restrict__ qq = reinterpret_cast<float4*>(c.q + rb);
+    const float beta = (float)a.beta;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 pv[4], av[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { pv[i] = pp[lane + 32 * (4 * h + i)]; av[i] = al[lane + 32 * (4 * h + i)]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {   // a3: q = beta Phi^T Phi p + alpha o p; a4: gamma partial
+        const float4 x = r4[lane + 32 * (4 * h + i)];
+        float4 q;
+        q.x = beta * x.x + av[i].x * pv[i].x; q.y = beta * x.y + av[i].y * pv[i].y;
+        q.z = beta * x.z + av[i].z * pv[i].z; q.w = beta * x.w + av[i].w * pv[i].w;
+        g += (double)pv[i].x * (double)q.x + (double)pv[i].y * (double)q.y + (double)pv[i].z * (double)q.z +
+             (double)pv[i].w * (double)q.w;
+        qq[lane + 32 * (4 * h + i)] = q;
+      }
+    }
+    __syncwarp();                    // the next item's FFT reuses the region
+    return warp_sum(g);
+  }
   const T* __restrict__ pp = c.p + rb;
   const T* __restrict__ al = alpha_of<T>(a, j) + rb;
   T* __restrict__ qq = c.q + rb;
   const T beta = (T)a.beta;
-  double g = 0.0;
 #pragma unroll
   for (int r = 0; r < 8; ++r) {     // a3: q = beta Phi^T Phi p + alpha o p  (loads first)
     int o[4];
