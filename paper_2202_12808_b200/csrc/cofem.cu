@@ -253,7 +253,13 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
     sh.a[j] = c.a;
     for (int w = 0; w < VEC_THREADS / 32; ++w) sh.red[w][j] = 0.0;
   }
-  __syncthreads();
+  {   // every column of the range frozen (R5): nothing to do (each thread votes on the entries
+      // it wrote; all CTAs exit alike, so the tickets stay untouched).  Sharded runs always
+      // finish, their column sums feed a cross-rank reduction.
+    int act = 0;
+    for (int j = a.jlo + threadIdx.x; j < a.jhi; j += blockDim.x) act |= sh.act[j];
+    if (!__syncthreads_or(act) && !a.colsum) return;
+  }
   const int64_t ntiles = a.Dp / VEC_TILE;
   const int klo = a.jlo > 0 ? a.jlo - 1 : 0, khi = a.jhi - 1;
   // work item = (D tile, chunk of the probe columns); uchunks > 1 only when D is small

@@ -109,5 +109,15 @@ __device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, in
   }
 }
 
+// True when some column of the launch is still active.  Each thread reads the entries it
+// wrote in load_colinfo, so no barrier is needed before the vote.  A launch whose columns have
+// all frozen (R5) returns before staging the tables: every CTA takes the same exit, so the
+// last-CTA tickets are untouched.
+__device__ __forceinline__ bool any_active(const ColInfo& ci, int ncols) {
+  int act = 0;
+  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) act |= !ci.frozen[jj];
+  return __syncthreads_or(act) != 0;
+}
+
 }  // namespace d1k
 }  // namespace cofem

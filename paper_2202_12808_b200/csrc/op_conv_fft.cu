@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int
   T* sm = reinterpret_cast<T*>(smraw);
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, a.ncols, true);
+  if (!a.colsum && !any_active(ci, a.ncols)) return;   // sharded runs feed a cross-rank sum
   const cplx<T>* gtab = reinterpret_cast<const cplx<T>*>(sizeof(T) == 8 ? a.tab64 : a.tab32);
   const Tw<T> tb = load_tables<T>(gtab, reinterpret_cast<cplx<T>*>(sm + NW * WREG), TTOTC);   // + barrier
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
   T* sm = reinterpret_cast<T*>(smraw);
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, false);
+  if (!any_active(ci, ncols)) return;
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, i
   T* sm = reinterpret_cast<T*>(smraw);
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, false);
+  if (!any_active(ci, ncols)) return;
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
@@ -312,6 +314,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   T* sm = reinterpret_cast<T*>(smraw);
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, true);
+  if (!any_active(ci, ncols)) return;
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   const int warp = threadIdx.x >> 5;
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
