@@ -498,7 +498,18 @@ struct PhiPArgs {
   float* Wpart;                    // [split][K][Npad]
   double* W0part;                  // [split][Npad]
   int Npad;
+  const ColState* cs; int m;       // cs != nullptr: the launch exits when all m columns have frozen
 };
+
+// A launch whose columns have all frozen (R5) does nothing: every CTA votes on the same flags
+// and returns before any barrier, TMEM or TMA setup (so the phiTW tickets stay untouched).
+// Sharded runs pass cs = nullptr (their partial sums feed cross-rank reductions).
+__device__ __forceinline__ bool all_frozen(const ColState* cs, int m) {
+  if (!cs) return false;
+  int act = 0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) act |= !cs[j].frozen;
+  return !__syncthreads_or(act);
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ CUtensorMap mA,
@@ -506,6 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiP(const __grid_constant__ 
                                                         const __grid_constant__ CUtensorMap mBl, PhiPArgs a) {
   constexpr int MT = 1;
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
+  if (all_frozen(a.cs, a.m)) return;
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   setup_cta(bs, a.pl.stages);
   const int row0 = blockIdx.x * BM * MT, split = blockIdx.y;
@@ -594,6 +606,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap mBl, PhiTWArgs a) {
   constexpr int MT = 1;
   extern __shared__ __align__(1024) unsigned char sm[];      // no static smem: the dynamic base is 1024-aligned
+  if (all_frozen(a.colsum ? nullptr : a.cs, a.K + 1)) return;
   Bars& bs = *reinterpret_cast<Bars*>(sm + a.pl.stages * a.pl.stage_bytes);
   for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
   setup_cta(bs, a.pl.stages);
@@ -800,6 +813,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   PhiPArgs a1;
   a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
   a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
+  a1.cs = c->sharded ? nullptr : c->cs; a1.m = m;
   const dim3 g1((unsigned)((c->N + rows - 1) / rows), t->splits);
   if (t->mode == 0) k_tc_phiP<0><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else if (t->mode == 1) k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
