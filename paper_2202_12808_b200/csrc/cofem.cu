@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
 
 // a5: r -= a q; x0 += a0 p0; s += (a_k/K) p_k o P_k; z = M^-1 r; rho' = r^T z; then
 // (last CTA) b = rho'/rho, rho = rho'.
-template <typename TP>
+template <typename TP, int UNR>
 __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
   __shared__ VecShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -293,28 +293,42 @@ __global__ void __launch_bounds__(VEC_THREADS) k_update(VecArgs<TP> a) {
     double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool any = false;
     const int k1 = min(khi, klo + (chunk + 1) * csz);
-    for (int k = klo + chunk * csz; k < k1; ++k) {
-      if (!sh.act[k + 1]) continue;
-      any = true;
-      const double ak = sh.a[k + 1];
-      const TP akt = (TP)ak;
-      const double aks = ak * a.invK;
-      uint32_t w = (a.bits[(int64_t)k * a.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
-      TP r[8], q[8], p[8];
-      TP* Rk = a.R + (int64_t)k * a.Dp + d0;
-      ld8(Rk, r); ld8(a.Q + (int64_t)k * a.Dp + d0, q); ld8(a.P + (int64_t)k * a.Dp + d0, p);
-      double acc = 0.0;
+    // UNR columns per step: their loads are issued before any of their arithmetic (the
+    // per-column operations and the order of the s sums do not depend on UNR)
+    for (int k = klo + chunk * csz; k < k1; k += UNR) {
+      bool act[UNR];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        r[e] = r[e] - akt * q[e];
-        TP z = dp[e] * r[e];
-        acc += (double)r[e] * (double)z;
-        double pe = (double)p[e];
-        sacc[e] += ((w >> e) & 1u) ? -aks * pe : aks * pe;
+      for (int u = 0; u < UNR; ++u) act[u] = k + u < k1 && sh.act[k + u + 1];   // warp-uniform
+      TP r[UNR][8], q[UNR][8], p[UNR][8];
+      uint32_t w[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        w[u] = 0u;
+        if (!act[u]) continue;
+        const int64_t o = (int64_t)(k + u) * a.Dp + d0;
+        ld8(a.R + o, r[u]); ld8(a.Q + o, q[u]); ld8(a.P + o, p[u]);
+        w[u] = (a.bits[(int64_t)(k + u) * a.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
       }
-      st8(Rk, r);
-      acc = warp_sum(acc);
-      if (lane == 0) sh.red[warp][k + 1] += acc;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        if (!act[u]) continue;
+        any = true;
+        const double ak = sh.a[k + u + 1];
+        const TP akt = (TP)ak;
+        const double aks = ak * a.invK;
+        double acc = 0.0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          r[u][e] = r[u][e] - akt * q[u][e];
+          TP z = dp[e] * r[u][e];
+          acc += (double)r[u][e] * (double)z;
+          double pe = (double)p[u][e];
+          sacc[e] += ((w[u] >> e) & 1u) ? -aks * pe : aks * pe;
+        }
+        st8(a.R + (int64_t)(k + u) * a.Dp + d0, r[u]);
+        acc = warp_sum(acc);
+        if (lane == 0) sh.red[warp][k + u + 1] += acc;
+      }
     }
     if (nch == 1) {
       if (any) {
@@ -538,7 +552,14 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
   a.jlo = jlo; a.jhi = jhi; a.counter = counter;
   if (s_acc) a.s = s_acc;
   launch_begin(c, cls, st);
-  k_update<TP><<<jlo == 0 && jhi == 1 ? c->vec_grid : c->upd_grid, VEC_THREADS, 0, st>>>(a);
+  // two probe columns per step where the update runs alone (conv, dense: C5 242 -> 229 ms per
+  // E-step); on the concurrent-group DCT path the lighter one-column kernel (126 vs 80
+  // registers) shares the SMs better (C4 52.5 vs 53.6 ms).  Grids: the resident CTAs, 4 / 2 per SM
+  static const int unr_env = getenv("COFEM_UPD_UNR") ? atoi(getenv("COFEM_UPD_UNR")) : 0;   // tuning hook
+  const bool two = jlo >= 1 && jhi - jlo >= 2 && (unr_env ? unr_env == 2 : c->probe_groups <= 1);
+  if (jlo == 0 && jhi == 1) k_update<TP, 1><<<c->vec_grid, VEC_THREADS, 0, st>>>(a);
+  else if (!two) k_update<TP, 1><<<c->upd_grid, VEC_THREADS, 0, st>>>(a);
+  else k_update<TP, 2><<<std::min(c->upd_grid, c->num_sms * 2), VEC_THREADS, 0, st>>>(a);
   launch_end(c, cls, st);
 }
 
@@ -640,8 +661,8 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     }
     if (st != COFEM_OK) return st;
     launch_begin(c, KC_UPDATE);
-    if (c->probe64) k_update<double><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
-    else k_update<float><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
+    if (c->probe64) k_update<double, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
+    else k_update<float, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
     if (c->sharded && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
