@@ -109,6 +109,19 @@ template <typename T, int N> __device__ __forceinline__ void ld32B(const T* p, T
   }
 }
 
+// L2 prefetch of one warp's next 4 KB line of an fp32 image (one 128-byte line per lane), issued
+// before the current item's work so the next item's loads hit L2 (COFEM_1K_NOPF disables, A/B)
+template <typename T> __device__ __forceinline__ void pf_line(const T* line) {
+#ifndef COFEM_1K_NOPF
+  if constexpr (sizeof(T) == 4)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(line + 32 * (threadIdx.x & 31)));
+#endif
+}
+
+#ifndef COFEM_1K_PFD
+#define COFEM_1K_PFD 1       // prefetch distance in items of the warp
+#endif
+
 template <typename T> __device__ __forceinline__ const cplx<T>* tab1k(const DctArgs& a) {
   if constexpr (sizeof(T) == 8) return (const cplx<T>*)a.tab1k64; else return (const cplx<T>*)a.tab1k32;
 }
@@ -134,6 +147,18 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
+    if (w + COFEM_1K_PFD * (int)gridDim.x < ncols * NT) {   // a later item of this warp: p and r rows
+      const int wn = w + COFEM_1K_PFD * gridDim.x, jn = wn / NT;
+      if (!ci.frozen[jn]) {
+        const DctCol<T> cn = col_of<T>(a, j0 + jn);
+        const int64_t rn = (int64_t)((wn % NT) * RT + (threadIdx.x >> 5)) * L;
+        pf_line(cn.p + rn);
+        if (dir) pf_line(cn.r + rn);
+#ifdef COFEM_1K_PF_SHARED
+        if (dir) pf_line(cn.dinv + rn);
+#endif
+      }
+    }
     rows_inv_item<T>(a, j0 + jj, w % NT, dir, ci.b[jj], sm, tb);
     __syncthreads();                 // smem tile reuse
   }
@@ -252,6 +277,10 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, i
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
+    if (w + COFEM_1K_PFD * (int)gridDim.x < ncols * NT) {   // a later item of this warp: its T^T line
+      const int wn = w + COFEM_1K_PFD * gridDim.x, jn = wn / NT;
+      if (!ci.frozen[jn]) pf_line(col_of<T>(a, j0 + jn).t1 + (int64_t)((wn % NT) * RT + (threadIdx.x >> 5)) * L);
+    }
     cols_item<T>(a, j0 + jj, w % NT, sm, tb);
   }
 }
@@ -320,6 +349,18 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
+    if (w + COFEM_1K_PFD * (int)gridDim.x < ncols * NT) {   // a later item of this warp: T2 and p rows
+      const int wn = w + COFEM_1K_PFD * gridDim.x, jn = wn / NT;
+      if (!ci.frozen[jn]) {
+        const DctCol<T> cn = col_of<T>(a, j0 + jn);
+        const int64_t rn = (int64_t)((wn % NT) * RT + (threadIdx.x >> 5)) * L;
+        pf_line(cn.t2 + rn);
+        pf_line(cn.p + rn);
+#ifdef COFEM_1K_PF_SHARED
+        pf_line(alpha_of<T>(a, j0 + jn) + rn);
+#endif
+      }
+    }
     const double gw = rows_fwd_item<T>(a, j0 + jj, w % NT, sm, tb);   // warp-reduced, valid in lane 0
     if ((threadIdx.x & 31) == 0) ci.g[warp][jj] += gw;
   }
