@@ -143,6 +143,12 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, false);
   if (!any_active(ci, ncols)) return;
+  if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT]) {   // the first item's rows, before the tables
+    const DctCol<T> cn = col_of<T>(a, j0 + blockIdx.x / NT);
+    const int64_t rn = (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L;
+    pf_line(cn.p + rn);
+    if (dir) pf_line(cn.r + rn);
+  }
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
@@ -273,6 +279,8 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, i
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, false);
   if (!any_active(ci, ncols)) return;
+  if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT])     // the first item's line, before the tables
+    pf_line(col_of<T>(a, j0 + blockIdx.x / NT).t1 + (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L);
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
@@ -344,6 +352,11 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   __shared__ ColInfo ci;
   load_colinfo(ci, a.cs, j0, ncols, true);
   if (!any_active(ci, ncols)) return;
+  if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT]) {   // the first item's rows, before the tables
+    const DctCol<T> cn = col_of<T>(a, j0 + blockIdx.x / NT);
+    const int64_t rn = (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L;
+    pf_line(cn.t2 + rn); pf_line(cn.p + rn);
+  }
   const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   const int warp = threadIdx.x >> 5;
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
