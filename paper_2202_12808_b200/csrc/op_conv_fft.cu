@@ -57,7 +57,10 @@ template <typename T> __device__ __forceinline__ CCol<T> ccol(const ConvArgs& a,
 }
 
 template <typename T>
-__global__ void __launch_bounds__(NW * 32, 2) k_conv_fft(ConvArgs a, int j0, int dir) {
+#ifndef COFEM_CONV_MINB
+#define COFEM_CONV_MINB (sizeof(T) == 4 ? 3 : 2)   // fp32: 85 registers, 3 CTAs per SM (C5 228 -> 210 ms)
+#endif
+__global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs a, int j0, int dir) {
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   __shared__ ColInfo ci;
