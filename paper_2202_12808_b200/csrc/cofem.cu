@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
 #define COFEM_UPD_MINB 3   // two-column kernel: 3 CTAs per SM (85 registers, 64 B spill): C5 217 -> 209.5 ms; 4: 215
 #endif
 template <typename TP, int UNR>
-__global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : 1) k_update(VecArgs<TP> a) {
+#ifndef COFEM_UPD1_MINB
+#define COFEM_UPD1_MINB 3   // one-column kernel: 80 registers, 3 CTAs per SM (with min-blocks 1 nvcc took 208: C4 53.5 vs 47.7 ms)
+#endif
+__global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM_UPD1_MINB) k_update(VecArgs<TP> a) {
   __shared__ VecShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = a.jlo + threadIdx.x; j < a.jhi; j += blockDim.x) {
