@@ -58,14 +58,24 @@ template <typename T> __device__ __forceinline__ CCol<T> ccol(const ConvArgs& a,
 
 template <typename T>
 #ifndef COFEM_CONV_MINB
-#define COFEM_CONV_MINB (sizeof(T) == 4 ? 3 : 2)   // fp32: 85 registers, 3 CTAs per SM (C5 228 -> 210 ms)
+#define COFEM_CONV_MINB (sizeof(T) == 4 ? 4 : 2)   // fp32: 64 registers, 4 CTAs per SM (C5 228 -> 210 -> 196 ms; the gamma partials sized by the launch, not MAXM, make the 4th CTA fit)
 #endif
 __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs a, int j0, int dir) {
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
-  __shared__ ColInfo ci;
-  load_colinfo(ci, a.cs, j0, a.ncols, true);
-  if (!a.colsum && !any_active(ci, a.ncols)) return;   // sharded runs feed a cross-rank sum
+  // column flags in static shared memory; the per-warp gamma partials g[NW][ncols] after the
+  // tables in dynamic shared memory, sized by the launch's columns (not MAXM)
+  __shared__ struct { int frozen[MAXM]; double b[MAXM]; } ci;
+  double* gsm = reinterpret_cast<double*>(smraw + NW * WREG * sizeof(T) + TTOTC * sizeof(cplx<T>));
+  int act = 0;
+  for (int jj = threadIdx.x; jj < a.ncols; jj += blockDim.x) {
+    const ColState c = a.cs[j0 + jj];
+    ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
+    act |= !c.frozen;
+    for (int w = 0; w < NW; ++w) gsm[w * a.ncols + jj] = 0.0;
+  }
+  // every column frozen (R5): all CTAs exit alike; sharded runs feed a cross-rank sum
+  if (!__syncthreads_or(act) && !a.colsum) return;
   const cplx<T>* gtab = reinterpret_cast<const cplx<T>*>(sizeof(T) == 8 ? a.tab64 : a.tab32);
   const Tw<T> tb = load_tables<T>(gtab, reinterpret_cast<cplx<T>*>(sm + NW * WREG), TTOTC);   // + barrier
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -191,14 +201,14 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
         }
       }
     g = warp_sum(g);
-    if (lane == 0) ci.g[warp][jj] += g;
+    if (lane == 0) gsm[warp * a.ncols + jj] += g;
   }
   // gamma_j: CTA partials (fixed warp order) -> part[j][cta]; the last CTA reduces (R5)
   __syncthreads();
   for (int jj = threadIdx.x; jj < a.ncols; jj += blockDim.x) {
     double v = 0.0;
 #pragma unroll
-    for (int ww = 0; ww < NW; ++ww) v += ci.g[ww][jj];
+    for (int ww = 0; ww < NW; ++ww) v += gsm[ww * a.ncols + jj];
     a.part[(int64_t)(j0 + jj) * a.stride + blockIdx.x] = v;
   }
   __threadfence();
@@ -250,7 +260,9 @@ template <typename T> static std::vector<cplx<T>> build_conv_tables(const std::v
   return h;
 }
 
-template <typename T> static size_t smem_bytes() { return (size_t)NW * WREG * sizeof(T) + (size_t)TTOTC * sizeof(cplx<T>); }
+template <typename T> static size_t smem_bytes(int ncols) {
+  return (size_t)NW * WREG * sizeof(T) + (size_t)TTOTC * sizeof(cplx<T>) + (size_t)NW * ncols * sizeof(double);
+}
 
 }  // namespace cfft
 
@@ -309,8 +321,8 @@ cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g) {
       cudaMalloc(&c->conv_tab64, h64.size() * sizeof(h64[0])) != cudaSuccess) { c->err = "cudaMalloc conv tables"; return COFEM_ERR_OOM; }
   cudaMemcpy(c->conv_tab32, h32.data(), h32.size() * sizeof(h32[0]), cudaMemcpyHostToDevice);
   cudaMemcpy(c->conv_tab64, h64.data(), h64.size() * sizeof(h64[0]), cudaMemcpyHostToDevice);
-  cudaFuncSetAttribute(k_conv_fft<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<float>());
-  cudaFuncSetAttribute(k_conv_fft<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<double>());
+  cudaFuncSetAttribute(k_conv_fft<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<float>(MAXM));
+  cudaFuncSetAttribute(k_conv_fft<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<double>(MAXM));
   c->part_stride = std::max(c->part_stride, c->num_sms * 8);
   return check_launch(c, "conv fft setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
@@ -331,7 +343,7 @@ cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStre
   a.colsum = c->sharded ? c->colsum : nullptr;
   const bool f64 = j0 == 0 || c->probe64;
   const void* fn = f64 ? (const void*)k_conv_fft<double> : (const void*)k_conv_fft<float>;
-  const size_t sm = f64 ? smem_bytes<double>() : smem_bytes<float>();
+  const size_t sm = f64 ? smem_bytes<double>(a.ncols) : smem_bytes<float>(a.ncols);
   int occ = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, NW * 32, sm);
   const int64_t items = (int64_t)a.ncols * (((c->D + V - 1) / V + NW - 1) / NW);
