@@ -95,11 +95,19 @@ __device__ __forceinline__ void canon(int lane, int r, int (&o)[4]) {
 
 // Per-launch column info, read once per CTA: frozen flags and direction coefficients b_j
 // (R5; a6), plus per-warp gamma accumulators for pass C (reduced once per CTA at exit).
-struct ColInfo {
+struct ColFlags {          // passes without a reduction (1.5 KB of static shared memory)
   int frozen[MAXM];
   double b[MAXM];
+};
+struct ColInfo : ColFlags {
   double g[8][MAXM];
 };
+__device__ __forceinline__ void load_colinfo(ColFlags& ci, const ColState* cs, int j0, int ncols) {
+  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
+    const ColState c = cs[j0 + jj];
+    ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
+  }
+}
 __device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, int j0, int ncols, bool zero_g) {
   for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
     const ColState c = cs[j0 + jj];
@@ -113,7 +121,7 @@ __device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, in
 // wrote in load_colinfo, so no barrier is needed before the vote.  A launch whose columns have
 // all frozen (R5) returns before staging the tables: every CTA takes the same exit, so the
 // last-CTA tickets are untouched.
-__device__ __forceinline__ bool any_active(const ColInfo& ci, int ncols) {
+__device__ __forceinline__ bool any_active(const ColFlags& ci, int ncols) {
   int act = 0;
   for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) act |= !ci.frozen[jj];
   return __syncthreads_or(act) != 0;

@@ -136,12 +136,15 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
                                               const Tw<T>& tb);
 
 template <typename T>
-__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j0, int ncols, int dir) {
+#ifndef COFEM_1K_INV_MINB
+#define COFEM_1K_INV_MINB 1   // explicit: nvcc then takes 96 registers (2 CTAs per SM): 47.7 -> 47.1 ms; 3: 47.6, 4: 48.4
+#endif
+__global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_INV_MINB : 1) k1k_rows_inv(DctArgs a, int j0, int ncols, int dir) {
   constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
-  __shared__ ColInfo ci;
-  load_colinfo(ci, a.cs, j0, ncols, false);
+  __shared__ ColFlags ci;
+  load_colinfo(ci, a.cs, j0, ncols);
   if (!any_active(ci, ncols)) return;
   if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT]) {   // the first item's rows, before the tables
     const DctCol<T> cn = col_of<T>(a, j0 + blockIdx.x / NT);
@@ -149,7 +152,8 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_inv(DctArgs a, int j
     pf_line(cn.p + rn);
     if (dir) pf_line(cn.r + rn);
   }
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  // pass A needs the FFT twiddles and the DCT-III pre tables only: the [0, TR1) prefix (12.8 KB in fp32)
+  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG), TR1);   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
@@ -501,13 +505,13 @@ __global__ void k1k_mask_lanes(const uint8_t* __restrict__ maskT, uint32_t* __re
   maskL[idx] = w;
 }
 
-template <typename T> static size_t smem_bytes() {
-  return (size_t)Geo<T>::RT * WREG * sizeof(T) + (size_t)TTOT * sizeof(cplx<T>);
+template <typename T> static size_t smem_bytes(int ntab = TTOT) {
+  return (size_t)Geo<T>::RT * WREG * sizeof(T) + (size_t)ntab * sizeof(cplx<T>);
 }
 
 template <typename T> static void set_attrs() {
   const int s = (int)smem_bytes<T>();
-  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(TR1));
   cudaFuncSetAttribute(k1k_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
   cudaFuncSetAttribute(k1k_rows_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
 }
@@ -588,11 +592,11 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   // concurrent probe groups): an eighth at >= 32 probes (57.3 vs 57.5 ms for a quarter), a
   // quarter at >= 16 (33.1 vs 33.3 for an eighth), half below (21.1 vs 24.0 at 8 probes)
   static const int mean_sms_env = getenv("COFEM_1K_MEAN_SMS") ? atoi(getenv("COFEM_1K_MEAN_SMS")) : -1;
-  auto grid_of = [&](const void* fn) {
+  auto grid_of = [&](const void* fn, size_t smb) {
     const int items = ncols * Work<T>::NTILE;
     if (slots_env == 0) return items;                  // one CTA per work item
     int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, RT * 32, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, RT * 32, smb);
     const int per_sm = slots_env > 0 ? std::min(slots_env, occ) : occ;
     int g = std::min(std::min(c->num_sms * per_sm, items), c->part_stride);
     if (j0 == 0 && c->fast1k) {
@@ -610,13 +614,14 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const dim3 blk(RT * 32);
   const bool mean = j0 == 0;        // the fp64 mean column is timed as its own class
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
-  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>), blk, sm, st>>>(a, j0, ncols, dir ? 1 : 0);
+  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(TR1)), blk, smem_bytes<T>(TR1), st>>>(
+      a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_COLS, st);
-  k1k_cols<T><<<grid_of((const void*)k1k_cols<T>), blk, sm, st>>>(a, j0, ncols);
+  k1k_cols<T><<<grid_of((const void*)k1k_cols<T>, sm), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_COLS, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
-  k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>), blk, sm, st>>>(a, j0, ncols);
+  k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>, sm), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
   return check_launch(c, "dct1k apply") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
