@@ -129,15 +129,27 @@ class CircConvOp:
             raise ValueError("D must be >= number of taps")
 
     def apply(self, V):
-        out = np.zeros_like(V, dtype=np.float64)
+        """(Phi V)_i = sum_j h_j V_{(i-j) mod D}, summed in tap order j = 0..T-1.
+        The wrapped rows are read from a copy of V with its last T-1 rows in front,
+        Vw[i + T-1] = V[(i) mod D] for i >= -(T-1), so Vw[T-1-j : T-1-j+D][i] = V[(i-j) mod D]
+        (the same products and sums as np.roll(V, j), without the per-tap copy)."""
+        V = np.asarray(V, dtype=np.float64)
+        T, D = self.h.size, self.D
+        Vw = np.concatenate([V[D - (T - 1):], V]) if T > 1 else V
+        out = np.zeros_like(V)
         for j, hj in enumerate(self.h):
-            out += hj * np.roll(V, j, axis=0)      # roll(x, j)[i] = x[i - j]
+            out += hj * Vw[T - 1 - j:T - 1 - j + D]
         return out
 
     def apply_T(self, W):
-        out = np.zeros_like(W, dtype=np.float64)
+        """(Phi^T W)_i = sum_j h_j W_{(i+j) mod D}, tap order j = 0..T-1; Ww[i] = W[i mod D]
+        for i < D + T-1, so Ww[j : j+D][i] = W[(i+j) mod D]."""
+        W = np.asarray(W, dtype=np.float64)
+        T, D = self.h.size, self.D
+        Ww = np.concatenate([W, W[:T - 1]]) if T > 1 else W
+        out = np.zeros_like(W)
         for j, hj in enumerate(self.h):
-            out += hj * np.roll(W, -j, axis=0)     # roll(w, -j)[i] = w[i + j]
+            out += hj * Ww[j:j + D]
         return out
 
     def colsq(self):

@@ -123,6 +123,29 @@ def test_eps_zero_is_the_fixed_u_run():
 
 
 # ---------------------------------------------------------------- E/M-step
+def test_estep_jacobi_diag_uses_alpha_one_iteration_exact():
+    """Pins jacobi_diag's alpha term (R6, diag(A) = beta colsq + alpha, A of Eq. 7 / P:133 depends
+    on alpha) through estep.  Phi with orthogonal columns of different norms makes
+    A = beta Phi^T Phi + diag(alpha) diagonal; Jacobi-PCG with the TRUE diagonal then solves
+    every column in one iteration (z = A^-1 r is already the solution direction, a = 1), so at
+    U = 1 and a non-uniform alpha: mu = b0_d / (beta c_d + alpha_d) and, since each x_k is
+    exact, s_d = Sigma_dd = 1 / (beta c_d + alpha_d) (Eq. 4/6) for any probes.  A diagonal
+    without alpha (or with alpha = 1) leaves z off the solution direction and misses both."""
+    rng = np.random.default_rng(7)
+    D = 12
+    Q, _ = np.linalg.qr(rng.standard_normal((16, D)))       # orthonormal columns (16 x 12)
+    c = rng.uniform(0.5, 3.0, D)
+    phi = Q * np.sqrt(c)[None, :]                           # Phi^T Phi = diag(c) exactly (up to u)
+    y = rng.standard_normal(16)
+    beta = 2.0
+    alpha = rng.uniform(0.2, 5.0, D)                        # non-uniform prior precisions
+    mu, s, rep = estep(DenseOp(phi), y, beta, alpha, K=3, seed=4, t=0, U=1)
+    lam = beta * c + alpha                                  # the exact eigenvalues of A
+    b0 = beta * (Q.T @ y) * np.sqrt(c)                      # beta Phi^T y, computed from Q, c
+    assert np.allclose(mu, b0 / lam, rtol=1e-10, atol=0), np.max(np.abs(mu * lam / b0 - 1))
+    assert np.allclose(s, 1.0 / lam, rtol=1e-10, atol=0), np.max(np.abs(s * lam - 1))
+
+
 def test_estep_phi_zero_gives_identity_system():
     op = DenseOp(np.zeros((3, 10)))
     mu, s, _ = estep(op, np.ones(3), 5.0, np.ones(10), K=4, seed=1, t=0, U=5)   # S:215
