@@ -9,10 +9,13 @@ N = 2^18, K = 32, U = 200), with alpha carried from step to step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C4]
 
-N > 1 (torchrun, one process per GPU): probe-parallel — each rank solves its
-share of the K probes plus a replica of the mean column; one NCCL all-reduce of
-s per E-step; total work fixed ("strong").  --impl reference times the CPU
-fp64 oracle (oracle/) on a bounded sample (rank 0 only).
+N > 1 (one process per GPU; `--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset): probe-parallel inside the library (cofem_options.dist_mode = 1) — rank 0
+solves the mean system and a smaller share of the K probes, the others their shares; one NCCL
+all-reduce of s and one broadcast of mu per E-step; total work fixed ("strong").  The line
+carries the N-rank vs 1-rank difference of mu and s (multirank_check).  --mode column: the
+column-sharded dense / D-sharded convolution modes.  --impl reference times the CPU fp64 oracle
+(oracle/) on a bounded sample (rank 0 only).
 """
 import argparse
 import json
@@ -41,6 +44,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-conformance", action="store_true",
+                    help="skip the fast-vs-parity-mode support comparison (2 extra EM iterations per mode)")
     ap.add_argument("--prof-steps", type=int, default=0,
                     help="EM iterations of the per-kernel profiled pass (0 = all timed iterations)")
     ap.add_argument("--rtol", type=float, default=0.0,
@@ -179,17 +184,6 @@ def active_bytes(cls, w, K_local, D_local, groups, frozen):
     return tot, colit / float(max(1, U * K * len(frozen)))
 
 
-def mean_cost(w):
-    """Effective cost of the fp64 mean system in probe columns, for probe_split_owner.  It runs
-    on a side stream concurrently with the probes, so its cost is the extra time it adds to a
-    rank, measured with tools/time_estep.py (C4 fixed alpha, per-rank E-step): +2.3 ms at 16
-    probes, +3.4 ms at 5, alone 9.7 ms vs ~2 ms per probe column -> ~2 probe columns.  Dense: the
-    mean column rides in every rank's tensor-core kernels anyway (no saving, cost 0)."""
-    if w.kind == "dense":
-        return 0.0
-    return 2.0 if w.kind == "circconv" or (w.rows, w.cols) == (1024, 1024) else 1.0
-
-
 def working_set_bytes(w, K_local, D_local):
     """Bytes one E-step keeps touching: ~5 fp32 vectors per probe column (r, p, q, x, z) plus
     the operator's own storage (dense Phi; the DCT mask and conv taps are negligible)."""
@@ -270,8 +264,38 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------ our arm
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a torchrun environment: re-launch this script as N ranks (one
+    process per GPU) with torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def executed_applies(frozen, U):
+    """Column-iterations whose apply actually ran: a column frozen at CG iteration F (R5,
+    report frozen_at) is applied in iterations 0..F (the apply of iteration F finds it frozen)."""
+    return sum(sum(U if f < 0 else min(f + 1, U) for f in fz) for fz in frozen)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -284,8 +308,8 @@ def main():
     import torch
 
     import synth
-    from paper_2202_12808_b200 import Context
-    from paper_2202_12808_b200.dist import column_shard, probe_split_owner
+    from paper_2202_12808_b200 import Context, get_unique_id
+    from paper_2202_12808_b200.dist import column_shard
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -293,59 +317,47 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     w = synth.preset(args.workload, seed=args.seed)
     column = args.mode == "column"
+    nid = None
+    if world > 1:       # the library's own NCCL communicator: one id from rank 0, broadcast
+        box = [get_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(box, src=0)
+        nid = box[0]
+    d0 = 0
     if column:
-        # column-sharded dense Phi: rank r holds Phi[:, d0:d0+Dr] and the D-slices of
-        # alpha, mu, s; the library all-reduces W and the column dots over NCCL inside the E-step
+        # column-sharded dense Phi / D-sharded convolution: rank r holds the D-slice
+        # [d0, d0 + Dr) of Phi (or of the signal) and of alpha, mu, s; the library all-reduces W and
+        # the column dots (or exchanges the 64-sample halos) over NCCL inside the E-step
         if w.kind not in ("dense", "circconv"):
             raise SystemExit("--mode column needs a dense (C1-C3, column-sharded) or convolution (C5, D-sharded) workload")
-        from paper_2202_12808_b200 import OP_CIRCCONV, OP_DENSE, get_unique_id
+        from paper_2202_12808_b200 import OP_CIRCCONV, OP_DENSE
         d0, Dr = column_shard(w.D, world, rank)
-        nid = get_unique_id() if rank == 0 else bytes(128)
-        if world > 1:
-            box = [nid]
-            torch.distributed.broadcast_object_list(box, src=0)
-            nid = box[0]
-        k_off, K_loc = 0, w.K
+        if nid is None:
+            nid = get_unique_id()
         if w.kind == "dense":
             ctx = Context(OP_DENSE, w.N, Dr, w.y, w.beta, phi=np.ascontiguousarray(w.phi[:, d0:d0 + Dr]),
                           cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
                           D_global=w.D, cg_rtol=args.rtol)
-        else:   # D-sharded circular convolution: 64-sample halos exchanged with both ring neighbours
+        else:
             ctx = Context(OP_CIRCCONV, Dr, Dr, np.ascontiguousarray(w.y[d0:d0 + Dr]), w.beta, taps=w.taps,
                           cg_iters=w.U, max_probes=w.K, rank=rank, world=world, nccl_id=nid, d_offset=d0,
                           D_global=w.D, cg_rtol=args.rtol)
         D = Dr
+    elif world > 1:
+        # probe-parallel inside the library (dist_mode 1): global K, owner split (rank 0 also solves
+        # the mean system), one NCCL all-reduce of s and a broadcast of mu per E-step
+        ctx = Context.from_workload(w, max_probes=(w.K + world - 1) // world + 2, rank=rank, world=world,
+                                    nccl_id=nid, dist_mode=1, cg_rtol=args.rtol)
+        D = w.D
     else:
-        # rank 0 owns the mean system (fewer probes), the others run cofem_estep_probes and get mu
-        # by broadcast; mean_cost = its cost in probe columns, measured per operator
-        k_off, K_loc, owns_mean = probe_split_owner(w.K, world, rank, mean_cost(w))
-        ctx = Context.from_workload(w, max_probes=K_loc, cg_rtol=args.rtol)
+        ctx = Context.from_workload(w, cg_rtol=args.rtol)
         D = w.D
     alpha = torch.ones(D, dtype=torch.float64, device=dev)
     mu = torch.empty_like(alpha)
     s = torch.empty_like(alpha)
     seed = args.seed
 
-    def probe_estep(a_in, t):
-        if owns_mean:
-            ctx.estep(a_in, K_loc, seed, t, mu, s, k_offset=k_off, K_total=w.K)
-        else:
-            ctx.estep_probes(a_in, K_loc, seed, t, s, k_offset=k_off, K_total=w.K)
-        torch.distributed.all_reduce(s)
-        torch.distributed.broadcast(mu, src=0)
-
-    def step(t, a_in, a_out, m_out, s_out):
-        if world == 1 or column:
-            ctx.em(1, w.K, seed, t, a_in, a_out, m_out, s_out)
-        else:
-            probe_estep(a_in, t)
-            ctx.mstep(mu, s, alpha)
-            if a_out is not alpha:
-                a_out.copy_(alpha)
-            if m_out is not None and m_out is not mu:
-                m_out.copy_(mu)
-            if s_out is not None and s_out is not s:
-                s_out.copy_(s)
+    def step(t, a_in, a_out, m_out, s_out):       # one EM iteration through the C ABI (all modes)
+        ctx.em(1, w.K, seed, t, a_in, a_out, m_out, s_out)
 
     def barrier():
         if world > 1:
@@ -356,6 +368,7 @@ def main():
     for _ in range(args.warmup):
         step(t, alpha, alpha, mu, s)
         t += 1
+    K_loc = ctx.report()["cols"] - 1            # this rank's probe columns (the library's split)
     # ---- device-timed region (inputs resident in HBM; the library replays one captured
     # CUDA graph per E-step)
     classes = ["dct_rows_inv", "dct_cols", "dct_rows_fwd", "pcg_update", "pcg_direction", "conv_apply",
@@ -398,10 +411,10 @@ def main():
         torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
     ms = float(ms_t.item())
     value = args.steps / (ms / 1000.0)
-    rhs_applies = (w.K + 1) * w.U * args.steps / (ms / 1000.0)
+    support_cert = ctx.report()["support"]
 
     # ---- per-kernel-class device time: a separate profiled pass (CUDA events around every
-    # launch on its stream, uncaptured) replaying the first args.prof_steps timed EM iterations
+    # launch on its stream, uncaptured) replaying the timed EM iterations
     ctx.profile_enable(classes)
     for c in classes:
         ctx.profile_read(c, reset=True)
@@ -426,6 +439,14 @@ def main():
     busy = {c: ctx.profile_busy(c) for c in classes}
     prof = {c: ctx.profile_read(c) for c in classes}
     ctx.profile_enable([])
+    # RHS-operator applies per second (BASELINE metric): executed column-iterations of this rank
+    # (mean column included; frozen columns do no work) summed over ranks, over the timed time
+    ex = torch.tensor([float(executed_applies(frozen, w.U))], dtype=torch.float64, device=dev)
+    if world > 1 and not column:
+        torch.distributed.all_reduce(ex)      # probe-parallel: ranks hold different columns
+    ex_per_step = float(ex.item()) / args.prof_steps
+    rhs_applies = ex_per_step * args.steps / (ms / 1000.0)
+    rhs_nominal = (w.K + 1) * w.U * args.steps / (ms / 1000.0)
 
     # ---- end-to-end through the C ABI with pinned host buffers
     e2e = None
@@ -439,12 +460,7 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(args.steps):
-            if world == 1 or column:
-                ctx.em(1, w.K, seed, t, a_h, a_h, m_h, s_h)      # h2d alpha; d2h alpha, mu, s
-            else:
-                probe_estep(a_h, t)
-                ctx.mstep(mu, s, a_h)
-                m_h.copy_(mu); s_h.copy_(s)
+            ctx.em(1, w.K, seed, t, a_h, a_h, m_h, s_h)      # h2d alpha; d2h alpha, mu, s
             t += 1
         f1.record()
         barrier()
@@ -454,12 +470,66 @@ def main():
         e2e = {"value": args.steps / (float(ems.item()) / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": D * 8, "d2h_bytes_per_step": 3 * D * 8}
 
+    # ---- multi-rank correctness: this N-rank E-step against a 1-rank single-GPU context on rank 0
+    multirank = None
+    if world > 1:
+        mu_n, s_n = torch.empty_like(alpha), torch.empty_like(alpha)
+        ctx.estep(alpha_timed, w.K, seed, t_timed, mu_n, s_n)
+        a_full, mu_f, s_f = alpha_timed, mu_n, s_n
+        if column:                      # gather the D-slices (padded to the largest slice)
+            sizes = [column_shard(w.D, world, r)[1] for r in range(world)]
+            mx = max(sizes)
+
+            def gather(v):
+                pad = torch.zeros(mx, dtype=torch.float64, device=dev)
+                pad[:v.numel()] = v
+                parts = [torch.empty_like(pad) for _ in range(world)]
+                torch.distributed.all_gather(parts, pad)
+                return torch.cat([p[:n] for p, n in zip(parts, sizes)])
+            a_full, mu_f, s_f = gather(alpha_timed), gather(mu_n), gather(s_n)
+        if rank == 0:
+            ref = Context.from_workload(w)
+            mu1, s1 = torch.empty_like(a_full), torch.empty_like(a_full)
+            ref.estep(a_full, w.K, seed, t_timed, mu1, s1)
+            torch.cuda.synchronize()
+            mrel = lambda a, b: float((a - b).abs().max() / b.abs().max())
+            multirank = {"ref": "1-rank single-GPU context on rank 0: same alpha, t and probes",
+                         "mu_max_rel_diff": mrel(mu_f, mu1), "s_max_rel_diff": mrel(s_f, s1),
+                         "mu_rel_l2": float((mu_f - mu1).norm() / mu1.norm()),
+                         "s_rel_l2": float((s_f - s1).norm() / s1.norm())}
+            ref.close()
+        barrier()
+
+    # ---- conformance: two EM iterations from the timed alpha in fast mode (fp32
+    # probe columns, this bench's path) and in parity mode (every column fp64, which matches the
+    # fp64 oracle to ~1e-7): support flips between them, each with its margin
+    conformance = None
+    if world == 1 and not args.no_conformance:
+        par = Context.from_workload(w, probe_precision=1, cg_rtol=args.rtol)
+        outs = []
+        for cx in (ctx, par):
+            ao, mo, so = torch.empty_like(alpha), torch.empty_like(alpha), torch.empty_like(alpha)
+            cx.em(2, w.K, seed, t_timed, alpha_timed, ao, mo, so)
+            outs.append((ao.cpu().numpy(), mo.cpu().numpy()))
+        par.close()
+        (af, mf), (ap, mp) = outs
+        thr = 1e-3
+        mxp = np.max(np.abs(mp))
+        sf, sp = np.abs(mf) > thr * np.max(np.abs(mf)), np.abs(mp) > thr * mxp
+        fl = np.nonzero(sf != sp)[0]
+        conformance = {"vs": "parity mode (probe_precision = 1, fp64 probe columns) on this GPU, same alpha/t/probes",
+                       "em_iters": 2, "support_size": int(sp.sum()), "support_flips": int(fl.size),
+                       "flips": [{"d": int(d), "margin": float(abs(abs(mp[d]) / mxp - thr)),
+                                  "dmu": float(abs(mf[d] - mp[d]) / mxp)} for d in fl[:10]],
+                       "mu_rel_l2": float(np.linalg.norm(mf - mp) / np.linalg.norm(mp)),
+                       "inv_alpha_rel_l2": float(np.linalg.norm(1 / af - 1 / ap) / np.linalg.norm(1 / ap)),
+                       "library_certificate": support_cert}
+
     # ---- roofline of the dominant kernel (live CUDA events over the timed region)
     pk, pk_kind = peaks()
-    # dominant = the HBM-bound class with the largest busy time (union of its launch intervals:
-    # concurrent probe groups count once); dct_cols is issue-bound (two FFTs per 8 B/element,
-    # DESIGN §7.1) and has no HBM roofline; the whole-step HBM roofline is roofline.step
-    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc, D) and c != "dct_cols"),
+    # dominant = the class with the largest busy time (union of its launch intervals: concurrent
+    # probe groups count once) among the classes with algorithmic bytes
+    dom = max((c for c in classes if prof[c][1] > 0 and algorithmic_bytes(c, w, K_loc, D)),
               key=lambda c: busy[c] if busy[c] > 0 else prof[c][0])
     tot_ms, cnt = prof[dom]
     avg_ms = tot_ms / cnt
@@ -500,28 +570,52 @@ def main():
                             "(probe classes; the fp64 mean column is not counted)"},
             "share_of_step": share, "busy_share_of_step": busy_share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
             args.prof_steps}
+    if w.kind == "dense" and flush is not None:
+        # Phi fits in L2 (C1, C2): the dense GEMMs are bound by the tensor pipe, not HBM.  3xTF32 =
+        # 3 tf32 MMAs per product, 2 N D flops per column per GEMM; tf32 peak = measured bf16 x 1/2
+        # (B200_PROFILING nominal ratio)
+        probe_ex = sum(sum(w.U if f < 0 else min(f + 1, w.U) for f in fz[1:]) for fz in frozen)
+        tf32_peak = pk.get("bf16_tflops", 1638.5) / 2.0
+        gemm_ms = busy.get("dense_phi_p", 0) + busy.get("dense_phiT_w", 0)
+        fl = 3 * 2 * 2 * w.N * D * probe_ex
+        if gemm_ms > 0:
+            ach = fl / (gemm_ms / 1000.0) / 1e12
+            roof.update({"bound": "tensor", "kernel": "dense_phi_p + dense_phiT_w", "achieved": ach,
+                         "peak": tf32_peak, "unit": "TFLOP/s", "frac": ach / tf32_peak,
+                         "peak_source": pk_kind + " bf16 x 1/2 (nominal tf32 ratio)",
+                         "achieved_def": "3xTF32 MMA flops (3 x 2 N D per probe column per GEMM, executed "
+                                         "column-iterations) / busy time of the two GEMM classes",
+                         "hbm_view": {"kernel": dom, "achieved": achieved, "frac_of_hbm": achieved / pk["hbm_gbs"],
+                                      "note": "Phi (%.0f MB) is L2-resident between launches" % (w.N * D * 4 / 1e6)}})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, desc, threads, _ = cpu_sample(w, seed)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+               "extrapolated": True, "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32 (probe columns) + f64 (mean column)",
+                "scaling": "strong" if not column or w.kind == "dense" else "strong",
+                "vs_baseline": None, "dtype": "f32 (probe columns) + f64 (mean column)",
                 "data": "synthetic",
                 "config": {"workload": w.name, **w.config(),
                            "parallelism": (("column-sharded x%d" if w.kind == "dense" else "D-sharded x%d") if column
-                                           else "probe-parallel x%d" + (", rank 0 owns the mean system"
+                                           else "probe-parallel x%d" + (" (library-owned NCCL: all-reduce of s, "
+                                                                         "broadcast of mu; rank 0 owns the mean system)"
                                                                          if world > 1 else "")) % world,
                            "K_per_rank": K_loc, "D_per_rank": D, **({"cg_rtol": args.rtol} if args.rtol > 0 else {}),
                            "l2": ("inputs larger than L2 (working set %.0f MB > 126 MB)" % ws_mb if flush is None
                                   else "working set %.1f MB fits in L2: 256 MB flush write before every timed "
                                        "EM iteration, outside its events" % ws_mb)},
-                "rhs_applies_per_s": rhs_applies, "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-                "clocks": clocks, "gpu_launches": launches}
+                "rhs_applies_per_s": rhs_applies,
+                "rhs_applies_def": "executed column-iterations (frozen columns, R5, do no work; mean column "
+                                   "included) per second; nominal (K+1) U per EM iteration: %.0f/s" % rhs_nominal,
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "multirank_check": multirank,
+                "conformance": conformance, "clocks": clocks, "gpu_launches": launches}
         print(json.dumps(line), flush=True)
+    ctx.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0

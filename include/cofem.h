@@ -18,8 +18,9 @@
  *    and stages host buffers through its own device workspace with
  *    cudaMemcpyAsync on the context's stream.  Device pointers must be on the
  *    context's device.  The caller owns every buffer it passes.
- *  - Phi (DENSE) is copied at setup (the library owns its device copy); it is
- *    never modified.
+ *  - Phi (DENSE) is never modified.  A DEVICE Phi is borrowed (zero-copy, row
+ *    stride ld; the tensor-core path needs ld % 4 == 0) and must outlive the
+ *    context; a HOST Phi is copied to a library-owned device buffer at setup.
  *  - Every call enqueues on the context's CUDA stream and returns after one
  *    stream synchronisation (needed to report numerical breakdown).
  *  - A context serves one stream and is not thread-safe.
@@ -98,13 +99,33 @@ typedef struct {
    * criterion holds and the remaining iterations launch but do no column work.  U stays the cap.
    * 0 (default): fixed U iterations (BASELINE north_star, R5).  Must be in [0, 1). */
   double cg_rtol;
+  /* Operator path (tests, comparisons): 0 = auto, the fastest eligible kernels (dense: tcgen05
+   * 3xTF32 for fp32 probes; DCT2 1024 x 1024: the warp-per-line FFT path; CIRCCONV: overlap-save
+   * FFT); 1 = the general kernels (dense FP32 SIMT, generic DCT passes, direct 127-tap stencil). */
+  int32_t apply_path;
+  /* 1024 x 1024 DCT path: probe columns run as this many concurrent groups on their own streams
+   * (DESIGN.md §7.1); 0 = auto (2).  Range 0..4. */
+  int32_t probe_groups;
+  /* 1 (default): each E-step is captured once into a CUDA graph and replayed; 0: launched directly. */
+  int32_t use_graph;
+  /* Multi-GPU mode; rank, world and nccl_id as above.
+   *  0: single GPU, or (nccl_id set) the sharded mode the operator implies: column-sharded DENSE /
+   *     D-sharded CIRCCONV (d_offset, D_global);
+   *  1: probe-parallel (BASELINE north_star "probe-parallel when Phi fits on one GPU"): every rank
+   *     holds the whole operator; cofem_estep / cofem_em take the GLOBAL K and this library splits
+   *     the probes over the ranks (global Philox indices, R8; rank 0 also solves the mean system
+   *     with fewer probes), then sums s over ranks (one NCCL all-reduce of D fp64 per E-step) and
+   *     broadcasts mu = x0 from rank 0; every rank returns the same mu, s and alpha.  max_probes is
+   *     the per-rank capacity (>= ceil(K / world) + 1). */
+  int32_t dist_mode;
 } cofem_options;
 
 /* NCCL unique id for cofem_options.nccl_id (call on one rank, broadcast the 128 bytes).
  * Returns COFEM_ERR_NCCL if libnccl.so.2 cannot be loaded. */
 cofem_status cofem_get_unique_id(uint8_t id[128]);
 
-/* Fill *opt with the defaults above (U = 100, precond = 1, max_probes = 32, single GPU). */
+/* Fill *opt with the defaults above (U = 100, precond = 1, max_probes = 32, apply_path = 0,
+ * probe_groups = 0, use_graph = 1, single GPU). */
 void cofem_default_options(cofem_options* opt);
 
 /* Build a context: validate, copy/derive the operator (dense Phi copy; DCT
@@ -171,7 +192,25 @@ typedef struct {
   int32_t bad_col, bad_iter;      /* first column that met NaN/Inf, -1 if none */
   double estep_ms_last;           /* device time of the last E-step (CUDA events) */
   int64_t launches;               /* kernels launched by this context so far */
+  /* Support certificate of the last E-step's mu (BASELINE north_star: recovered support
+   * |mu_d| > 1e-3 max|mu|, reading R16; SURVEY §8(c) "fragility"): support_count coordinates are
+   * in the support; support_adjacent of them or of the rest lie within support_delta of the
+   * threshold, | |mu_d| / max|mu| - 1e-3 | < support_delta -- the only coordinates whose membership
+   * a relative perturbation of mu below support_delta (e.g. fp32 probe columns vs fp64) can flip;
+   * support_min_margin is the smallest such margin over all d.  support_delta = 1e-6. */
+  int64_t support_count, support_adjacent;
+  double support_max_abs_mu, support_min_margin, support_delta;
 } cofem_report;
+
+/* The probe-parallel owner split (dist_mode 1) of a global K over `world` ranks, a host-only
+ * utility (no GPU): rank 0 owns the mean system and K0 = max(1, min(K - (world - 1),
+ * floor((K + mean_cost) / world - mean_cost + 1/2))) probes; ranks 1.. split the remaining K - K0
+ * contiguously.  mean_cost = the mean system's cost in probe columns (the library uses 2 on the
+ * 1024 x 1024 DCT and FFT-convolution paths, 0 on the dense tensor-core path).  Writes the first
+ * global probe index, the count and whether the rank solves the mean system.
+ * Errors: COFEM_ERR_INVALID when K < world or rank is out of range. */
+cofem_status cofem_probe_split(int32_t K, int32_t world, int32_t rank, double mean_cost, int32_t* k_offset,
+                               int32_t* K_local, int32_t* owns_mean);
 
 /* Report of the last E-step; the pointers stay valid until the next call on ctx. */
 cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out);

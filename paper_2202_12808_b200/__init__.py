@@ -5,4 +5,4 @@ The product is the C-ABI library `libcofem.so` (include/cofem.h) built from
 fallback.  See DESIGN.md.
 """
 from .cofem import (OP_CIRCCONV, OP_DCT2_MASKED, OP_DENSE, CofemError, Context, get_unique_id,  # noqa: F401
-                    kernel_classes, lib)
+                    kernel_classes, lib, probe_split)

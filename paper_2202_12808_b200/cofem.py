@@ -42,14 +42,18 @@ class _Options(ctypes.Structure):
     _fields_ = [("cg_iters", ctypes.c_int32), ("precond", ctypes.c_int32), ("den_floor", ctypes.c_double),
                 ("alpha_max", ctypes.c_double), ("probe_precision", ctypes.c_int32),
                 ("max_probes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("nccl_id", ctypes.c_void_p), ("cg_rtol", ctypes.c_double)]
+                ("nccl_id", ctypes.c_void_p), ("cg_rtol", ctypes.c_double), ("apply_path", ctypes.c_int32),
+                ("probe_groups", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("dist_mode", ctypes.c_int32)]
 
 
 class _Report(ctypes.Structure):
     _fields_ = [("cols", ctypes.c_int32), ("cg_iters", ctypes.c_int32),
                 ("frozen_at", ctypes.POINTER(ctypes.c_int32)), ("rho", ctypes.POINTER(ctypes.c_double)),
                 ("rho0", ctypes.POINTER(ctypes.c_double)), ("bad_col", ctypes.c_int32),
-                ("bad_iter", ctypes.c_int32), ("estep_ms_last", ctypes.c_double), ("launches", ctypes.c_int64)]
+                ("bad_iter", ctypes.c_int32), ("estep_ms_last", ctypes.c_double), ("launches", ctypes.c_int64),
+                ("support_count", ctypes.c_int64), ("support_adjacent", ctypes.c_int64),
+                ("support_max_abs_mu", ctypes.c_double), ("support_min_margin", ctypes.c_double),
+                ("support_delta", ctypes.c_double)]
 
 
 # (name, restype, argtypes) — every entry point of include/cofem.h
@@ -69,6 +73,9 @@ SYMBOLS = [
     ("cofem_em", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_last_report", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_Report)]),
+    ("cofem_probe_split", ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_int32)]),
     ("cofem_profile_enable", ctypes.c_int, [ctypes.c_void_p, ctypes.c_uint32]),
     ("cofem_profile_busy", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     ("cofem_profile_read", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
@@ -107,6 +114,17 @@ def get_unique_id():
     return buf.raw
 
 
+def probe_split(K, world, rank, mean_cost):
+    """The library's probe-parallel owner split (cofem_probe_split, host only):
+    (k_offset, K_local, owns_mean)."""
+    o, n, m = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    st = lib().cofem_probe_split(int(K), int(world), int(rank), float(mean_cost), ctypes.byref(o), ctypes.byref(n),
+                                 ctypes.byref(m))
+    if st != 0:
+        raise CofemError(st, lib().cofem_last_error(None).decode())
+    return o.value, n.value, bool(m.value)
+
+
 def kernel_classes():
     out, i = [], 0
     while True:
@@ -143,18 +161,22 @@ class Context:
 
     def __init__(self, kind, N, D, y, beta, phi=None, rows=0, cols=0, obs_idx=None, convention=0, taps=None,
                  cg_iters=100, precond=1, probe_precision=0, max_probes=32, den_floor=1e-12, alpha_max=1e12,
-                 stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None, cg_rtol=0.0):
-        """Column-sharded dense mode: phi holds this rank's columns
-        [d_offset, d_offset + D) of D_global; nccl_id = get_unique_id() from one rank,
-        broadcast; the library all-reduces W and the column dots over NCCL itself."""
+                 stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None, cg_rtol=0.0, apply_path=0,
+                 probe_groups=0, use_graph=True, dist_mode=0, ld=None):
+        """Multi-GPU; nccl_id = get_unique_id() from one rank, broadcast to all.
+        dist_mode 0 with nccl_id: column-sharded dense / D-sharded conv -- phi (or y) holds this
+        rank's slice [d_offset, d_offset + D) of D_global; the library all-reduces W and the column
+        dots (or exchanges halos) over NCCL itself.  dist_mode 1: probe-parallel -- every rank holds
+        the whole operator, estep/em take the GLOBAL K, the library splits the probes, all-reduces s
+        and broadcasts mu.  apply_path 1: the general kernels (tests); use_graph False: no CUDA graph."""
         L = lib()
         self.N, self.D, self.kind = int(N), int(D), int(kind)
         self._keep = [y, phi, obs_idx, taps]
         op = _Operator()
         op.kind, op.N, op.D = self.kind, self.N, self.D
-        if phi is not None:
-            op.phi = _ptr(phi, np.float32, self.N * self.D, "phi")
-            op.ld = self.D
+        if phi is not None:        # a CUDA tensor is borrowed (zero-copy, row stride ld), host data copied
+            op.ld = self.D if ld is None else int(ld)
+            op.phi = _ptr(phi, np.float32, (self.N - 1) * op.ld + self.D, "phi")
         op.rows, op.cols, op.convention = int(rows), int(cols), int(convention)
         op.d_offset, op.D_global = int(d_offset), int(D_global)
         if obs_idx is not None:
@@ -169,6 +191,8 @@ class Context:
         opt.den_floor, opt.alpha_max = float(den_floor), float(alpha_max)
         opt.rank, opt.world = int(rank), int(world)
         opt.cg_rtol = float(cg_rtol)
+        opt.apply_path, opt.probe_groups = int(apply_path), int(probe_groups)
+        opt.use_graph, opt.dist_mode = int(bool(use_graph)), int(dist_mode)
         if nccl_id is not None:
             self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opt.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)
@@ -246,7 +270,10 @@ class Context:
                 "frozen_at": [r.frozen_at[i] for i in range(n)],
                 "rho": [r.rho[i] for i in range(n)], "rho0": [r.rho0[i] for i in range(n)],
                 "bad_col": r.bad_col, "bad_iter": r.bad_iter, "estep_ms": r.estep_ms_last,
-                "launches": r.launches}
+                "launches": r.launches,
+                "support": {"count": r.support_count, "adjacent": r.support_adjacent,
+                            "max_abs_mu": r.support_max_abs_mu, "min_margin": r.support_min_margin,
+                            "delta": r.support_delta}}
 
     def profile_enable(self, classes):
         names = kernel_classes()

@@ -290,7 +290,9 @@ __global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM
       if (lane == 0) sh.red[warp][0] += acc;
     }
   }
-  for (int64_t item = blockIdx.x; item < ntiles * nch; item += gridDim.x) {
+  // probe columns (none in the mean-column launch, jlo = 0, jhi = 1: dinvp is then not read —
+  // it holds probe-precision values, Dp floats with fp32 probes)
+  for (int64_t item = blockIdx.x; ncol > 0 && item < ntiles * nch; item += gridDim.x) {
     const int64_t tile = item / nch;
     const int chunk = (int)(item % nch);
     const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
@@ -440,6 +442,39 @@ __global__ void k_check_alpha(int64_t D, const double* __restrict__ alpha, int* 
   }
 }
 
+// Support certificate (cofem_report.support_*): max|mu| (non-negative doubles order like their bit
+// patterns, so an unsigned atomicMax on the bits is exact), then the counts and the smallest
+// margin | |mu_d| / max - thr | (again as bit patterns, atomicMin).
+struct SupportStats { unsigned long long maxbits, minmargin_bits, count, adjacent; };
+__global__ void k_support_max(int64_t D, const double* __restrict__ mu, SupportStats* st) {
+  double m = 0.0;
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(mu[d]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&st->maxbits, (unsigned long long)__double_as_longlong(m));
+}
+__global__ void k_support_count(int64_t D, const double* __restrict__ mu, double thr, double delta, SupportStats* st) {
+  const double mx = __longlong_as_double((long long)st->maxbits);
+  unsigned long long cnt = 0, adj = 0;
+  double mm = INFINITY;
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    const double a = fabs(mu[d]);
+    cnt += a > thr * mx;
+    const double margin = mx > 0.0 ? fabs(a / mx - thr) : INFINITY;
+    adj += margin < delta;
+    mm = fmin(mm, margin);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    adj += __shfl_xor_sync(0xffffffffu, adj, o);
+    mm = fmin(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&st->count, cnt); atomicAdd(&st->adjacent, adj);
+    atomicMin(&st->minmargin_bits, (unsigned long long)__double_as_longlong(mm));
+  }
+}
+
 __global__ void k_add_vec(int64_t n, double* __restrict__ a, const double* __restrict__ b) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a[i] += b[i];
@@ -542,15 +577,16 @@ static cofem_status stage_in(Ctx* c, const double* src, double* dst_ws, const do
   return COFEM_OK;
 }
 
+// alpha > 0 and finite (cofem.h): one check kernel into the flag allocated at setup, read back
+// through pinned host memory (no allocation per call).  cofem_em checks only a caller-given
+// alpha_init; the alphas of its own M-steps are positive and finite by construction (floor, clamp).
 static cofem_status validate_alpha(Ctx* c, const double* alpha_dev) {
-  int* bad; CK(cudaMalloc(&bad, sizeof(int)));
-  CK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
-  k_check_alpha<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, alpha_dev, bad);
-  int hb = 0;
-  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemsetAsync(c->bad_flag, 0, sizeof(int), c->stream));
+  k_check_alpha<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, alpha_dev, c->bad_flag);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(c->bad_host, c->bad_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  cudaFree(bad);
-  if (hb) { c->err = "alpha must be positive and finite"; return COFEM_ERR_INVALID; }
+  if (*c->bad_host) { c->err = "alpha must be positive and finite"; return COFEM_ERR_INVALID; }
   return COFEM_OK;
 }
 
@@ -569,7 +605,10 @@ static void update_range(Ctx* c, int K, double invK, int jlo, int jhi, unsigned*
   // two probe columns per step where the update runs alone (conv, dense: C5 242 -> 229 ms per
   // E-step); on the concurrent-group DCT path the lighter one-column kernel (126 vs 80
   // registers) shares the SMs better (C4 52.5 vs 53.6 ms).  Grids: the resident CTAs, 4 / 2 per SM
-  static const int unr_env = getenv("COFEM_UPD_UNR") ? atoi(getenv("COFEM_UPD_UNR")) : 0;   // tuning hook
+#ifndef COFEM_UPD_UNR
+#define COFEM_UPD_UNR 0   // tuning build switch: force the one- (1) or two-column (2) update
+#endif
+  constexpr int unr_env = COFEM_UPD_UNR;
   const bool two = jlo >= 1 && jhi - jlo >= 2 && (unr_env ? unr_env == 2 : c->probe_groups <= 1);
   if (jlo == 0 && jhi == 1) k_update<TP, 1><<<c->vec_grid, VEC_THREADS, 0, st>>>(a);
   else if (!two) k_update<TP, 1><<<c->upd_grid, VEC_THREADS, 0, st>>>(a);
@@ -588,16 +627,14 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   // the conv path ping-pongs p between two buffers; every E-step starts from the same
   // assignment (k_init rewrites p), which keeps a captured graph's pointers valid
   void* const P_entry = c->P; double* const p0_entry = c->p0;
-  static const bool serial = getenv("COFEM_1K_SERIAL") != nullptr;   // tuning hook: mean column on the main stream
-  cudaStream_t ms = serial ? c->stream : c->side;
+  cudaStream_t ms = c->side;
   // fast DCT path: the probe columns run as G independent groups on G streams, so that one
   // group's issue-bound column pass overlaps another's bandwidth-bound passes (C4 fixed-alpha
   // E-step: G = 1 62.7 ms, G = 2 58.3 ms, 57.6 with each probe launch on ~80 % of the SMs;
   // G = 3 59.7, G = 4 61.6)
-  static const int groups_env = getenv("COFEM_PROBE_GROUPS") ? atoi(getenv("COFEM_PROBE_GROUPS")) : 2;
-  int G = c->fast1k ? std::max(1, std::min(Ctx::MAXG, groups_env)) : 1;
-  static const int gmin_env = getenv("COFEM_GROUP_MIN") ? atoi(getenv("COFEM_GROUP_MIN")) : -1;   // tuning hook
-  const int gmin = gmin_env > 0 ? gmin_env : 2;      // measured: groups of >= 2 columns help at every K
+  const int groups = c->opt.probe_groups > 0 ? c->opt.probe_groups : 2;
+  int G = c->fast1k ? std::max(1, std::min(Ctx::MAXG, groups)) : 1;
+  const int gmin = 2;      // measured: groups of >= 2 columns help at every K
   while (G > 1 && ((m - 1) / G < gmin || !c->gs[G - 1])) --G;
   c->probe_groups = G;
   int gj[Ctx::MAXG + 1];
@@ -611,7 +648,11 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
     CK(cudaEventRecord(c->ev_fork, c->stream));
     for (int g = 1; g < G; ++g) CK(cudaStreamWaitEvent(c->gstream[g], c->ev_fork, 0));
   }
-  static const bool no_mean = getenv("COFEM_EXP_NO_MEAN") != nullptr;   // timing experiment only (results invalid)
+#ifdef COFEM_EXP_NO_MEAN
+  constexpr bool no_mean = true;     // timing experiment build only (results invalid)
+#else
+  constexpr bool no_mean = false;
+#endif
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
     if (!no_mean && !c->skip_mean) {
@@ -720,8 +761,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   ProbeParams pv{(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), t, k_offset, (long long)(c->d_offset / 128)};
   k_set_probe_params<<<1, 1, 0, c->stream>>>((ProbeParams*)c->dparams, pv);
   CK(cudaGetLastError());
-  static const bool no_graph = getenv("COFEM_NO_GRAPH") != nullptr;   // test hook
-  if (no_graph || c->prof_mask) return estep_body(c, K, K_total);
+  if (!c->opt.use_graph || c->prof_mask) return estep_body(c, K, K_total);
   cudaStream_t user = c->stream;
   CK(cudaEventRecord(c->ev_in, user));
   CK(cudaStreamWaitEvent(c->work, c->ev_in, 0));
@@ -757,11 +797,76 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   return COFEM_OK;
 }
 
-// Read the column states back (the one end-of-E-step sync) and fill the report.
-static cofem_status estep_report(Ctx* c, int m) {
+// Probe-parallel mode (dist_mode 1): the owner split of the GLOBAL K over the ranks
+// (paper_2202_12808_b200/dist.py probe_split_owner mirrors it on the host): rank 0 solves the mean
+// system and K0 = max(1, min(K - (world - 1), floor((K + mc) / world - mc + 1/2))) probes, mc = the
+// mean system's cost in probe columns (it runs concurrently with the probes: 2 on the DCT / FFT
+// convolution paths, 0 on the dense tensor-core path where it rides in the same kernels);
+// ranks 1.. split the other K - K0 contiguously.
+static void split_owner(int K, int W, int r, double mc, int* k_off, int* K_loc, bool* owns) {
+  if (W == 1) { *k_off = 0; *K_loc = K; *owns = true; return; }
+  const int K0 = std::max(1, std::min(K - (W - 1), (int)floor((K + mc) / W - mc + 0.5)));
+  if (r == 0) { *k_off = 0; *K_loc = K0; *owns = true; return; }
+  const int rest = K - K0, base = rest / (W - 1), extra = rest % (W - 1), q = r - 1;
+  *K_loc = base + (q < extra ? 1 : 0);
+  *k_off = K0 + q * base + std::min(q, extra);
+  *owns = false;
+}
+static void pp_split(const Ctx* c, int K, int* k_off, int* K_loc, bool* owns) {
+  split_owner(K, c->world, c->rank, c->pp_mean_cost, k_off, K_loc, owns);
+}
+
+// One E-step of the probe-parallel mode: this rank's probes (global indices, R8) and, on rank 0,
+// the mean system; then s (this rank's partial (1/K) sum, Eq. 6) is summed over the ranks and
+// mu = x0 is broadcast from rank 0 -- one all-reduce + one broadcast of D fp64 per E-step, both
+// enqueued on the context stream.  Afterwards every rank holds the same x0 and s.
+static cofem_status estep_pp(Ctx* c, int K, uint64_t seed, int t, int* K_loc) {
+  int off, kl; bool owns;
+  pp_split(c, K, &off, &kl, &owns);
+  *K_loc = kl;
+  c->skip_mean = !owns;
+  cofem_status st = estep_device(c, kl, seed, t, off, K);
+  c->skip_mean = false;
+  if (st != COFEM_OK) return st;
+  if ((st = comm_allreduce(c, c->s, (size_t)c->D, 1)) != COFEM_OK) return st;
+  return comm_bcast(c, c->x0, (size_t)c->D, 1, 0);
+}
+
+static cofem_status check_K(Ctx* c, int K) {
+  if (!c->pp) {
+    if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes] (S:148)"; return COFEM_ERR_INVALID; }
+    return COFEM_OK;
+  }
+  if (K < c->world) { c->err = "probe-parallel: K must be >= world (every rank solves >= 1 probe)"; return COFEM_ERR_INVALID; }
+  int off, kl; bool owns;
+  pp_split(c, K, &off, &kl, &owns);
+  if (kl > c->Kcap) { c->err = "probe-parallel: this rank's share of K exceeds max_probes"; return COFEM_ERR_INVALID; }
+  return COFEM_OK;
+}
+
+static constexpr double SUPPORT_THR = 1e-3, SUPPORT_DELTA = 1e-6;   // reading R16; cofem_report
+
+// Read the column states back (the one end-of-E-step sync) and fill the report; with
+// `support`, also the support certificate of mu = x0 (two small kernels, read back with the states).
+static cofem_status estep_report(Ctx* c, int m, bool support = true) {
   c->cs_host.resize(m);
+  if (support) {
+    CK(cudaMemsetAsync(c->sup_stats, 0, sizeof(SupportStats), c->stream));
+    CK(cudaMemsetAsync((char*)c->sup_stats + 8, 0x7f, 8, c->stream));     // min margin: a huge double
+    k_support_max<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, c->x0, (SupportStats*)c->sup_stats);
+    k_support_count<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, c->x0, SUPPORT_THR, SUPPORT_DELTA,
+                                                            (SupportStats*)c->sup_stats);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->sup_host, c->sup_stats, sizeof(SupportStats), cudaMemcpyDeviceToHost, c->stream));
+  }
   CK(cudaMemcpyAsync(c->cs_host.data(), c->cs, m * sizeof(ColState), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (support) {
+    const SupportStats* h = (const SupportStats*)c->sup_host;
+    union { unsigned long long u; double d; } mx{h->maxbits}, mm{h->minmargin_bits};
+    c->sup_count = (int64_t)h->count; c->sup_adjacent = (int64_t)h->adjacent;
+    c->sup_max = mx.d; c->sup_min_margin = mm.d;
+  }
   c->last_cols = m;
   c->frozen_host.resize(m); c->rho_host.resize(m); c->rho0_host.resize(m);
   c->bad_col = -1; c->bad_iter = -1;
@@ -798,6 +903,7 @@ void cofem_default_options(cofem_options* o) {
   o->probe_precision = 0; o->max_probes = 32;
   o->rank = 0; o->world = 1; o->nccl_id = nullptr;
   o->cg_rtol = 0.0;
+  o->apply_path = 0; o->probe_groups = 0; o->use_graph = 1; o->dist_mode = 0;
 }
 
 const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
@@ -816,6 +922,7 @@ static void free_all(Ctx* c) {
   if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
   comm_destroy(c);
   dense_tc_free(c);
+  if (c->phi && !c->phi_owned) c->phi = nullptr;   // borrowed from the caller
   void* ptrs[] = {c->phi, c->mask_vvT, c->dct_tab32, c->dct_tab64, c->taps, c->g64, c->g32, c->b0, c->colsq,
                   c->alpha, c->dinv64, c->dinvp, c->x0, c->r0, c->p0, c->q0, c->R, c->P, c->Q, c->s,
                   c->mu_out, c->s_out, c->alpha_out, c->bits, c->cs, c->part, c->counters,
@@ -840,6 +947,10 @@ static void free_all(Ctx* c) {
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->dparams) cudaFree(c->dparams);
+  if (c->bad_flag) cudaFree(c->bad_flag);
+  if (c->bad_host) cudaFreeHost(c->bad_host);
+  if (c->sup_stats) cudaFree(c->sup_stats);
+  if (c->sup_host) cudaFreeHost(c->sup_host);
 }
 
 void cofem_destroy(cofem_ctx ctx) {
@@ -858,9 +969,18 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (!(opt->cg_rtol >= 0.0 && opt->cg_rtol < 1.0)) { c->err = "cg_rtol must be in [0, 1)"; return COFEM_ERR_INVALID; }
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
+  if (opt->apply_path < 0 || opt->apply_path > 1) { c->err = "apply_path must be 0 or 1"; return COFEM_ERR_INVALID; }
+  if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 4]"; return COFEM_ERR_INVALID; }
+  if (opt->dist_mode < 0 || opt->dist_mode > 1) { c->err = "dist_mode must be 0 or 1"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
   c->freeze_tau = std::max(FREEZE_TAU, opt->cg_rtol * opt->cg_rtol);
-  if (opt->nccl_id || op->D_global) {          // column-sharded dense / D-sharded conv mode (comm.cu)
+  if (opt->dist_mode == 1) {                    // probe-parallel (comm.cu: all-reduce of s, broadcast of mu)
+    if (!opt->nccl_id || opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) {
+      c->err = "probe-parallel: need nccl_id and 0 <= rank < world"; return COFEM_ERR_INVALID;
+    }
+    if (op->D_global || op->d_offset) { c->err = "probe-parallel: every rank holds the whole operator (D_global = 0)"; return COFEM_ERR_INVALID; }
+    c->pp = true; c->rank = opt->rank; c->world = opt->world;
+  } else if (opt->nccl_id || op->D_global) {    // column-sharded dense / D-sharded conv mode (comm.cu)
     if (op->kind == COFEM_OP_DCT2_MASKED) { c->err = "sharded mode: DENSE or CIRCCONV operators only"; return COFEM_ERR_UNSUPPORTED; }
     if (!opt->nccl_id || opt->world < 1 || opt->rank < 0 || opt->rank >= opt->world) {
       c->err = "sharded mode: need nccl_id and 0 <= rank < world"; return COFEM_ERR_INVALID;
@@ -889,6 +1009,10 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
   CK(cudaMalloc(&c->dparams, 64));
+  CK(cudaMalloc(&c->bad_flag, sizeof(int)));
+  CK(cudaMallocHost(&c->bad_host, sizeof(int)));
+  CK(cudaMalloc(&c->sup_stats, sizeof(SupportStats)));
+  CK(cudaMallocHost(&c->sup_host, sizeof(SupportStats)));
 
   const size_t tp = c->probe64 ? sizeof(double) : sizeof(float);
   const int64_t Dp = c->Dp;
@@ -908,7 +1032,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   {   // k_update: with fewer D tiles than 2 per SM, split the probe columns into chunks as well
     const int64_t ntiles = Dp / VEC_TILE;
     int ch = 1;
-    if (ntiles < 2 * c->num_sms && c->Kcap > 1 && !getenv("COFEM_UPD_NOCHUNK"))
+    if (ntiles < 2 * c->num_sms && c->Kcap > 1)
       ch = (int)std::min<int64_t>(c->Kcap, (2 * c->num_sms + ntiles - 1) / ntiles);
     c->upd_chunks = ch;
     c->upd_grid = (int)std::min<int64_t>(ntiles * ch, (int64_t)c->num_sms * 4);
@@ -916,9 +1040,11 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   }
   c->part_stride = std::max(std::max(c->vec_grid, c->upd_grid), 1);
 
-  if (c->sharded) {     // the communicator first: the D-sharded conv setup exchanges y halos
+  if (c->sharded || c->pp) {     // the communicator first: the D-sharded conv setup exchanges y halos
     cofem_status cst = comm_init(c, opt->rank, opt->world, opt->nccl_id);
     if (cst != COFEM_OK) return cst;
+  }
+  if (c->sharded) {
     if (c->kind == COFEM_OP_CIRCCONV) {
       const size_t tp = c->probe64 ? 8 : 4;
       char* p;
@@ -939,14 +1065,19 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (op->kind == COFEM_OP_DENSE) {
     if (op->ld < op->D || !op->phi) { c->err = "DENSE: phi NULL or ld < D"; st = COFEM_ERR_INVALID; }
     else {
-      c->ld = op->D;
-      cudaError_t e = cudaMalloc(&c->phi, (size_t)op->N * op->D * sizeof(float));
-      if (e != cudaSuccess) { c->err = "cudaMalloc phi"; st = COFEM_ERR_OOM; }
-      else {
-        e = cudaMemcpy2DAsync(c->phi, op->D * sizeof(float), op->phi, op->ld * sizeof(float),
-                              op->D * sizeof(float), op->N, cudaMemcpyDefault, c->stream);
-        st = e == cudaSuccess ? dense_setup(c, y_dev) : COFEM_ERR_CUDA;
-        if (e != cudaSuccess) c->err = cudaGetErrorString(e);
+      if (is_device_ptr(op->phi)) {     // borrowed: zero-copy, must outlive the context (cofem.h)
+        c->phi = const_cast<float*>(op->phi); c->ld = op->ld; c->phi_owned = false;
+        st = dense_setup(c, y_dev);
+      } else {                          // host Phi: the library's own device copy (row stride D)
+        c->ld = op->D; c->phi_owned = true;
+        cudaError_t e = cudaMalloc(&c->phi, (size_t)op->N * op->D * sizeof(float));
+        if (e != cudaSuccess) { c->err = "cudaMalloc phi"; st = COFEM_ERR_OOM; }
+        else {
+          e = cudaMemcpy2DAsync(c->phi, op->D * sizeof(float), op->phi, op->ld * sizeof(float),
+                                op->D * sizeof(float), op->N, cudaMemcpyDefault, c->stream);
+          st = e == cudaSuccess ? dense_setup(c, y_dev) : COFEM_ERR_CUDA;
+          if (e != cudaSuccess) c->err = cudaGetErrorString(e);
+        }
       }
     }
   } else if (op->kind == COFEM_OP_DCT2_MASKED) {
@@ -993,6 +1124,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (y_tmp) cudaFree(y_tmp);
   if (st != COFEM_OK) return st;
   ALLOC(c->part, (size_t)c->m_cap * c->part_stride);
+  c->pp_mean_cost = (c->fast1k || c->fast_conv) ? 2.0 : 0.0;
   if (c->sharded) {
     ALLOC(c->colsum, MAXM);
     if (c->kind == COFEM_OP_DENSE && !c->dense_tc) {
@@ -1027,15 +1159,22 @@ cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* 
 static cofem_status estep_impl(Ctx* c, const double* alpha, int32_t K, uint64_t seed, int32_t t,
                                int32_t k_offset, int32_t K_total, double* mu, double* s) {
   if (!alpha) { c->err = "alpha is NULL"; return COFEM_ERR_INVALID; }
-  if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes] (S:148)"; return COFEM_ERR_INVALID; }
+  cofem_status st;
+  if ((st = check_K(c, K))) return st;
   if (K_total < K || k_offset < 0) { c->err = "need K_total >= K and k_offset >= 0"; return COFEM_ERR_INVALID; }
+  if (c->pp && (k_offset != 0 || K_total != K || c->skip_mean)) {
+    c->err = "probe-parallel: pass the global K (k_offset 0, K_total K); cofem_estep_probes is not used";
+    return COFEM_ERR_INVALID;
+  }
   const double* a_dev;
-  cofem_status st = stage_in(c, alpha, c->alpha, &a_dev);
+  st = stage_in(c, alpha, c->alpha, &a_dev);
   if (st) return st;
   if (a_dev != c->alpha) CK(cudaMemcpyAsync(c->alpha, a_dev, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   if ((st = validate_alpha(c, c->alpha))) return st;
   CK(cudaEventRecord(c->ev0, c->stream));
-  if ((st = estep_device(c, K, seed, t, k_offset, K_total))) return st;
+  int m = K + 1;
+  if (c->pp) { int kl; if ((st = estep_pp(c, K, seed, t, &kl))) return st; m = kl + 1; }
+  else if ((st = estep_device(c, K, seed, t, k_offset, K_total))) return st;
   const bool mu_dev = mu && is_device_ptr(mu), s_dev = s && is_device_ptr(s);
   launch_begin(c, KC_FINAL);
   k_finalize<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, c->x0, c->s, mu_dev ? mu : c->mu_out,
@@ -1045,7 +1184,7 @@ static cofem_status estep_impl(Ctx* c, const double* alpha, int32_t K, uint64_t 
   CK(cudaEventRecord(c->ev1, c->stream));
   if (mu && !mu_dev) CK(cudaMemcpyAsync(mu, c->mu_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   if (s && !s_dev) CK(cudaMemcpyAsync(s, c->s_out, c->D * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  st = estep_report(c, K + 1);
+  st = estep_report(c, m);
   float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->estep_ms = ms;
   prof_collect(c);
   return st;
@@ -1062,6 +1201,7 @@ cofem_status cofem_estep_probes(cofem_ctx ctx, const double* alpha, int32_t K, u
                                 int32_t k_offset, int32_t K_total, double* s) {
   if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
   ctx->c.err.clear();
+  if (ctx->c.pp) { ctx->c.err = "cofem_estep_probes: not used in the probe-parallel mode (cofem_estep splits the probes)"; return COFEM_ERR_INVALID; }
   ctx->c.skip_mean = true;
   const cofem_status st = estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, nullptr, s);
   ctx->c.skip_mean = false;
@@ -1158,8 +1298,8 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
   Ctx* c = &ctx->c;
   c->err.clear();
   if (iters < 1) { c->err = "iters must be >= 1"; return COFEM_ERR_INVALID; }
-  if (K < 1 || K > c->Kcap) { c->err = "K must be in [1, max_probes] (S:148)"; return COFEM_ERR_INVALID; }
   cofem_status st;
+  if ((st = check_K(c, K))) return st;
   if (alpha_init) {
     const double* a_dev;
     if ((st = stage_in(c, alpha_init, c->alpha, &a_dev))) return st;
@@ -1175,7 +1315,9 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
   const bool s_dev = s_out && is_device_ptr(s_out);
   for (int i = 0; i < iters; ++i) {
     CK(cudaEventRecord(c->ev0, c->stream));
-    if ((st = estep_device(c, K, seed, t0 + i, 0, K))) return st;
+    int m = K + 1;
+    if (c->pp) { int kl; if ((st = estep_pp(c, K, seed, t0 + i, &kl))) return st; m = kl + 1; }
+    else if ((st = estep_device(c, K, seed, t0 + i, 0, K))) return st;
     const bool lastit = i == iters - 1;
     launch_begin(c, KC_FINAL);
     // the M-step writes the next alpha in place (the E-step state no longer needs it)
@@ -1185,7 +1327,7 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
     launch_end(c, KC_FINAL);
     if (check_launch(c, "k_finalize")) return COFEM_ERR_CUDA;
     CK(cudaEventRecord(c->ev1, c->stream));
-    st = estep_report(c, K + 1);
+    st = estep_report(c, m, lastit);
     float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->estep_ms = ms;
     if (st != COFEM_OK) return st;
   }
@@ -1204,6 +1346,21 @@ cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out) {
   out->frozen_at = c->frozen_host.data(); out->rho = c->rho_host.data(); out->rho0 = c->rho0_host.data();
   out->bad_col = c->bad_col; out->bad_iter = c->bad_iter;
   out->estep_ms_last = c->estep_ms; out->launches = c->launches;
+  out->support_count = c->sup_count; out->support_adjacent = c->sup_adjacent;
+  out->support_max_abs_mu = c->sup_max; out->support_min_margin = c->sup_min_margin;
+  out->support_delta = SUPPORT_DELTA;
+  return COFEM_OK;
+}
+
+cofem_status cofem_probe_split(int32_t K, int32_t world, int32_t rank, double mean_cost, int32_t* k_offset,
+                               int32_t* K_local, int32_t* owns_mean) {
+  if (world < 1 || rank < 0 || rank >= world || K < world || !k_offset || !K_local || !owns_mean || !(mean_cost >= 0)) {
+    g_err = "cofem_probe_split: need K >= world >= 1, 0 <= rank < world, mean_cost >= 0";
+    return COFEM_ERR_INVALID;
+  }
+  int off, kl; bool owns;
+  split_owner(K, world, rank, mean_cost, &off, &kl, &owns);
+  *k_offset = off; *K_local = kl; *owns_mean = owns ? 1 : 0;
   return COFEM_OK;
 }
 

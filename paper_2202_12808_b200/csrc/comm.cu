@@ -26,6 +26,7 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -49,9 +50,10 @@ static NcclApi& nccl(std::string& err) {
   api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
   api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
   api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
   api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
   api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString && api.Send &&
-           api.Recv && api.GroupStart && api.GroupEnd;
+           api.Recv && api.GroupStart && api.GroupEnd && api.Broadcast;
   if (!api.ok) err = "libnccl.so.2 lacks required symbols";
   return api;
 }
@@ -85,6 +87,15 @@ cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype) {
   ncclResult_t r = a.AllReduce(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, ncclSum, (ncclComm_t)c->comm,
                                c->stream);
   if (r != ncclSuccess) { c->err = std::string("ncclAllReduce: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
+  return COFEM_OK;
+}
+
+// In-place broadcast from `root` on the context stream (probe-parallel: mu = x0 from rank 0).
+cofem_status comm_bcast(Ctx* c, void* buf, size_t count, int dtype, int root) {
+  NcclApi& a = nccl(c->err);
+  if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
+  ncclResult_t r = a.Broadcast(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, root, (ncclComm_t)c->comm, c->stream);
+  if (r != ncclSuccess) { c->err = std::string("ncclBroadcast: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
   return COFEM_OK;
 }
 

@@ -94,26 +94,15 @@ __device__ __forceinline__ void canon(int lane, int r, int (&o)[4]) {
 }
 
 // Per-launch column info, read once per CTA: frozen flags and direction coefficients b_j
-// (R5; a6), plus per-warp gamma accumulators for pass C (reduced once per CTA at exit).
-struct ColFlags {          // passes without a reduction (1.5 KB of static shared memory)
+// (R5; a6); 1.5 KB of static shared memory.
+struct ColFlags {
   int frozen[MAXM];
   double b[MAXM];
-};
-struct ColInfo : ColFlags {
-  double g[8][MAXM];
 };
 __device__ __forceinline__ void load_colinfo(ColFlags& ci, const ColState* cs, int j0, int ncols) {
   for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
     const ColState c = cs[j0 + jj];
     ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
-  }
-}
-__device__ __forceinline__ void load_colinfo(ColInfo& ci, const ColState* cs, int j0, int ncols, bool zero_g) {
-  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
-    const ColState c = cs[j0 + jj];
-    ci.frozen[jj] = c.frozen; ci.b[jj] = c.b;
-    if (zero_g)
-      for (int w = 0; w < 8; ++w) ci.g[w][jj] = 0.0;
   }
 }
 

@@ -55,7 +55,8 @@ struct Ctx {
   int Kcap = 0, m_cap = 0;              // workspace capacity (columns = Kcap + 1)
 
   // operator data
-  float* phi = nullptr; int64_t ld = 0; // DENSE device copy, row-major N x ld
+  float* phi = nullptr; int64_t ld = 0; // DENSE Phi on the device, row-major N x ld
+  bool phi_owned = false;               // true: the library's copy of a host Phi; false: borrowed
   int rows = 0, cols = 0, conv = 0;     // DCT2
   uint8_t* mask_vvT = nullptr;          // DCT2: mask in v-order, transposed [cols][rows]
   uint32_t* maskL = nullptr;            // DCT2 1024 fast path: lane-packed mask (op_dct1k.cu)
@@ -72,6 +73,11 @@ struct Ctx {
   cudaStream_t work = nullptr;          // capturable stream the E-step graph runs on
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   void* dparams = nullptr;              // device ProbeParams of the current E-step
+  int* bad_flag = nullptr;              // validate_alpha: device flag
+  int* bad_host = nullptr;              //   and its pinned host mirror
+  void* sup_stats = nullptr; void* sup_host = nullptr;   // support certificate (device / pinned host)
+  int64_t sup_count = 0, sup_adjacent = 0;
+  double sup_max = 0, sup_min_margin = 0;
   cudaGraphExec_t graph_exec = nullptr; // captured E-step (cofem.cu estep_device)
   int graph_K = -1, graph_Kt = -1, graph_skip = -1;
   bool skip_mean = false;          // cofem_estep_probes: column 0 frozen from the start (mean owned elsewhere)
@@ -114,6 +120,8 @@ struct Ctx {
   void* dense_tc = nullptr;             // tensor-core dense path state (op_dense_tc.cu), NULL: SIMT
   // column-sharded dense mode (comm.cu): per-column sums go through colsum + an NCCL all-reduce
   bool sharded = false;
+  bool pp = false;                      // probe-parallel mode (dist_mode 1): probes split over ranks
+  double pp_mean_cost = 0;              // the mean system's cost in probe columns (owner split)
   int64_t d_offset = 0, D_global = 0;
   void* comm = nullptr;                 // ncclComm_t
   double* colsum = nullptr;             // [MAXM] per-column totals of this rank
@@ -268,6 +276,7 @@ cofem_status conv_halo_exchange(Ctx* c, int K);
 cofem_status comm_init(Ctx* c, int rank, int world, const uint8_t* id);
 void comm_destroy(Ctx* c);
 cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype);
+cofem_status comm_bcast(Ctx* c, void* buf, size_t count, int dtype, int root);
 cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, void* recv_left, void* recv_right,
                        size_t count, int dtype);
 // after a per-column reduction written to c->colsum: sum over ranks, then apply it (mode:

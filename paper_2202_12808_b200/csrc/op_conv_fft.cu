@@ -310,7 +310,7 @@ cofem_status conv_halo_exchange(Ctx* c, int K) {
   return comm_halo(c, c->halo_send0, c->halo_send0 + 192, c->halo_recv0, c->halo_recv0 + 192, 192, 1);
 }
 
-bool conv_fft_eligible(const Ctx* c) { return c->D >= 2048 && c->ntaps <= 64 && !getenv("COFEM_CONV_DIRECT"); }
+bool conv_fft_eligible(const Ctx* c) { return c->D >= 2048 && c->ntaps <= 64 && c->opt.apply_path != 1; }
 
 cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g) {
   using namespace cfft;

@@ -438,7 +438,7 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   const int gridA = (rows + rpc - 1) / rpc;
   c->part_stride = std::max(c->part_stride, gridA);
   cofem_status st = c->probe64 ? set_attrs<double>(c) : set_attrs<float>(c);
-  if (st == COFEM_OK && dct1k_eligible(c) && !getenv("COFEM_DCT_GENERIC")) {   // env: test hook for the generic path
+  if (st == COFEM_OK && dct1k_eligible(c) && c->opt.apply_path != 1) {   // apply_path 1: the generic passes
     st = dct1k_setup(c);
     c->fast1k = st == COFEM_OK;
     for (int g = 1; c->fast1k && g < Ctx::MAXG; ++g)      // probe groups' s accumulators (cofem.cu)

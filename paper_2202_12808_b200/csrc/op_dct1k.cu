@@ -280,8 +280,8 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, i
   constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
-  __shared__ ColInfo ci;
-  load_colinfo(ci, a.cs, j0, ncols, false);
+  __shared__ ColFlags ci;
+  load_colinfo(ci, a.cs, j0, ncols);
   if (!any_active(ci, ncols)) return;
   if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT])     // the first item's line, before the tables
     pf_line(col_of<T>(a, j0 + blockIdx.x / NT).t1 + (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L);
@@ -353,8 +353,8 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
-  __shared__ ColInfo ci;
-  load_colinfo(ci, a.cs, j0, ncols, true);
+  __shared__ ColFlags ci;
+  load_colinfo(ci, a.cs, j0, ncols);
   if (!any_active(ci, ncols)) return;
   if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT]) {   // the first item's rows, before the tables
     const DctCol<T> cn = col_of<T>(a, j0 + blockIdx.x / NT);
@@ -379,17 +379,12 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
       }
     }
     const double gw = rows_fwd_item<T>(a, j0 + jj, w % NT, sm, tb);   // warp-reduced, valid in lane 0
-    if ((threadIdx.x & 31) == 0) ci.g[warp][jj] += gw;
+    // a4 partial of image row (tile RT + warp): part[j][row].  One slot per row, whatever the grid,
+    // so gamma (and mu, s) do not depend on the launch size, K, max_probes or the probe groups
+    if ((threadIdx.x & 31) == 0) a.part[(int64_t)(j0 + jj) * a.stride + (w % NT) * RT + warp] = gw;
   }
-  // a4: gamma_j = p_j^T q_j.  CTA partials (fixed warp order) -> part[j][cta]; the last CTA
-  // reduces all columns in fixed order and applies the freeze rule / step length (R5).
-  __syncthreads();
-  for (int jj = threadIdx.x; jj < ncols; jj += blockDim.x) {
-    double v = 0.0;
-#pragma unroll
-    for (int ww = 0; ww < RT; ++ww) v += ci.g[ww][jj];
-    a.part[(int64_t)(j0 + jj) * a.stride + blockIdx.x] = v;
-  }
+  // a4: gamma_j = p_j^T q_j.  The last CTA reduces the L row partials of every column in fixed
+  // order and applies the freeze rule / step length (R5).
   __threadfence();
   __syncthreads();
   __shared__ bool last;
@@ -399,7 +394,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   __threadfence();
   for (int jj = warp; jj < ncols; jj += RT) {
     const int j = j0 + jj;
-    const double tot = reduce_partials(a.part + (int64_t)j * a.stride, gridDim.x);
+    const double tot = reduce_partials(a.part + (int64_t)j * a.stride, L);
     if ((threadIdx.x & 31) == 0 && !ci.frozen[jj]) {
       ColState cc = a.cs[j]; finish_gamma(cc, tot, a.iter); a.cs[j] = cc;
     }
@@ -570,7 +565,7 @@ cofem_status dct1k_setup(Ctx* c) {
   launch_end(c, KC_SETUP);
   set_attrs<float>();
   set_attrs<double>();
-  c->part_stride = std::max(c->part_stride, std::max(L / Geo<double>::RT, c->num_sms * 8));   // >= persistent grids
+  c->part_stride = std::max(c->part_stride, std::max(L, c->num_sms * 8));   // >= L row partials (pass C), grids
   return check_launch(c, "dct1k setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
@@ -586,12 +581,18 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const int ncols = j1 - j0;
   const size_t sm = smem_bytes<T>();
   // persistent grids at full occupancy (measured best: tools/sweep_slots.sh)
-  static const int slots_env = getenv("COFEM_1K_SLOTS") ? atoi(getenv("COFEM_1K_SLOTS")) : -1;   // tuning hook
+#ifndef COFEM_1K_SLOTS
+#define COFEM_1K_SLOTS -1   // tuning build switch: CTAs per SM of the persistent grids (-1 = occupancy, 0 = one per item)
+#endif
+  constexpr int slots_env = COFEM_1K_SLOTS;
   // the concurrent fp64 mean column is confined to a fraction of the SMs (COFEM_1K_MEAN_SMS),
   // shrinking as the probe work grows (tools/time_estep.py, C4 at a fixed alpha, with the
   // concurrent probe groups): an eighth at >= 32 probes (57.3 vs 57.5 ms for a quarter), a
   // quarter at >= 16 (33.1 vs 33.3 for an eighth), half below (21.1 vs 24.0 at 8 probes)
-  static const int mean_sms_env = getenv("COFEM_1K_MEAN_SMS") ? atoi(getenv("COFEM_1K_MEAN_SMS")) : -1;
+#ifndef COFEM_1K_MEAN_SMS
+#define COFEM_1K_MEAN_SMS -1   // tuning build switch: SMs of the mean column (-1 = the rule above)
+#endif
+  constexpr int mean_sms_env = COFEM_1K_MEAN_SMS;
   auto grid_of = [&](const void* fn, size_t smb) {
     const int items = ncols * Work<T>::NTILE;
     if (slots_env == 0) return items;                  // one CTA per work item
@@ -606,7 +607,10 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
     }
     // with concurrent probe groups each probe launch takes ~80 % of the SMs (C4: 120 of 148 best,
     // 16.70 vs 16.51 EM it/s uncapped; tools/time_estep.py sweep 74..148)
-    static const int group_sms_env = getenv("COFEM_1K_GROUP_SMS") ? atoi(getenv("COFEM_1K_GROUP_SMS")) : -1;
+#ifndef COFEM_1K_GROUP_SMS
+#define COFEM_1K_GROUP_SMS -1   // tuning build switch: SMs of each probe-group launch (-1 = 120/148)
+#endif
+    constexpr int group_sms_env = COFEM_1K_GROUP_SMS;
     const int gsms = group_sms_env >= 0 ? group_sms_env : (c->probe_groups > 1 ? (c->num_sms * 120) / 148 : 0);
     if (j0 > 0 && gsms > 0) g = std::min(g, gsms * per_sm);
     return g;

@@ -751,15 +751,20 @@ void dense_tc_free(Ctx* c) {
 // the shape cannot use it.
 cofem_status dense_tc_setup(Ctx* c) {
   using namespace tc;
-  if (c->probe64 || getenv("COFEM_DENSE_SIMT")) return COFEM_OK;    // env: test hook for the SIMT path
-  if (c->D % 4 != 0 || c->Kcap > 128) return COFEM_OK;              // TMA needs 16-B row pitches; N <= 128 per MMA
+  if (c->probe64 || c->opt.apply_path == 1) return COFEM_OK;        // parity mode / general kernels: FP32 SIMT
+  if (c->D % 4 != 0 || c->ld % 4 != 0 || ((uintptr_t)c->phi & 15) || c->Kcap > 128)
+    return COFEM_OK;                                                // TMA: 16-B base and row pitch; N <= 128 per MMA
   if (!encoder()) return COFEM_OK;
   DenseTC* t = new DenseTC();
   memset(t, 0, sizeof *t);
   c->dense_tc = t;
   t->bn = std::max(16, (c->Kcap + 15) / 16 * 16);
   t->mt = 1;                                      // one 128-row M-tile per CTA (pair protocol)
-  t->mode = t->bn > 64 ? 2 : getenv("COFEM_TC_FUSE") ? 0 : 1;   // env: timing comparison hook
+#ifdef COFEM_TC_FUSE
+  t->mode = t->bn > 64 ? 2 : 0;                   // timing comparison build (tools/build_variant.sh)
+#else
+  t->mode = t->bn > 64 ? 2 : 1;
+#endif
   t->pl = plan_for(t->bn, t->mt, t->mode);
   if (smem_of(t->pl) > 227 * 1024) { c->err = "dense tc: shared-memory plan too large"; return COFEM_ERR_INVALID; }
   t->Npad = (int)((c->N + 31) / 32 * 32);
@@ -841,7 +846,8 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
   if (c->sharded) { cofem_status st = sharded_finish(c, m, 1, iter); if (st != COFEM_OK) return st; }
-  if (getenv("COFEM_TC_DEBUG")) {     // synchronous protocol check (debug hook)
+#ifdef COFEM_TC_DEBUG
+  {                                   // synchronous protocol check (debug build)
     cudaStreamSynchronize(c->stream);
     unsigned long long h[4];
     cudaMemcpyFromSymbol(h, g_tc_stuck, sizeof h);
@@ -851,6 +857,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
       c->err = "tensor-core pipeline stall"; return COFEM_ERR_CUDA;
     }
   }
+#endif
   return COFEM_OK;
 }
 

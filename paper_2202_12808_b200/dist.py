@@ -7,8 +7,12 @@ given) only rank 0 solves the mean system, with fewer probes, and broadcasts mu;
 exchange is one sum-allreduce of the partial s = (1/K) sum_{k in rank} p_k o x_k per
 E-step (Eq. 6) (+ the mu broadcast), after which every rank applies the M-step (Eq. 8).
 The collective is injected (torch.distributed NCCL on GPUs, gloo in the CPU
-tests); this module holds only the host-side orchestration.
+tests); this module holds only the host-side orchestration.  The product's multi-GPU
+probe-parallel mode lives in the library itself (cofem_options.dist_mode = 1: NCCL all-reduce of s
+and broadcast of mu inside cofem_estep / cofem_em); this module is its host-side model, exercised
+over gloo in tests/test_dist_gloo.py.
 """
+import math
 
 
 def column_shard(D, world, rank, align=128):
@@ -44,7 +48,8 @@ def probe_split_owner(K, world, rank, mean_cost):
     """Probe split when rank 0 OWNS the mean system (the other ranks skip it, cofem_estep_probes,
     and receive mu by broadcast).  mean_cost = the mean system's effective cost in probe columns
     (it runs concurrently with the probes: bench.py mean_cost).  Rank 0 gets
-    K0 = max(1, round((K + mean_cost) / world - mean_cost)) probes, the other ranks split the
+    K0 = max(1, floor((K + mean_cost) / world - mean_cost + 1/2)) probes (the library's own split in the
+    probe-parallel mode, cofem.cu pp_split, is the same rule), the other ranks split the
     remaining K - K0 contiguously (>= 1 each).  Returns (k_offset, K_local, owns_mean)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
@@ -52,7 +57,7 @@ def probe_split_owner(K, world, rank, mean_cost):
         return 0, K, True
     if K < world:
         raise ValueError("probe-parallel needs K >= world (every rank solves >= 1 probe)")
-    K0 = max(1, min(K - (world - 1), int(round((K + mean_cost) / world - mean_cost))))
+    K0 = max(1, min(K - (world - 1), int(math.floor((K + mean_cost) / world - mean_cost + 0.5))))
     if rank == 0:
         return 0, K0, True
     off, n = probe_split(K - K0, world - 1, rank - 1)

@@ -57,3 +57,10 @@ def test_all_frozen_at_zero_executes_one_apply_and_no_update():
     assert tot_u == 0 and frac_u == 0.0
     tot_a, frac_a = bench.active_bytes("conv_apply", w, K, w.D, 1, frozen)
     assert abs(frac_a - 1 / 50.0) < 1e-12 and tot_a > 0
+
+
+def test_executed_applies_counts_frozen_columns():
+    """rhs_applies_per_s counts executed column-iterations: a column frozen at CG iteration F is
+    applied in iterations 0..F (the apply of F finds it frozen), one never frozen in all U."""
+    assert bench.executed_applies([[-1, 3, 0]], 10) == 10 + 4 + 1
+    assert bench.executed_applies([[-1, -1], [9, 12]], 10) == 20 + 10 + 10

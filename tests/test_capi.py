@@ -56,3 +56,36 @@ def test_no_oracle_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower().replace("oracle/", ""), f
+
+
+def test_default_options_new_fields(L):
+    from paper_2202_12808_b200 import cofem
+    o = cofem._Options()
+    L.cofem_default_options(o)
+    assert (o.apply_path, o.probe_groups, o.use_graph, o.dist_mode) == (0, 0, 1, 0)
+    assert o.world == 1 and o.rank == 0 and not o.nccl_id
+
+
+@pytest.mark.parametrize("mean_cost", [0.0, 1.0, 2.0, 3.5])
+def test_probe_split_matches_host_model(L, mean_cost):
+    """The library's probe-parallel split (cofem_probe_split, used by dist_mode 1) equals the host
+    model dist.probe_split_owner, covers [0, K) exactly once and gives every rank >= 1 probe."""
+    from paper_2202_12808_b200 import probe_split
+    from paper_2202_12808_b200.dist import probe_split_owner
+    for world in range(1, 9):
+        for K in range(world, 70):
+            seen = []
+            for r in range(world):
+                got = probe_split(K, world, r, mean_cost)
+                assert got == probe_split_owner(K, world, r, mean_cost), (K, world, r)
+                off, n, owns = got
+                assert n >= 1 and owns == (r == 0)
+                seen.extend(range(off, off + n))
+            assert seen == list(range(K))
+
+
+def test_probe_split_rejects_bad_arguments(L):
+    from paper_2202_12808_b200 import CofemError, probe_split
+    for args in [(3, 4, 0, 0.0), (8, 2, 2, 0.0), (8, 0, 0, 0.0), (8, 2, -1, 0.0)]:
+        with pytest.raises(CofemError):
+            probe_split(*args)

@@ -40,21 +40,11 @@ def col_err(a, b):
     return np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)
 
 
-def run_apply(w, K, blocks, env=None, alpha_seed=3):
-    """GPU apply of [x0 | X] (fp64 mean column + K fp32 probe columns) and the fp64 oracle."""
+def run_apply(w, K, blocks, apply_path=0, alpha_seed=3):
+    """GPU apply of [x0 | X] (fp64 mean column + K fp32 probe columns) and the fp64 oracle.
+    apply_path 1 selects the general kernels (cofem_options.apply_path)."""
     from paper_2202_12808_b200 import Context
-    old = {}
-    for k, v in (env or {}).items():
-        old[k] = os.environ.get(k)
-        os.environ[k] = v
-    try:
-        ctx = Context.from_workload(w, max_probes=K, cg_iters=1)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k)
-            else:
-                os.environ[k] = v
+    ctx = Context.from_workload(w, max_probes=K, cg_iters=1, apply_path=apply_path)
     rng = np.random.default_rng(alpha_seed)
     alpha = np.exp(rng.uniform(-3.0, 6.0, w.D))           # EM-like spread of precisions
     x0 = rng.standard_normal(w.D)
@@ -87,8 +77,7 @@ DENSE = [synth.preset("C2"), synth.dense(250, 1000, 20, K=8, U=1, T=1, seed=1, n
 @pytest.mark.parametrize("blocks", [rademacher, gaussian], ids=["rademacher", "gaussian"])
 @pytest.mark.parametrize("path", ["tcgen05_3xtf32", "fp32_simt"])
 def test_dense_apply(w, blocks, path):
-    env = {"COFEM_DENSE_SIMT": "1"} if path == "fp32_simt" else {}
-    e, eg = run_apply(w, 16, blocks, env)
+    e, eg = run_apply(w, 16, blocks, 1 if path == "fp32_simt" else 0)
     assert e[0] <= 1e-12, e[0]
     assert e[1:].max() <= 2e-6, e[1:].max()
     assert eg.max() <= 2e-6, eg.max()
@@ -101,24 +90,24 @@ def test_dense_apply_c3_shape_tensor_cores():
     assert e[0] <= 1e-12 and e[1:].max() <= 2e-6, (e[0], e[1:].max())
 
 
-@pytest.mark.parametrize("w,env", [
-    (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), {}),                       # fast path
-    (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), {"COFEM_DCT_GENERIC": "1"}),
-    (synth.dct(64, 128, 2048, 40, K=8, U=1, T=1, seed=5), {}),                             # generic, rows != cols
+@pytest.mark.parametrize("w,path", [
+    (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), 0),                       # fast path
+    (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), 1),
+    (synth.dct(64, 128, 2048, 40, K=8, U=1, T=1, seed=5), 0),                             # generic, rows != cols
 ], ids=["dct1024_fast", "dct1024_generic", "dct64x128"])
-def test_dct_apply(w, env):
-    e, eg = run_apply(w, 8, gaussian, env)
+def test_dct_apply(w, path):
+    e, eg = run_apply(w, 8, gaussian, path)
     assert e[0] <= 1e-12 and e[1:].max() <= 2e-6, (e[0], e[1:].max())
     assert eg.max() <= 2e-6
 
 
-@pytest.mark.parametrize("w,env", [
-    (synth.circconv(65536, 64, 60, K=8, U=1, T=1, seed=6), {}),                            # FFT, D multiple of 896? no
-    (synth.circconv(5003, 64, 5, K=8, U=1, T=1, seed=7), {}),                              # FFT, prime D: wrapped windows
-    (synth.circconv(5003, 64, 5, K=8, U=1, T=1, seed=7), {"COFEM_CONV_DIRECT": "1"}),       # direct stencil
-    (synth.circconv(1500, 17, 5, K=8, U=1, T=1, seed=8), {}),                              # D < 2048: direct
+@pytest.mark.parametrize("w,path", [
+    (synth.circconv(65536, 64, 60, K=8, U=1, T=1, seed=6), 0),                            # FFT, D multiple of 896? no
+    (synth.circconv(5003, 64, 5, K=8, U=1, T=1, seed=7), 0),                              # FFT, prime D: wrapped windows
+    (synth.circconv(5003, 64, 5, K=8, U=1, T=1, seed=7), 1),       # direct stencil
+    (synth.circconv(1500, 17, 5, K=8, U=1, T=1, seed=8), 0),                              # D < 2048: direct
 ], ids=["fft_65536", "fft_5003", "direct_5003", "direct_1500_T17"])
-def test_conv_apply(w, env):
-    e, eg = run_apply(w, 8, gaussian, env)
+def test_conv_apply(w, path):
+    e, eg = run_apply(w, 8, gaussian, path)
     assert e[0] <= 1e-12 and e[1:].max() <= 2e-6, (e[0], e[1:].max())
     assert eg.max() <= 2e-6

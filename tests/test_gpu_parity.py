@@ -417,3 +417,69 @@ def test_c4_full_size_bitwise_deterministic():
     r2 = gpu_em(ctx_of(w), w, 2, w.K, 4)
     for x, y in zip(r1, r2):
         assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------------ round 2: library modes and boundary
+def test_probe_parallel_library_mode_world1():
+    """dist_mode 1 (probe-parallel inside the library: owner split, NCCL all-reduce of s and
+    broadcast of mu) on a 1-rank communicator: the collectives are identities, so cofem_em must be
+    bitwise equal to the single-GPU run, on the generic DCT path and the 1024^2 fast path."""
+    from paper_2202_12808_b200 import get_unique_id
+    for w in [SMALL[2], synth.dct(1024, 1024, 262144, 400, K=4, U=8, T=1, seed=1)]:
+        ref = gpu_em(ctx_of(w, cg_iters=w.U), w, 2, w.K, 3)
+        pp = ctx_of(w, cg_iters=w.U, rank=0, world=1, nccl_id=get_unique_id(), dist_mode=1)
+        got = gpu_em(pp, w, 2, w.K, 3)
+        for x, y in zip(got, ref):
+            assert np.array_equal(x, y)
+        mu, s = gpu_estep(pp, w, np.ones(w.D), w.K, 3, 0)
+        mu_r, s_r = gpu_estep(ctx_of(w, cg_iters=w.U), w, np.ones(w.D), w.K, 3, 0)
+        assert np.array_equal(mu, mu_r) and np.array_equal(s, s_r)
+
+
+def test_mu_independent_of_max_probes_and_groups():
+    """mu (the fp64 mean column) does not depend on max_probes, K or the probe groups: its gamma is
+    reduced from one partial per image row in fixed order, whatever the launch size."""
+    w = synth.dct(1024, 1024, 262144, 400, K=4, U=12, T=1, seed=2)
+    outs = []
+    for mp, groups, K in [(4, 0, 4), (32, 0, 4), (32, 1, 4), (32, 2, 20)]:
+        ctx = ctx_of(w, cg_iters=w.U, max_probes=mp, probe_groups=groups)
+        outs.append(gpu_estep(ctx, w, np.ones(w.D), K, 1, 0)[0])
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
+def test_support_certificate_in_report():
+    """cofem_report.support_*: count of |mu_d| > 1e-3 max|mu|, coordinates within 1e-6 of the
+    threshold and the smallest margin, against NumPy on the returned mu."""
+    w = SMALL[2]
+    ctx = ctx_of(w)
+    mu, _ = gpu_estep(ctx, w, np.ones(w.D), w.K, 5, 0)
+    sup = ctx.report()["support"]
+    mx = np.max(np.abs(mu))
+    margin = np.abs(np.abs(mu) / mx - 1e-3)
+    assert sup["max_abs_mu"] == mx
+    assert sup["count"] == int(np.sum(np.abs(mu) > 1e-3 * mx))
+    assert sup["adjacent"] == int(np.sum(margin < 1e-6))
+    assert sup["min_margin"] == pytest.approx(float(margin.min()), rel=1e-12, abs=1e-300)
+    a, mu2, _ = gpu_em(ctx, w, 2, w.K, 5)
+    assert ctx.report()["support"]["count"] == int(np.sum(np.abs(mu2) > 1e-3 * np.max(np.abs(mu2))))
+
+
+def test_dense_device_phi_is_borrowed():
+    """A device Phi is borrowed (zero-copy) with its row stride ld: the same E-step, bit for bit, as
+    the library's own copy of the host Phi, on the tensor-core path (ld % 4 == 0) and the SIMT path
+    (ld odd)."""
+    from paper_2202_12808_b200 import OP_DENSE, Context
+    w = synth.dense(250, 1000, 20, K=8, U=40, T=1, seed=3)
+    ref = gpu_estep(ctx_of(w, cg_iters=40), w, np.ones(w.D), 8, 2, 0)
+    for pad in (0, 4, 3):
+        ld = w.D + pad
+        buf = torch.full((w.N, ld), float("nan"), dtype=torch.float32, device="cuda")
+        buf[:, :w.D] = torch.as_tensor(w.phi, device="cuda")
+        ctx = Context(OP_DENSE, w.N, w.D, w.y, w.beta, phi=buf, ld=ld, cg_iters=40, max_probes=8)
+        got = gpu_estep(ctx, w, np.ones(w.D), 8, 2, 0)
+        if pad % 4 == 0:
+            assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])
+        else:   # SIMT path: same fp32-class accuracy, different kernels
+            assert rel(got[0], ref[0]) <= 1e-6 and rel(got[1], ref[1]) <= 1e-4
+        buf[:, w.D:] = 0.0   # the padding is never read (NaN there would have propagated)

@@ -8,10 +8,8 @@ from oracle.operators import DenseOp, gram_apply
 from paper_2202_12808_b200 import Context
 
 def err(N, D, simt, K=8):
-    if simt: os.environ["COFEM_DENSE_SIMT"] = "1"
-    else: os.environ.pop("COFEM_DENSE_SIMT", None)
     w = synth.dense(N, D, 5, K=K, U=1, T=1, seed=1)
-    ctx = Context.from_workload(w, max_probes=K, cg_iters=1)
+    ctx = Context.from_workload(w, max_probes=K, cg_iters=1, apply_path=1 if simt else 0)
     rng = np.random.default_rng(0)
     alpha = np.ones(D) * 1e-3
     x0 = rng.standard_normal(D)
