@@ -69,7 +69,7 @@ typedef struct {
   /* DCT2_MASKED */
   int32_t rows, cols;        /* grid, rows * cols == D, each a power of two in [16, 1024] */
   const int64_t* obs_idx;    /* N pixel indices (r * cols + c), sorted, distinct, in [0, D); host or device */
-  int32_t convention;        /* 0: Phi = S C2^T (paper, default); 1: Phi = S C2 */
+  int32_t convention;        /* 0: Phi = S C2^T (paper, default; 1024 x 1024 fast path); 1: Phi = S C2 (BASELINE config 4 literally; generic passes) */
   /* CIRCCONV */
   const float* taps;         /* ntaps fp32 filter taps h_j; host or device */
   int32_t ntaps;             /* 1 <= ntaps <= 64, ntaps <= D */

@@ -24,7 +24,7 @@ namespace cofem {
 static const char* kClassNames[KC_COUNT] = {
     "probe_bits", "pcg_init", "pcg_direction", "pcg_update", "finalize_mstep",
     "dense_phi_p", "dense_phiT_w", "dct_rows_inv", "dct_cols", "dct_rows_fwd",
-    "conv_apply", "mean_column", "setup"};
+    "conv_apply", "mean_column", "setup", "dct_flow"};
 
 // ------------------------------------------------------------------ bookkeeping
 static cudaEvent_t pool_get(Ctx* c) {
@@ -633,7 +633,7 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   // E-step: G = 1 62.7 ms, G = 2 58.3 ms, 57.6 with each probe launch on ~80 % of the SMs;
   // G = 3 59.7, G = 4 61.6)
   const int groups = c->opt.probe_groups > 0 ? c->opt.probe_groups : 2;
-  int G = c->fast1k ? std::max(1, std::min(Ctx::MAXG, groups)) : 1;
+  int G = c->fast1k ? std::max(1, std::min(4, groups)) : 1;
   const int gmin = 2;      // measured: groups of >= 2 columns help at every K
   while (G > 1 && ((m - 1) / G < gmin || !c->gs[G - 1])) --G;
   c->probe_groups = G;
@@ -683,6 +683,34 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
   return COFEM_OK;
 }
 
+// 1024 x 1024 DCT path, fp32 probes: the probe columns' whole CG loop is one dataflow launch
+// (op_dct1k.cu k1k_flow); the fp64 mean column runs its per-pass kernels on the side stream
+// concurrently, and the group s accumulators are summed in group order at the end.
+[[maybe_unused]] static cofem_status cg_loop_flow(Ctx* c, int K, int K_total, double invK) {
+  const int G = dct1k_flow_groups(c, K);
+  for (int g = 1; g < G; ++g)
+    if (!c->gs[g]) { c->err = "flow: group accumulators missing"; return COFEM_ERR_CUDA; }
+  CK(cudaEventRecord(c->ev_fork, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  if (!c->skip_mean) {
+    for (int it = 0; it < c->opt.cg_iters; ++it) {
+      cofem_status st = dct1k_apply(c, 0, 1, it, it > 0, c->side);
+      if (st != COFEM_OK) return st;
+      update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->side, KC_MEAN);
+    }
+  }
+  for (int g = 1; g < G; ++g) CK(cudaMemsetAsync(c->gs[g], 0, c->Dp * sizeof(double), c->stream));
+  cofem_status st = dct1k_flow(c, K, K_total, c->stream);
+  if (st != COFEM_OK) return st;
+  CK(cudaEventRecord(c->ev_join, c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  for (int g = 1; g < G; ++g) {   // s = s_0 + s_1 + ... in group order (deterministic)
+    k_add_vec<<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(c->Dp, c->s, c->gs[g]);
+    if (check_launch(c, "k_add_vec")) return COFEM_ERR_CUDA;
+  }
+  return COFEM_OK;
+}
+
 // Runs Alg. 1 lines 3-7 with alpha already in c->alpha.  No host sync inside.
 static cofem_status cg_loop_conv_sharded(Ctx* c, int K, double invK);
 
@@ -707,6 +735,9 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   if (check_launch(c, "k_init")) return COFEM_ERR_CUDA;
   if (c->sharded) { cofem_status st = sharded_finish(c, m, 0, 0); if (st != COFEM_OK) return st; }
   if (c->skip_mean) k_freeze_col0<<<1, 32, 0, c->stream>>>(c->cs);   // every kernel skips a frozen column
+#ifdef COFEM_1K_FLOW   // experiment build: the dataflow probe kernel (measured slower)
+  if (c->fast1k && !c->probe64) return cg_loop_flow(c, K, K_total, invK);
+#endif
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
   if (c->fast_conv && c->sharded) return cg_loop_conv_sharded(c, K, invK);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
@@ -929,8 +960,9 @@ static void free_all(Ctx* c) {
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
                   c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt,
-                  c->gs[1], c->gs[2], c->gs[3]};
+                  c->flow_state, c->flow_part2};
   for (void* p : ptrs) if (p) cudaFree(p);
+  for (int g = 1; g < Ctx::MAXG; ++g) if (c->gs[g]) cudaFree(c->gs[g]);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -970,7 +1002,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
   if (opt->apply_path < 0 || opt->apply_path > 1) { c->err = "apply_path must be 0 or 1"; return COFEM_ERR_INVALID; }
-  if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 4]"; return COFEM_ERR_INVALID; }
+  if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 8]"; return COFEM_ERR_INVALID; }
   if (opt->dist_mode < 0 || opt->dist_mode > 1) { c->err = "dist_mode must be 0 or 1"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
   c->freeze_tau = std::max(FREEZE_TAU, opt->cg_rtol * opt->cg_rtol);

@@ -22,7 +22,7 @@ enum KernelClass : int {
   KC_PROBES = 0, KC_INIT, KC_DIR, KC_UPDATE, KC_FINAL,
   KC_DENSE_PHI_P, KC_DENSE_PHIT_W,
   KC_DCT_ROWS_INV, KC_DCT_COLS, KC_DCT_ROWS_FWD,
-  KC_CONV_APPLY, KC_MEAN, KC_SETUP, KC_COUNT
+  KC_CONV_APPLY, KC_MEAN, KC_SETUP, KC_DCT_FLOW, KC_COUNT
 };
 
 // Per-column CG scalars (device).  Column 0 = mean system (R2).
@@ -62,10 +62,12 @@ struct Ctx {
   uint32_t* maskL = nullptr;            // DCT2 1024 fast path: lane-packed mask (op_dct1k.cu)
   void* tab1k32 = nullptr; void* tab1k64 = nullptr;   // its twiddle tables (float / double)
   bool fast1k = false;                  // DCT2 1024 x 1024: fast path, mean column on `side`
+  void* flow_state = nullptr;           // k1k_flow (dataflow probe kernel): dispenser / counters
+  void* flow_part2 = nullptr;           //   and its rho' partials [m_cap][D tiles]
   cudaStream_t side = nullptr;          // second stream (mean column of the fast DCT path)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // fast DCT path: probe-column groups 1..3 on their own streams with their own s accumulators
-  static constexpr int MAXG = 4;
+  static constexpr int MAXG = 8;
   int probe_groups = 1;                 // groups of the E-step being enqueued (launch sizing)
   cudaStream_t gstream[MAXG] = {};
   cudaEvent_t gjoin[MAXG] = {};
@@ -268,6 +270,8 @@ cofem_status conv_apply(Ctx* c, int m, int iter);
 bool dct1k_eligible(const Ctx* c);
 cofem_status dct1k_setup(Ctx* c);
 cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);
+cofem_status dct1k_flow(Ctx* c, int K, int K_total, cudaStream_t st);   // all U iterations of the fp32 probes
+int dct1k_flow_groups(const Ctx* c, int K);                             // its column groups
 bool conv_fft_eligible(const Ctx* c);
 cofem_status conv_fft_setup(Ctx* c, const std::vector<double>& g);
 cofem_status conv_fft_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st);

@@ -114,6 +114,22 @@ __device__ __forceinline__ void dct2_post(const cplx<T>* W, int t, T (&lo)[8], T
   }
 }
 
+// v-order permutation m -> natural index (Makhoul's even/odd shuffle)
+__host__ __device__ __forceinline__ int vperm(int m, int L) { return m < L / 2 ? 2 * m : 2 * (L - 1 - m) + 1; }
+
+// Convention 1 (Phi = S C2, reading R11: BASELINE config 4's literal "rows of DCT-II"): the forward
+// transform comes first.  DCT-II of a natural-order sequence X (stride xs): the packed input of the
+// M-point FFT, z[i] = X[vperm(2i)] + i X[vperm(2i+1)] for i = t + r M/8 (thread t of the team).
+template <typename T, int L>
+__device__ __forceinline__ void dct2_gather(const T* X, int xs, int t, cplx<T> (&v)[8]) {
+  constexpr int M = L / 2, NT = M / 8;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int i = t + r * NT;
+    v[r] = {X[vperm(2 * i, L) * xs], X[vperm(2 * i + 1, L) * xs]};
+  }
+}
+
 constexpr int DCT_THREADS = 256;
 constexpr int ROW_ITERS = 2;
 template <int L> struct RowGeom {
@@ -121,7 +137,7 @@ template <int L> struct RowGeom {
 };
 
 // ---------------------------------------------------------------- pass A
-template <typename T, int L>
+template <typename T, int L, int CONV>
 __device__ void rows_inv_body(const DctArgs& a, int j, bool dir, double bcoef, T* sm) {
   using G = RowGeom<L>;
   const int team = threadIdx.x / G::NT, t = threadIdx.x % G::NT;
@@ -143,8 +159,19 @@ __device__ void rows_inv_body(const DctArgs& a, int j, bool dir, double bcoef, T
     }
     __syncthreads();
     cplx<T> v[8];
-    dct3_gather<T, L>(row, 1, t, v, tb);
-    fft_team<T, G::M, +1>(buf, v, t, tb.tw);
+    if constexpr (CONV == 0) {         // DCT-III along the row -> v-order pixel columns
+      dct3_gather<T, L>(row, 1, t, v, tb);
+      fft_team<T, G::M, +1>(buf, v, t, tb.tw);
+    } else {                           // DCT-II along the row -> natural-order pixel columns
+      dct2_gather<T, L>(row, 1, t, v);
+      fft_team<T, G::M, -1>(buf, v, t, tb.tw);
+      T lo[8], hi[8];
+      dct2_post<T, L>(buf, t, lo, hi, tb);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { row[t + q * G::NT] = lo[q]; row[t + q * G::NT + G::M] = hi[q]; }
+      __syncthreads();
+    }
     if (active) {
       const int64_t base = (int64_t)r * L;
       for (int e = t; e < L; e += G::NT) c.t1[base + e] = row[e];
@@ -153,20 +180,20 @@ __device__ void rows_inv_body(const DctArgs& a, int j, bool dir, double bcoef, T
   }
 }
 
-template <typename TP, int L>
+template <typename TP, int L, int CONV>
 __global__ void __launch_bounds__(DCT_THREADS) k_dct_rows_inv(DctArgs a, int dir) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int j = blockIdx.y;
   const ColState st = a.cs[j];
   if (st.frozen) return;
-  if (j == 0) rows_inv_body<double, L>(a, 0, dir, st.b, reinterpret_cast<double*>(smem_raw));
-  else rows_inv_body<TP, L>(a, j, dir, st.b, reinterpret_cast<TP*>(smem_raw));
+  if (j == 0) rows_inv_body<double, L, CONV>(a, 0, dir, st.b, reinterpret_cast<double*>(smem_raw));
+  else rows_inv_body<TP, L, CONV>(a, j, dir, st.b, reinterpret_cast<TP*>(smem_raw));
 }
 
 // ---------------------------------------------------------------- pass B
 template <typename T> struct StripW { static constexpr int W = sizeof(T) == 8 ? 8 : 16; };
 
-template <typename T, int L>
+template <typename T, int L, int CONV>
 __device__ void cols_body(const DctArgs& a, int j, T* sm) {
   constexpr int M = L / 2, NT = M / 8, TEAMS = DCT_THREADS / NT, W = StripW<T>::W, WS = W + 1;
   const int c0 = blockIdx.x * W;
@@ -187,6 +214,37 @@ __device__ void cols_body(const DctArgs& a, int j, T* sm) {
     const bool active = cc < W;
     const int ccs = active ? cc : 0;
     cplx<T> v[8];
+    if constexpr (CONV == 1) {
+      // DCT-II along the column (natural-order pixel rows), mask, DCT-III back (v-order output rows)
+      dct2_gather<T, L>(strip + ccs, WS, t, v);
+      fft_team<T, M, -1>(buf, v, t, tb.tw);
+      T lo[8], hi[8];
+      dct2_post<T, L>(buf, t, lo, hi, tb);
+      const uint8_t* mk = a.maskT + (int64_t)(c0 + ccs) * a.rows;   // natural-order mask, [cols][rows]
+      __syncthreads();                           // every team has read its column
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int k = t + r * NT;
+          strip[k * WS + cc] = mk[k] ? lo[r] : (T)0;
+          strip[(k + M) * WS + cc] = mk[k + M] ? hi[r] : (T)0;
+        }
+      }
+      __syncthreads();
+      dct3_gather<T, L>(strip + ccs, WS, t, v, tb);
+      fft_team<T, M, +1>(buf, v, t, tb.tw);      // v-order rows, complex-packed
+      if (active) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = t + r * NT;
+          const cplx<T> w = buf[i];
+          strip[(2 * i) * WS + cc] = w.x;
+          strip[(2 * i + 1) * WS + cc] = w.y;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     dct3_gather<T, L>(strip + ccs, WS, t, v, tb);
     fft_team<T, M, +1>(buf, v, t, tb.tw);        // v-order pixel column (complex-packed)
     const uint8_t* mk = a.maskT + (int64_t)(c0 + ccs) * a.rows;
@@ -216,17 +274,17 @@ __device__ void cols_body(const DctArgs& a, int j, T* sm) {
   }
 }
 
-template <typename TP, int L>
+template <typename TP, int L, int CONV>
 __global__ void __launch_bounds__(DCT_THREADS) k_dct_cols(DctArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int j = blockIdx.y;
   if (a.cs[j].frozen) return;
-  if (j == 0) cols_body<double, L>(a, 0, reinterpret_cast<double*>(smem_raw));
-  else cols_body<TP, L>(a, j, reinterpret_cast<TP*>(smem_raw));
+  if (j == 0) cols_body<double, L, CONV>(a, 0, reinterpret_cast<double*>(smem_raw));
+  else cols_body<TP, L, CONV>(a, j, reinterpret_cast<TP*>(smem_raw));
 }
 
 // ---------------------------------------------------------------- pass C
-template <typename T, int L>
+template <typename T, int L, int CONV>
 __device__ double rows_fwd_body(const DctArgs& a, int j, T* sm) {
   using G = RowGeom<L>;
   const int team = threadIdx.x / G::NT, t = threadIdx.x % G::NT;
@@ -239,19 +297,35 @@ __device__ double rows_fwd_body(const DctArgs& a, int j, T* sm) {
   for (int it = 0; it < ROW_ITERS; ++it) {
     const int r = blockIdx.x * G::RPC + it * G::TEAMS + team;
     const bool active = r < a.rows;
-    const int64_t base = (int64_t)r * L;
+    // conv. 1: T2 row r holds coefficient row vperm(r) (pass B left the rows in v-order)
+    const int64_t base = (int64_t)(CONV == 0 || !active ? r : vperm(r, a.rows)) * L, base_in = (int64_t)r * L;
     if (active)
-      for (int e = t; e < L; e += G::NT) row[e] = c.t2[base + e];
+      for (int e = t; e < L; e += G::NT) row[e] = c.t2[base_in + e];
     __syncthreads();
     cplx<T> v[8];
+    if constexpr (CONV == 0) {         // DCT-II along the row (packed v-order input) -> natural coefficients
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = buf[t + q * G::NT];
-    fft_team<T, G::M, -1>(buf, v, t, tb.tw);
-    T lo[8], hi[8];
-    dct2_post<T, L>(buf, t, lo, hi, tb);
-    __syncthreads();
+      for (int q = 0; q < 8; ++q) v[q] = buf[t + q * G::NT];
+      fft_team<T, G::M, -1>(buf, v, t, tb.tw);
+      T lo[8], hi[8];
+      dct2_post<T, L>(buf, t, lo, hi, tb);
+      __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 8; ++q) { row[t + q * G::NT] = lo[q]; row[t + q * G::NT + G::M] = hi[q]; }
+      for (int q = 0; q < 8; ++q) { row[t + q * G::NT] = lo[q]; row[t + q * G::NT + G::M] = hi[q]; }
+    } else {                           // DCT-III along the row (natural input) -> v-order, un-shuffled
+      dct3_gather<T, L>(row, 1, t, v, tb);
+      fft_team<T, G::M, +1>(buf, v, t, tb.tw);
+      cplx<T> w[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w[q] = buf[t + q * G::NT];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = t + q * G::NT;
+        row[vperm(2 * i, L)] = w[q].x;
+        row[vperm(2 * i + 1, L)] = w[q].y;
+      }
+    }
     __syncthreads();
     if (active) {
       for (int e = t; e < L; e += G::NT) {
@@ -266,13 +340,13 @@ __device__ double rows_fwd_body(const DctArgs& a, int j, T* sm) {
   return g;
 }
 
-template <typename TP, int L>
+template <typename TP, int L, int CONV>
 __global__ void __launch_bounds__(DCT_THREADS) k_dct_rows_fwd(DctArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int j = blockIdx.y;
   if (a.cs[j].frozen) return;
-  double g = j == 0 ? rows_fwd_body<double, L>(a, 0, reinterpret_cast<double*>(smem_raw))
-                    : rows_fwd_body<TP, L>(a, j, reinterpret_cast<TP*>(smem_raw));
+  double g = j == 0 ? rows_fwd_body<double, L, CONV>(a, 0, reinterpret_cast<double*>(smem_raw))
+                    : rows_fwd_body<TP, L, CONV>(a, j, reinterpret_cast<TP*>(smem_raw));
   g = block_sum(g);
   ColState* cs = a.cs;
   const int iter = a.iter;
@@ -282,8 +356,6 @@ __global__ void __launch_bounds__(DCT_THREADS) k_dct_rows_fwd(DctArgs a) {
 }
 
 // ---------------------------------------------------------------- setup kernels
-// v-order permutation m -> pixel index
-__host__ __device__ __forceinline__ int vperm(int m, int L) { return m < L / 2 ? 2 * m : 2 * (L - 1 - m) + 1; }
 
 __global__ void k_mask_scatter(const int64_t* __restrict__ obs, int64_t N, uint8_t* __restrict__ mask) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
@@ -299,6 +371,13 @@ __global__ void k_mask_vvT(const uint8_t* __restrict__ mask, int rows, int cols,
 __global__ void k_y_scatter(const int64_t* __restrict__ obs, int64_t N, const float* __restrict__ y, double* __restrict__ img) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
     img[obs[i]] = (double)y[i];
+}
+__global__ void k_mask_T(const uint8_t* __restrict__ mask, int rows, int cols, uint8_t* __restrict__ maskT) {
+  const int64_t total = (int64_t)rows * cols;     // natural order, transposed [cols][rows] (convention 1)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i / rows), r = (int)(i % rows);
+    maskT[i] = mask[(int64_t)r * cols + c];
+  }
 }
 __global__ void k_mask_to_double(const uint8_t* __restrict__ m, int64_t n, double* __restrict__ out) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -369,13 +448,18 @@ template <int L> static size_t col_smem() {
 
 template <typename TP>
 static cofem_status set_attrs(Ctx* c) {
-#define SET_ROW(L)                                                                                               \
-  if (c->cols == L) {                                                                                            \
-    cudaFuncSetAttribute(k_dct_rows_inv<TP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
-    cudaFuncSetAttribute(k_dct_rows_fwd<TP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
+#define SET_ROW(L)                                                                                                  \
+  if (c->cols == L) {                                                                                               \
+    cudaFuncSetAttribute(k_dct_rows_inv<TP, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
+    cudaFuncSetAttribute(k_dct_rows_fwd<TP, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
+    cudaFuncSetAttribute(k_dct_rows_inv<TP, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
+    cudaFuncSetAttribute(k_dct_rows_fwd<TP, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)row_smem<L>()); \
   }
-#define SET_COL(L) \
-  if (c->rows == L) cudaFuncSetAttribute(k_dct_cols<TP, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem<L>());
+#define SET_COL(L)                                                                                                  \
+  if (c->rows == L) {                                                                                               \
+    cudaFuncSetAttribute(k_dct_cols<TP, L, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem<L>());     \
+    cudaFuncSetAttribute(k_dct_cols<TP, L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)col_smem<L>());     \
+  }
   DCT_LENGTHS(SET_ROW)
   DCT_LENGTHS(SET_COL)
 #undef SET_ROW
@@ -384,7 +468,6 @@ static cofem_status set_attrs(Ctx* c) {
 }
 
 cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
-  if (c->conv != 0) { c->err = "DCT2: convention 1 is not implemented on the GPU path"; return COFEM_ERR_UNSUPPORTED; }
   const int rows = c->rows, cols = c->cols;
   const int64_t D = c->D;
   // twiddle tables: [rows-length | cols-length], float and double
@@ -412,7 +495,8 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   cudaMemsetAsync(img, 0, D * 8, c->stream);
   launch_begin(c, KC_SETUP);
   k_mask_scatter<<<c->num_sms * 4, 256, 0, c->stream>>>(obs_dev, c->N, mask);
-  k_mask_vvT<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, rows, cols, c->mask_vvT);
+  if (c->conv == 0) k_mask_vvT<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, rows, cols, c->mask_vvT);
+  else k_mask_T<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, rows, cols, c->mask_vvT);
   k_mask_to_double<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, D, md);
   k_y_scatter<<<c->num_sms * 4, 256, 0, c->stream>>>(obs_dev, c->N, y_dev, img);
   launch_end(c, KC_SETUP);
@@ -420,13 +504,16 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   std::vector<double> h;
   dct_matrix(h, rows, true); cudaMemcpyAsync(Cr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
   dct_matrix(h, cols, true); cudaMemcpyAsync(Cc, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
-  gemm64(c, rows, cols, cols, md, cols, 0, Cc, cols, 1, tmp, cols, 1.0);        // M Q_c^T
-  gemm64(c, rows, cols, rows, Cr, rows, 0, tmp, cols, 0, c->colsq, cols, 1.0);  // Q_r (M Q_c^T)
+  // convention 1 (Phi = S C2, Phi[n, d] = C2[obs_n, d]): colsq = Q_r^T M Q_c
+  const int tcv = c->conv ? 0 : 1, tr = c->conv ? 1 : 0;
+  gemm64(c, rows, cols, cols, md, cols, 0, Cc, cols, tcv, tmp, cols, 1.0);        // M Q_c^T  (conv. 1: M Q_c)
+  gemm64(c, rows, cols, rows, Cr, rows, tr, tmp, cols, 0, c->colsq, cols, 1.0);   // Q_r (.)  (conv. 1: Q_r^T (.))
   // b0 = beta C_r Y C_c^T (Phi^T y: scatter, forward 2D DCT), fp64
   dct_matrix(h, rows, false); cudaMemcpyAsync(Cr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
   dct_matrix(h, cols, false); cudaMemcpyAsync(Cc, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
-  gemm64(c, rows, cols, cols, img, cols, 0, Cc, cols, 1, tmp, cols, 1.0);
-  gemm64(c, rows, cols, rows, Cr, rows, 0, tmp, cols, 0, c->b0, cols, c->beta);
+  // convention 1: Phi^T y = C2^T (S^T y) = C_r^T Y C_c
+  gemm64(c, rows, cols, cols, img, cols, 0, Cc, cols, tcv, tmp, cols, 1.0);
+  gemm64(c, rows, cols, rows, Cr, rows, tr, tmp, cols, 0, c->b0, cols, c->beta);
   cudaStreamSynchronize(c->stream);
   cudaFree(mask); cudaFree(md); cudaFree(tmp); cudaFree(img); cudaFree(Cr); cudaFree(Cc);
   if (check_launch(c, "dct setup")) return COFEM_ERR_CUDA;
@@ -438,7 +525,7 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   const int gridA = (rows + rpc - 1) / rpc;
   c->part_stride = std::max(c->part_stride, gridA);
   cofem_status st = c->probe64 ? set_attrs<double>(c) : set_attrs<float>(c);
-  if (st == COFEM_OK && dct1k_eligible(c) && c->opt.apply_path != 1) {   // apply_path 1: the generic passes
+  if (st == COFEM_OK && dct1k_eligible(c) && c->opt.apply_path != 1 && c->conv == 0) {   // apply_path 1 / conv. 1: generic
     st = dct1k_setup(c);
     c->fast1k = st == COFEM_OK;
     for (int g = 1; c->fast1k && g < Ctx::MAXG; ++g)      // probe groups' s accumulators (cofem.cu)
@@ -473,7 +560,8 @@ static cofem_status dct_apply_t(Ctx* c, int m, int iter, bool dir) {
   if (c->cols == L) {                                                                                    \
     dim3 g((c->rows + RowGeom<L>::RPC - 1) / RowGeom<L>::RPC, m);                                        \
     launch_begin(c, KC_DCT_ROWS_INV);                                                                    \
-    k_dct_rows_inv<TP, L><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a, dir ? 1 : 0);                  \
+    if (c->conv) k_dct_rows_inv<TP, L, 1><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a, dir ? 1 : 0);  \
+    else k_dct_rows_inv<TP, L, 0><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a, dir ? 1 : 0);          \
     launch_end(c, KC_DCT_ROWS_INV);                                                                      \
     launched = true;                                                                                     \
   }
@@ -485,7 +573,8 @@ static cofem_status dct_apply_t(Ctx* c, int m, int iter, bool dir) {
   if (c->rows == L) {                                                                                    \
     dim3 g(c->cols / StripW<double>::W, m);                                                              \
     launch_begin(c, KC_DCT_COLS);                                                                        \
-    k_dct_cols<TP, L><<<g, DCT_THREADS, col_smem<L>(), c->stream>>>(a);                                  \
+    if (c->conv) k_dct_cols<TP, L, 1><<<g, DCT_THREADS, col_smem<L>(), c->stream>>>(a);                  \
+    else k_dct_cols<TP, L, 0><<<g, DCT_THREADS, col_smem<L>(), c->stream>>>(a);                          \
     launch_end(c, KC_DCT_COLS);                                                                          \
     launched = true;                                                                                     \
   }
@@ -497,7 +586,8 @@ static cofem_status dct_apply_t(Ctx* c, int m, int iter, bool dir) {
   if (c->cols == L) {                                                                                    \
     dim3 g((c->rows + RowGeom<L>::RPC - 1) / RowGeom<L>::RPC, m);                                        \
     launch_begin(c, KC_DCT_ROWS_FWD);                                                                    \
-    k_dct_rows_fwd<TP, L><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a);                               \
+    if (c->conv) k_dct_rows_fwd<TP, L, 1><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a);               \
+    else k_dct_rows_fwd<TP, L, 0><<<g, DCT_THREADS, row_smem<L>(), c->stream>>>(a);                       \
     launch_end(c, KC_DCT_ROWS_FWD);                                                                      \
     launched = true;                                                                                     \
   }

@@ -82,10 +82,30 @@ __device__ __forceinline__ void post_all(int lane, const cplx<T> (&va)[8], const
   }
 }
 
+// Loads of arrays other CTAs of the same launch may have rewritten (the dataflow kernel k1k_flow:
+// p, r, T^T, T2, q change between its items): CG = true reads through L2 (ld.global.cg), never a
+// stale L1 line.  The per-pass kernels (one pass per launch) read normally.
+template <bool CG, typename V> __device__ __forceinline__ V ldx(const V* p) {
+  if constexpr (CG) return __ldcg(p); else return *p;
+}
+template <bool CG> __device__ __forceinline__ cplx<float> ldc(const cplx<float>* p) {
+  const float2 v = ldx<CG>(reinterpret_cast<const float2*>(p));
+  return {v.x, v.y};
+}
+template <bool CG> __device__ __forceinline__ cplx<double> ldc(const cplx<double>* p) {
+  const double2 v = ldx<CG>(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+
 template <typename T> __device__ __forceinline__ const T* alpha_of(const DctArgs& a, int j) {
   if constexpr (sizeof(T) == 8) { if (j == 0) return a.alpha; }
   return (const T*)a.alphap;
 }
+
+// Barrier of the RT warps that process an item: barrier 1 over RT * 32 threads.  In the per-pass
+// kernels that is the whole CTA (= __syncthreads); in k1k_flow the worker warps, without the
+// control warp.
+template <int RT> __device__ __forceinline__ void bar_rt() { asm volatile("bar.sync 1, %0;" ::"n"(RT * 32) : "memory"); }
 
 // RT consecutive elements (32 bytes) <-> registers
 template <typename T, int N> __device__ __forceinline__ void st32B(T* p, const T (&v)[N]) {
@@ -131,7 +151,7 @@ template <typename T> __device__ __forceinline__ const cplx<T>* tab1k(const DctA
 // Persistent kernels: work item w = (column j0 + w / NTILE, tile w % NTILE), grid-strided.
 template <typename T> struct Work { static constexpr int NTILE = L / Geo<T>::RT; };
 
-template <typename T>
+template <typename T, bool CG = false>
 __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile, int dir, double bcoef, T* sm,
                                               const Tw<T>& tb);
 
@@ -174,7 +194,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_INV
   }
 }
 
-template <typename T>
+template <typename T, bool CG>
 __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile, int dir, double bcoef, T* sm,
                                               const Tw<T>& tb) {
   constexpr int RT = Geo<T>::RT;
@@ -196,11 +216,11 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
     for (int h = 0; h < 2; ++h) {
       float4 pv[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) pv[i] = pr[lane + 32 * (4 * h + i)];
+      for (int i = 0; i < 4; ++i) pv[i] = ldx<CG>(pr + lane + 32 * (4 * h + i));
       if (dir) {
         float4 rv[4], dd[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { rv[i] = rr[lane + 32 * (4 * h + i)]; dd[i] = dv[lane + 32 * (4 * h + i)]; }
+        for (int i = 0; i < 4; ++i) { rv[i] = ldx<CG>(rr + lane + 32 * (4 * h + i)); dd[i] = dv[lane + 32 * (4 * h + i)]; }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {    // a6: p = M^-1 r + b p
           pv[i].x = dd[i].x * rv[i].x + bb * pv[i].x; pv[i].y = dd[i].y * rv[i].y + bb * pv[i].y;
@@ -259,7 +279,7 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
     *reinterpret_cast<cplx<T>*>(reg + 2 * (ja + 64 * r)) = va[r];
     *reinterpret_cast<cplx<T>*>(reg + 2 * (jb + 64 * r)) = vb[r];
   }
-  __syncthreads();
+  bar_rt<RT>();
   T* __restrict__ out = c.t1;       // T^T[cv][row], line length L
 #pragma unroll
   for (int it = 0; it < L / (RT * 32); ++it) {
@@ -272,7 +292,7 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
 }
 
 // ---------------------------------------------------------------- pass B
-template <typename T>
+template <typename T, bool CG = false>
 __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
 
 template <typename T>
@@ -297,7 +317,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, i
   }
 }
 
-template <typename T>
+template <typename T, bool CG>
 __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb) {
   constexpr int RT = Geo<T>::RT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -310,7 +330,7 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
   for (int r = 0; r < 8; ++r) {
     int o[4];
     canon(lane, r, o);
-    A[r] = ln[o[0]]; B[r] = ln[o[1]]; C[r] = ln[o[2]]; E[r] = ln[o[3]];
+    A[r] = ldx<CG>(ln + o[0]); B[r] = ldx<CG>(ln + o[1]); C[r] = ldx<CG>(ln + o[2]); E[r] = ldx<CG>(ln + o[3]);
   }
   cplx<T> va[8], vb[8];
   pre_all<T>(lane, A, B, C, E, va, vb, tb);
@@ -331,7 +351,7 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
     canon(lane, r, o);
     reg[o[0]] = A[r]; reg[o[1]] = B[r]; reg[o[2]] = C[r]; reg[o[3]] = E[r];
   }
-  __syncthreads();
+  bar_rt<RT>();
   T* __restrict__ out = c.t2;       // T2[row][cv] row-major: 32-byte segments of RT v-order columns
 #pragma unroll
   for (int it = 0; it < L / (RT * 32); ++it) {
@@ -341,11 +361,11 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
     for (int i = 0; i < RT; ++i) v[i] = sm[i * WREG + row];
     st32B<T, RT>(out + (int64_t)row * L + tile * RT, v);
   }
-  __syncthreads();
+  bar_rt<RT>();
 }
 
 // ---------------------------------------------------------------- pass C
-template <typename T>
+template <typename T, bool CG = false>
 __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
 
 template <typename T>
@@ -402,7 +422,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
   if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
-template <typename T>
+template <typename T, bool CG>
 __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb) {
   constexpr int RT = Geo<T>::RT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -415,7 +435,7 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
   {
     const cplx<T>* __restrict__ rowc = reinterpret_cast<const cplx<T>*>(c.t2 + rb);   // packed v-order z[n]
 #pragma unroll
-    for (int r = 0; r < 8; ++r) { va[r] = rowc[ja + 64 * r]; vb[r] = rowc[jb + 64 * r]; }
+    for (int r = 0; r < 8; ++r) { va[r] = ldc<CG>(rowc + ja + 64 * r); vb[r] = ldc<CG>(rowc + jb + 64 * r); }
   }
   fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   T A[8], B[8], C[8], E[8];
@@ -440,7 +460,7 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
     for (int h = 0; h < 2; ++h) {
       float4 pv[4], av[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { pv[i] = pp[lane + 32 * (4 * h + i)]; av[i] = al[lane + 32 * (4 * h + i)]; }
+      for (int i = 0; i < 4; ++i) { pv[i] = ldx<CG>(pp + lane + 32 * (4 * h + i)); av[i] = al[lane + 32 * (4 * h + i)]; }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {   // a3: q = beta Phi^T Phi p + alpha o p; a4: gamma partial
         const float4 x = r4[lane + 32 * (4 * h + i)];
@@ -479,6 +499,389 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
   }
   return warp_sum(g);
 }
+
+
+// ---------------------------------------------------------------- dataflow E-step (fp32 probe columns)
+// All U CG iterations of the fp32 probe columns in ONE persistent launch.  The columns are
+// independent systems (reading R3), so nothing forces them into lockstep: the work is a stream of
+// items -- A (pass A, 8 image rows of one column), B (pass B, 8 T^T lines), C (pass C, 8 rows +
+// gamma partials), U (the update a5 of one 2048-element D tile for a GROUP of columns, with the
+// group's s accumulator) -- that CTAs take from a global counter in a fixed order.  An item waits
+// only for the phase before it of its own column (A(i) <- U(i-1) of its group: b_j; B(i) <- all
+// A(i) of the column: the transpose; C(i) <- all B(i); U(i) <- gamma of every column of the group),
+// and that phase was dispensed earlier, so the earliest unfinished item can always run: no
+// deadlock, whatever the number of resident CTAs.  The G groups are dispensed one phase apart
+// (step tau: group g at phase tau - g), so A, B, C and U items of different groups run side by side
+// on every SM (HBM-heavy row passes next to the shared-memory-heavy column pass) without the
+// launch fill/drain of the per-pass kernels.  Reductions: gamma from one partial per image row
+// (pass C), rho' from one partial per D tile, each reduced in fixed order by the CTA that completes
+// the phase (deterministic).  Data other items rewrote is read through L2 (CG loads).
+namespace flow {
+constexpr int MAXG = 8;
+constexpr int NT = L / 8;                 // fp32: 8 rows / lines per A, B, C item
+struct State {                            // zeroed before every launch
+  unsigned long long head;                // next item to dispense
+  int nfrozen, pad;
+  unsigned cntA[MAXM], cntB[MAXM], cntC[MAXM];   // completed items per probe column (all iterations)
+  int doneC[MAXM];                        // iterations whose gamma is applied, per probe column
+  int frozen[MAXM];                       // polling mirror of ColState::frozen
+  unsigned cntU[MAXG];
+  int doneU[MAXG];                        // iterations whose rho' is applied, per group
+};
+struct Args {
+  State* st;
+  int K, G, U, ntiles;                    // probe columns (global 1..K), groups, CG iterations, D tiles
+  int g0[MAXG + 1];                       // group g = probe columns [g0[g], g0[g+1]) (0-based)
+  int H, Gh, VS;                          // halves of a step, groups per half, virtual block size
+  long long step, total;                  // items per step; items to dispense
+  double invK;                            // 1 / K_total (Eq. 6)
+  double* s[MAXG];                        // s accumulator of each group
+  double* part2;                          // rho' partials, [column j][tile]
+  const uint32_t* bits; int64_t wpc;
+  const float *R0, *dinvp;                // for the update items (R is DctArgs::R)
+};
+
+__device__ __forceinline__ int ld_acq(const int* p) {
+  int v; asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v; asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
+}
+__device__ __forceinline__ void st_rel(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// thread 0: wait until *cnt >= target, or the column froze (returns false then)
+template <typename C>
+__device__ __forceinline__ bool wait_ge(const C* cnt, C target, const int* frozen) {
+  for (;;) {
+    if (ld_acq(cnt) >= target) return true;
+    if (frozen && ld_acq(frozen)) return false;
+    __nanosleep(100);
+  }
+}
+
+// ColState read through L2: other CTAs of the launch rewrite it (the gamma / rho' finishers)
+__device__ __forceinline__ ColState ld_cs(const ColState* p) {
+  static_assert(sizeof(ColState) == 64, "ColState layout");
+  const double* d = reinterpret_cast<const double*>(p);
+  const int* n = reinterpret_cast<const int*>(d + 5);
+  ColState c;
+  c.rho = __ldcg(d); c.rho0 = __ldcg(d + 1); c.gamma = __ldcg(d + 2); c.a = __ldcg(d + 3); c.b = __ldcg(d + 4);
+  c.frozen = __ldcg(n); c.frozen_at = __ldcg(n + 1); c.nonfinite = __ldcg(n + 2); c.pad = __ldcg(n + 3);
+  c.tau = __ldcg(d + 7);
+  return c;
+}
+
+__device__ __forceinline__ int size_of(const Args& f, int g, int ph) {
+  return ph < 3 ? (f.g0[g + 1] - f.g0[g]) * NT : f.ntiles;
+}
+// Dispense order.  Step tau holds one block per group: group g at phase counter pi = tau - g
+// (pi = 4 i + phase).  A step is split into H halves of Gh groups; within a half the items of its
+// blocks are dealt round-robin (item r -> block r mod Gh, index r / Gh), every block padded to the
+// virtual size VS (padding items are skipped), so the SMs always hold a mix of the phase types of
+// Gh consecutive groups.  A block depends on its own group's block of the previous step, which sat
+// in the same half one step earlier: (H - 1) / H of a step apart, so the dependency is complete
+// before the block starts (no bubble) when H = 2.
+__device__ __forceinline__ void decode(const Args& f, long long q, int& g, int& pi, int& k) {
+  const long long tau = q / f.step;
+  const int r = (int)(q - tau * f.step);
+  const int hs = f.Gh * f.VS, h = r / hs, rr = r - h * hs;
+  g = h * f.Gh + rr % f.Gh;
+  k = rr / f.Gh;
+  pi = (int)tau - g;
+  if (g >= f.G || k >= size_of(f, g, pi & 3)) pi = -1;    // padding
+}
+
+// Worker barrier: the 8 worker warps of k1k_flow (and the RT warps of the per-pass kernels,
+// where it equals __syncthreads); barrier 1, so the control warp never takes part.
+template <int N> __device__ __forceinline__ void worker_sync() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
+
+constexpr int NW = 8;                     // worker warps (one image row / T^T line each)
+constexpr int FLOW_THREADS = (NW + 1) * 32;   // + the control warp
+
+struct Item {                             // one published work item (ring slot)
+  int go;                                 // 1 work, 2 skip, 0 stop
+  int ph, i, g, k;                        // phase (A, B, C, U), CG iteration, group, index in block
+};
+#ifndef COFEM_FLOW_SLOTS
+#define COFEM_FLOW_SLOTS 2      // ring depth (items published ahead of the workers)
+#endif
+constexpr int NSLOT = COFEM_FLOW_SLOTS;
+struct Smem {
+  Item ring[NSLOT];
+  uint64_t full[NSLOT], done[NSLOT];      // mbarriers: item published / item finished by the workers
+  double red[NW][MAXM];                   // U items: per-warp rho' sums
+  double a[NSLOT][MAXM]; int act[NSLOT][MAXM];   // U items: step lengths / activity of the group, per slot
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  for (;;) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(su32(b)), "r"(parity) : "memory");
+    if (ok) return;
+  }
+}
+
+// U item: a5 for the columns of group g on D tile t (k_update's arithmetic): r -= a q, z = r / diag,
+// rho' partial, s += (a/K) p_k o p (x_k never stored)
+__device__ __forceinline__ void update_item(const DctArgs& a, const Args& f, Smem& sh, int slot, int g, int t) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = f.g0[g], c1 = f.g0[g + 1];
+  const int64_t d0 = (int64_t)t * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
+  float dp[8];
+  {
+    const float4 x = *reinterpret_cast<const float4*>(f.dinvp + d0), y = *reinterpret_cast<const float4*>(f.dinvp + d0 + 4);
+    dp[0] = x.x; dp[1] = x.y; dp[2] = x.z; dp[3] = x.w; dp[4] = y.x; dp[5] = y.y; dp[6] = y.z; dp[7] = y.w;
+  }
+  double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  bool any = false;
+  for (int jj = c0; jj < c1; ++jj) {
+    const int cl = jj - c0;
+    if (!sh.act[slot][cl]) { if (lane == 0) sh.red[warp][cl] = 0.0; continue; }
+    any = true;
+    const int64_t o = (int64_t)jj * a.Dp + d0;
+    float* Rp = (float*)a.R + o;
+    const float* Qp = (const float*)a.Q + o;
+    const float* Pp = (const float*)a.P + o;
+    float4 r4[2] = {__ldcg(reinterpret_cast<const float4*>(Rp)), __ldcg(reinterpret_cast<const float4*>(Rp) + 1)};
+    const float4 q4[2] = {__ldcg(reinterpret_cast<const float4*>(Qp)), __ldcg(reinterpret_cast<const float4*>(Qp) + 1)};
+    const float4 p4[2] = {__ldcg(reinterpret_cast<const float4*>(Pp)), __ldcg(reinterpret_cast<const float4*>(Pp) + 1)};
+    const uint32_t w = (f.bits[(int64_t)jj * f.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
+    const double ak = sh.a[slot][cl];
+    const float akt = (float)ak;
+    const double aks = ak * f.invK;
+    float* r = reinterpret_cast<float*>(r4);
+    const float* q = reinterpret_cast<const float*>(q4);
+    const float* pv = reinterpret_cast<const float*>(p4);
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      r[e] = r[e] - akt * q[e];
+      const float z = dp[e] * r[e];
+      acc += (double)r[e] * (double)z;
+      const double pe = (double)pv[e];
+      sacc[e] += ((w >> e) & 1u) ? -aks * pe : aks * pe;
+    }
+    reinterpret_cast<float4*>(Rp)[0] = r4[0]; reinterpret_cast<float4*>(Rp)[1] = r4[1];
+    acc = warp_sum(acc);
+    if (lane == 0) sh.red[warp][cl] = acc;
+  }
+  if (any) {
+    double* sp = f.s[g] + d0;
+    double2 v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { v[e] = __ldcg(reinterpret_cast<const double2*>(sp) + e); v[e].x += sacc[2 * e]; v[e].y += sacc[2 * e + 1]; }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) reinterpret_cast<double2*>(sp)[e] = v[e];
+  }
+  worker_sync<NW * 32>();
+  for (int cl = threadIdx.x; cl < c1 - c0; cl += NW * 32) {
+    double v = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) v += sh.red[ww][cl];
+    f.part2[(int64_t)(c0 + cl + 1) * f.ntiles + t] = v;
+  }
+}
+
+#ifndef COFEM_FLOW_MINB
+#define COFEM_FLOW_MINB 2     // CTAs per SM
+#endif
+// Warp-specialised: warps 0..7 process items; warp 8 (control) dispenses them into a two-slot ring
+// (mbarriers), waits for their dependencies, and after the workers finish an item releases it
+// (fence + completion count) and runs the gamma / rho' finishers -- so the worker warps never
+// wait on the dispenser atomic, the dependency polls or the release fences.
+__global__ void __launch_bounds__(FLOW_THREADS, COFEM_FLOW_MINB) k1k_flow(DctArgs a, Args f) {
+  using T = float;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  __shared__ Smem sh;
+  State* st = f.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s2 = 0; s2 < NSLOT; ++s2) { mb_init(&sh.full[s2], 1); mb_init(&sh.done[s2], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const Tw<T> tb = load_tables<T>((const cplx<T>*)a.tab1k32, reinterpret_cast<cplx<T>*>(sm + NW * WREG));   // + barrier
+  if (warp == NW) {
+    // ------------------------------------------------------------ control warp
+    // A polling state machine, never blocking on another CTA while it holds finished work: it
+    // releases finished items in order, keeps one dequeued candidate, and publishes it into a free
+    // slot once its dependency holds (deadlock-free: published items have no open dependencies,
+    // and the candidate is the latest item the CTA holds).
+    const int U4 = 4 * f.U;
+    Item pend[NSLOT] = {}, cand = {};
+    int n_pub = 0, n_rel = 0;
+    bool have = false, stop = false;
+    for (;;) {
+      bool progress = false;
+      // 1) release the oldest published item once the workers are done with it
+      if (n_rel < n_pub) {
+        const int slot = n_rel % NSLOT;
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(su32(&sh.done[slot])), "r"((uint32_t)((n_rel / NSLOT) & 1)) : "memory");
+        if (ok) {
+          const Item it = pend[slot];
+          const int i = it.i, g = it.g;
+          if (it.ph < 3) {
+            const int jj = f.g0[g] + it.k / NT, j = jj + 1;
+            unsigned old = 0;
+            if (lane == 0) {
+              __threadfence();
+              unsigned* cnt = it.ph == 0 ? st->cntA + jj : it.ph == 1 ? st->cntB + jj : st->cntC + jj;
+              old = atomicAdd(cnt, 1u);
+            }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (it.ph == 2 && old + 1 == (unsigned)(NT * (i + 1))) {   // gamma_j complete (fixed-order reduction)
+              __threadfence();
+              const double tot = reduce_partials(a.part + (int64_t)j * a.stride, L);
+              if (lane == 0) {
+                ColState c = ld_cs(a.cs + j);
+                finish_gamma(c, tot, i);
+                a.cs[j] = c;
+                if (c.frozen) { st->frozen[jj] = 1; atomicAdd(&st->nfrozen, 1); }
+                __threadfence();
+                st_rel(st->doneC + jj, i + 1);
+              }
+            }
+          } else {
+            unsigned old = 0;
+            if (lane == 0) { __threadfence(); old = atomicAdd(st->cntU + g, 1u); }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            if (old + 1 == (unsigned)(f.ntiles * (i + 1))) {         // rho' of the group's columns
+              __threadfence();
+              for (int jj = f.g0[g]; jj < f.g0[g + 1]; ++jj) {
+                const int j = jj + 1;
+                const double v = reduce_partials(f.part2 + (int64_t)j * f.ntiles, f.ntiles);
+                if (lane == 0) {
+                  ColState c = ld_cs(a.cs + j);
+                  if (!c.frozen) { c.b = v / c.rho; c.rho = v; a.cs[j] = c; }
+                }
+              }
+              if (lane == 0) { __threadfence(); st_rel(st->doneU + g, i + 1); }
+            }
+          }
+          ++n_rel;
+          progress = true;
+        }
+      }
+      // 2) dequeue a candidate (skipping items outside the schedule and of frozen columns)
+      if (!have && !stop) {
+        int go = 1, g = 0, pi = 0, k = 0;
+        if (lane == 0) {
+          const long long q = (long long)atomicAdd(&st->head, 1ull);
+          if (q >= f.total || ld_acq(&st->nfrozen) >= f.K) go = 0;   // done / every column frozen (R5)
+          else {
+            decode(f, q, g, pi, k);
+            if (pi < 0 || pi >= U4) go = 2;
+            else if ((pi & 3) < 3 && ld_acq(st->frozen + f.g0[g] + k / NT)) go = 2;
+          }
+        }
+        go = __shfl_sync(0xffffffffu, go, 0);
+        if (go == 0) stop = true;
+        else if (go == 1) {
+          cand.go = 1; cand.g = __shfl_sync(0xffffffffu, g, 0); pi = __shfl_sync(0xffffffffu, pi, 0);
+          cand.k = __shfl_sync(0xffffffffu, k, 0); cand.ph = pi & 3; cand.i = pi >> 2;
+          have = true;
+        }
+        progress = true;
+      }
+      // 3) publish the candidate into a free slot once its dependency holds
+      if (have && n_pub - n_rel < NSLOT) {
+        int ready = 0;                              // 1 ready, 2 drop (column froze meanwhile)
+        if (lane == 0) {
+          const int i = cand.i, g = cand.g;
+          if (cand.ph < 3) {
+            const int jj = f.g0[g] + cand.k / NT;
+            if (ld_acq(st->frozen + jj)) ready = 2;
+            else if (cand.ph == 0) ready = (i == 0 || ld_acq(st->doneU + g) >= i) ? 1 : 0;
+            else if (cand.ph == 1) ready = ld_acq(st->cntA + jj) >= (unsigned)(NT * (i + 1)) ? 1 : 0;
+            else ready = ld_acq(st->cntB + jj) >= (unsigned)(NT * (i + 1)) ? 1 : 0;
+          } else {
+            ready = 1;
+            for (int jj = f.g0[g]; jj < f.g0[g + 1]; ++jj)
+              if (ld_acq(st->doneC + jj) < i + 1 && !ld_acq(st->frozen + jj)) { ready = 0; break; }
+          }
+          if (ready == 1) __threadfence();          // acquire side
+        }
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready == 2) { have = false; progress = true; }
+        else if (ready == 1) {
+          const int slot = n_pub % NSLOT;
+          if (cand.ph == 3) {                       // U: the group's a_j and activity
+            for (int cl = lane; cl < f.g0[cand.g + 1] - f.g0[cand.g]; cl += 32) {
+              const int j = f.g0[cand.g] + cl + 1;
+              sh.act[slot][cl] = !__ldcg(&a.cs[j].frozen);
+              sh.a[slot][cl] = __ldcg(&a.cs[j].a);
+            }
+          } else {                                  // L2 prefetch of its lines, one 128-B line per lane per row
+            const int j = f.g0[cand.g] + cand.k / NT + 1, tile = cand.k % NT;
+            const DctCol<T> cn = col_of<T>(a, j);
+            for (int w = 0; w < NW; ++w) {
+              const int64_t rn = (int64_t)(tile * NW + w) * L + 32 * lane;
+              if (cand.ph == 0) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cn.p + rn));
+                if (cand.i > 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(cn.r + rn));
+              } else if (cand.ph == 1) {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cn.t1 + rn));
+              } else {
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cn.t2 + rn));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(cn.p + rn));
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) { sh.ring[slot] = cand; mb_arrive(&sh.full[slot]); }
+          pend[slot] = cand;
+          ++n_pub;
+          have = false;
+          progress = true;
+        }
+      }
+      // 4) stop: every published item released -> publish the stop item and leave
+      if (stop && !have && n_rel == n_pub) {
+        if (lane == 0) { Item z{}; z.go = 0; sh.ring[n_pub % NSLOT] = z; mb_arrive(&sh.full[n_pub % NSLOT]); }
+        break;
+      }
+      if (!progress) __nanosleep(64);
+    }
+    return;
+  }
+  // ------------------------------------------------------------ worker warps 0..7
+  for (int n = 0;; ++n) {
+    const int slot = n % NSLOT;
+    mb_wait(&sh.full[slot], (n / NSLOT) & 1);
+    const Item it = sh.ring[slot];
+    if (it.go == 0) break;
+    if (it.go == 1) {
+      if (it.ph < 3) {
+        const int jj = f.g0[it.g] + it.k / NT, tile = it.k % NT, j = jj + 1;
+        if (it.ph == 0) {
+          const double b = __ldcg(&a.cs[j].b);
+          rows_inv_item<T, true>(a, j, tile, it.i > 0 ? 1 : 0, b, sm, tb);
+        } else if (it.ph == 1) {
+          cols_item<T, true>(a, j, tile, sm, tb);
+        } else {
+          const double gw = rows_fwd_item<T, true>(a, j, tile, sm, tb);
+          if (lane == 0) a.part[(int64_t)j * a.stride + tile * NW + warp] = gw;
+        }
+      } else {
+        update_item(a, f, sh, slot, it.g, it.k);
+      }
+    }
+    worker_sync<NW * 32>();                           // item done by every worker (smem reuse, writes)
+    if (threadIdx.x == 0) mb_arrive(&sh.done[slot]);
+  }
+}
+}  // namespace flow
 
 // ---------------------------------------------------------------- setup: lane-packed mask
 // maskL[cv][lane] bit 2r / 2r+1 = mask at v-order rows 2n, 2n+1, n = ja + 64 r; bits 16+2r, 17+2r
@@ -565,6 +968,14 @@ cofem_status dct1k_setup(Ctx* c) {
   launch_end(c, KC_SETUP);
   set_attrs<float>();
   set_attrs<double>();
+  {   // dataflow probe kernel: dispenser state and rho' partials (allocated here: E-steps are captured)
+    if (cudaMalloc(&c->flow_state, sizeof(flow::State)) != cudaSuccess ||
+        cudaMalloc(&c->flow_part2, (size_t)c->m_cap * (c->Dp / VEC_TILE) * sizeof(double)) != cudaSuccess) {
+      c->err = "cudaMalloc flow state"; return COFEM_ERR_OOM;
+    }
+    const size_t smb = (size_t)8 * WREG * sizeof(float) + (size_t)TTOT * sizeof(cplx<float>);
+    cudaFuncSetAttribute(flow::k1k_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb);
+  }
   c->part_stride = std::max(c->part_stride, std::max(L, c->num_sms * 8));   // >= L row partials (pass C), grids
   return check_launch(c, "dct1k setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
@@ -628,6 +1039,52 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>, sm), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
   return check_launch(c, "dct1k apply") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
+// Column groups of the dataflow kernel: 8 (groups of 4 at K = 32: two halves of 4 groups, so
+// the four phase types of consecutive groups share the SMs), fewer when K is small
+int dct1k_flow_groups(const Ctx* c, int K) {
+  const int want = c->opt.probe_groups > 0 ? c->opt.probe_groups : 4;
+  return std::max(1, std::min(K, std::min(want, d1k::flow::MAXG)));
+}
+
+// The whole CG loop of the fp32 probe columns as one k1k_flow launch on `st` (the state, the
+// group s accumulators and the probe bits are ready; the mean column runs elsewhere).
+cofem_status dct1k_flow(Ctx* c, int K, int K_total, cudaStream_t st) {
+  using namespace d1k;
+  using namespace d1k::flow;
+  if (!c->flow_state) { c->err = "flow state not allocated"; return COFEM_ERR_CUDA; }   // dct1k_setup
+  Args f;
+  memset(&f, 0, sizeof f);
+  f.st = (State*)c->flow_state; f.K = K; f.U = c->opt.cg_iters; f.ntiles = (int)(c->Dp / VEC_TILE);
+  const int G = dct1k_flow_groups(c, K);
+  f.G = G;
+  for (int g = 0; g <= G; ++g) f.g0[g] = (int)((int64_t)K * g / G);
+  f.H = G >= 2 ? 2 : 1;
+  f.Gh = (G + f.H - 1) / f.H;
+  f.VS = std::max(f.ntiles, ((K + G - 1) / G) * NT);
+  f.step = (long long)f.H * f.Gh * f.VS;
+  f.total = f.step * (4LL * f.U + G - 1);
+  f.invK = 1.0 / (double)K_total;
+  for (int g = 0; g < G; ++g) f.s[g] = g ? c->gs[g] : c->s;
+  f.part2 = (double*)c->flow_part2;
+  f.bits = c->bits; f.wpc = c->Dp / 32;
+  f.dinvp = (const float*)c->dinvp;
+  DctArgs a = dct_args(c, K + 1, 0);
+  const size_t smb = (size_t)8 * WREG * sizeof(float) + (size_t)TTOT * sizeof(cplx<float>);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k1k_flow, FLOW_THREADS, smb);
+  // leave room for the concurrent fp64 mean column (an eighth of the SMs, as the per-pass path)
+#ifndef COFEM_FLOW_RESERVE
+#define COFEM_FLOW_RESERVE (c->num_sms / 8)
+#endif
+  const int sms = c->skip_mean ? c->num_sms : c->num_sms - std::max(0, (int)(COFEM_FLOW_RESERVE));
+  const int grid = std::max(1, sms * std::max(occ, 1));
+  if (cudaMemsetAsync(c->flow_state, 0, sizeof(State), st) != cudaSuccess) { c->err = "memset flow state"; return COFEM_ERR_CUDA; }
+  launch_begin(c, KC_DCT_FLOW, st);
+  k1k_flow<<<grid, FLOW_THREADS, smb, st>>>(a, f);
+  launch_end(c, KC_DCT_FLOW, st);
+  return check_launch(c, "k1k_flow") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
 cofem_status dct1k_apply(Ctx* c, int j0, int j1, int iter, bool dir, cudaStream_t st) {

@@ -94,7 +94,9 @@ def test_dense_apply_c3_shape_tensor_cores():
     (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), 0),                       # fast path
     (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4), 1),
     (synth.dct(64, 128, 2048, 40, K=8, U=1, T=1, seed=5), 0),                             # generic, rows != cols
-], ids=["dct1024_fast", "dct1024_generic", "dct64x128"])
+    (synth.dct(64, 128, 2048, 40, K=8, U=1, T=1, seed=5, convention=1), 0),               # Phi = S C2 (R11)
+    (synth.dct(1024, 1024, 262144, 100, K=8, U=1, T=1, seed=4, convention=1), 0),         # conv. 1, C4 shape
+], ids=["dct1024_fast", "dct1024_generic", "dct64x128", "dct64x128_conv1", "dct1024_conv1"])
 def test_dct_apply(w, path):
     e, eg = run_apply(w, 8, gaussian, path)
     assert e[0] <= 1e-12 and e[1:].max() <= 2e-6, (e[0], e[1:].max())

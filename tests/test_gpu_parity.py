@@ -71,6 +71,8 @@ SMALL = [
     synth.dct(128, 128, 4096, 163, K=8, U=200, T=3, seed=3),
     synth.circconv(5003, 64, 5, K=16, U=150, T=5, seed=0),              # ragged (prime) D
     synth.circconv(20000, 64, 20, K=8, U=150, T=3, seed=4),
+    synth.dct(64, 64, 1024, 41, K=8, U=150, T=4, seed=6, convention=1, name="dct_64x64_conv1"),   # Phi = S C2
+    synth.dct(32, 128, 1024, 40, K=6, U=150, T=3, seed=7, convention=1, name="dct_32x128_conv1"),
 ]
 
 
@@ -483,3 +485,17 @@ def test_dense_device_phi_is_borrowed():
         else:   # SIMT path: same fp32-class accuracy, different kernels
             assert rel(got[0], ref[0]) <= 1e-6 and rel(got[1], ref[1]) <= 1e-4
         buf[:, w.D:] = 0.0   # the padding is never read (NaN there would have propagated)
+
+
+def test_c4_shape_convention1_estep1_closed_form():
+    """DCT convention 1 (Phi = S C2, BASELINE config 4's literal "rows of DCT-II", reading R11) at
+    the C4 shape (1024 x 1024, N = 2^18; generic passes): E-step 1 against the closed form
+    mu = b0/(beta+1), x_k = p_k - beta/(beta+1) Phi^T Phi p_k, element by element."""
+    from parity_util import check
+    w = synth.dct(1024, 1024, 262144, 10485, K=8, U=200, T=1, seed=0, convention=1, name="C4_conv1")
+    ctx = ctx_of(w)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 0, 0)
+    P = rademacher_probes(w.D, w.K, 0, 0)
+    emu, es, _ = cf.masked_dct_estep1(w.rows, w.cols, w.obs_idx, w.y, w.beta, P, convention=1)
+    check("mu", mu, emu, 1e-4)
+    check("s", s, es, 1e-4, 1e-3)

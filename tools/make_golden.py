@@ -20,6 +20,14 @@ Storage: D-vectors at D >= 2^20 are stored as float32 (the bars are 1e-4 / 1e-3,
 except alpha_in, which is an INPUT and is stored exactly (fp64); support bits are computed in fp64.
 
     python tools/make_golden.py CASE [CASE ...]
+    python tools/make_golden.py --slim      # drop the arrays the tests do not read (repo size)
+
+Rounding sensitivity (cases <case>_pert, meta only): the oracle against ITSELF when its input is
+perturbed at the rounding level -- alpha times (1 + 1e-15 r), r = +-1 seeded -- once for the
+steady-state E-step (alpha_in) and once for the whole K = 4 EM from alpha = 1.  Where U leaves the
+CG unconverged the iterate amplifies rounding, so two correct fp64 implementations that differ only
+in summation order differ by about this much; the GPU tests use it as the floor of their bars
+(reading R20).
 """
 import json
 import os
@@ -87,8 +95,72 @@ def em_case(case, w, K, U, T, seed=0, extra_K=None):
              mu=vec(mu2, w.D), s=vec(s2, w.D), support=np.packbits(support(mu2)))
 
 
+def slim():
+    """Keep only what tests/test_gpu_fullcfg.py reads: the steady-state cases do not need their
+    E-step-1 vectors, and C5s_k16 shares C5s_ss's alpha_in (the same oracle alpha_5)."""
+    for name in sorted(os.listdir(OUT)):
+        path = os.path.join(OUT, name)
+        f = np.load(path)
+        arrays = {k: f[k] for k in f.files if k != "meta"}
+        meta = json.loads(str(f["meta"]))
+        drop = []
+        if name.endswith("_ss.npz"):
+            drop = ["mu1", "s1"]
+        if name.endswith("_k16.npz"):
+            drop = ["alpha_in"]
+            meta["alpha_in_from"] = meta.get("from_case")
+        drop = [k for k in drop if k in arrays]
+        if drop:
+            for k in drop:
+                arrays.pop(k)
+            np.savez_compressed(path, meta=json.dumps(meta), **arrays)
+            print("slimmed", name, "dropped", drop)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def elem(a, b):
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+def pert_case(case):
+    """Oracle vs oracle at a 1e-15 relative perturbation of alpha (see the module docstring)."""
+    base = case[:-len("_pert")]
+    w = workload(base)
+    f = np.load(os.path.join(OUT, base + ".npz"))
+    meta = json.loads(str(f["meta"]))
+    K, U, T, seed = meta["K"], meta["U"], meta["T"], meta["seed"]
+    op = op_of(w)
+    r = np.random.default_rng(12345).choice([-1.0, 1.0], size=w.D)
+    a_in = f["alpha_in"] * (1.0 + 1e-15 * r)
+    t0 = time.time()
+    mu_p, s_p, _ = estep(op, w.y, w.beta, a_in, K, seed, T - 1, U)
+    # the stored steady-state result (float32 at D >= 2^20) against the perturbed fp64 one
+    out = {"workload": w.name, "K": K, "U": U, "T": T, "perturbation": "alpha * (1 + 1e-15 r), r = +-1",
+           "estep_mu_rel": rel(mu_p, f["mu"]), "estep_s_rel": rel(s_p, f["s"]),
+           "estep_mu_elem": elem(mu_p, f["mu"]), "estep_s_elem": elem(s_p, f["s"])}
+    a_em, mu_em, s_em = cofem_em(op, w.y, w.beta, T, K, seed, U, alpha_init=np.ones(w.D) * (1.0 + 1e-15 * r))
+    from oracle.cofem import mstep
+    a_ref = mstep(f["mu"].astype(np.float64), f["s"].astype(np.float64))
+    out.update({"em_inv_alpha_rel": rel(1 / a_em, 1 / a_ref), "em_mu_rel": rel(mu_em, f["mu"]),
+                "em_inv_alpha_elem": elem(1 / a_em, 1 / a_ref), "em_mu_elem": elem(mu_em, f["mu"]),
+                "em_support_flips": int(np.sum(support(mu_em) != np.unpackbits(f["support"])[:w.D].astype(bool))),
+                "seconds": time.time() - t0})
+    save(case, out)
+    print(case, json.dumps(out), flush=True)
+
+
 def main(cases):
+    if cases == ["--slim"]:
+        return slim()
     for case in cases:
+        if case.endswith("_pert"):
+            pert_case(case)
+            continue
         w = workload(case)
         print(case, w.name, flush=True)
         if case == "C2_full":

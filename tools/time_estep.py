@@ -14,9 +14,12 @@ w = synth.preset(sys.argv[1] if len(sys.argv) > 1 else "C4")
 if os.environ.get("TIME_K"):          # emulate one rank of a probe-parallel run (K / world probes)
     w.K = int(os.environ["TIME_K"])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+kw = {"probe_groups": int(os.environ["TIME_GROUPS"])} if os.environ.get("TIME_GROUPS") else {}
+if os.environ.get("TIME_NOGRAPH"):
+    kw["use_graph"] = False
 if os.environ.get("TIME_U"):          # CG iterations per E-step (use with an existing alpha file)
     w.U = int(os.environ["TIME_U"])
-ctx = Context.from_workload(w, max_probes=w.K)
+ctx = Context.from_workload(w, max_probes=w.K, **kw)
 alpha = torch.ones(w.D, dtype=torch.float64, device="cuda")
 mu, s = torch.empty_like(alpha), torch.empty_like(alpha)
 ap = sys.argv[3] if len(sys.argv) > 3 else None
