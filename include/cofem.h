@@ -118,6 +118,12 @@ typedef struct {
    *     broadcasts mu = x0 from rank 0; every rank returns the same mu, s and alpha.  max_probes is
    *     the per-rank capacity (>= ceil(K / world) + 1). */
   int32_t dist_mode;
+  /* NEXT-1 (reading R20, P:98 leaves the initial guess open): 1 =
+   * inside cofem_em, every E-step after the call's first starts the mean system's CG from the
+   * previous E-step's mu (x0 = mu_prev, r0 = b0 - A mu_prev: one extra mean-column apply per
+   * E-step), the probes from zero (they are fresh); the freeze threshold stays relative to
+   * b0^T M^-1 b0.  0 (default): X0 = 0 every E-step (R4).  Not in the sharded modes. */
+  int32_t warm_start;
 } cofem_options;
 
 /* NCCL unique id for cofem_options.nccl_id (call on one rank, broadcast the 128 bytes).

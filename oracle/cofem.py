@@ -25,6 +25,10 @@ Readings of silent/ambiguous passages:
       rho_j <= eps^2 rho_j(0) with rho = r^T M^-1 r (plain CG: ||r_j|| <= eps ||b_j||); once
       every column is frozen the Frobenius criterion holds.  rtol = 0: fixed U (R5).
   R9  Algorithm 1 returns alpha after the last M-step and mu, s of the last E-step
+  R20 (NEXT-1, optional) warm start: the paper's initial guess is unstated (SPEC S:254-256
+      lists warm starts as unvalidated); with warm_start the mean system's CG starts from the
+      previous E-step's mu (x = mu_prev, r = b0 - A mu_prev), the probes from 0 (they are fresh),
+      and rho0 stays b^T M^-1 b so the freeze threshold is relative to b.  Off by default (R4).
 """
 import numpy as np
 
@@ -44,11 +48,14 @@ class PCGReport:
         self.rho_hist = []                                # per-iteration rho (recursive residual^2, M-norm)
 
 
-def pcg(apply_A, B, diag, U, precond=True, tau=FREEZE_TAU):
+def pcg(apply_A, B, diag, U, precond=True, tau=FREEZE_TAU, X0=None):
     """Jacobi-preconditioned CG on every column of B, column-independently (R3-R6).
 
     Per column j, the textbook PCG recurrence:
         x = 0, r = b, z = M^-1 r, p = z, rho = r^T z, rho0 = rho
+    (X0 given -- reading R20, NEXT-1 warm start: x = x0, r = b - A x0, and rho0 = b^T M^-1 b, the
+    cold-start value, so the freeze threshold stays relative to b as in the paper's criterion
+    ||A X - B||_F / ||B||_F < eps)
         repeat U times (skipping frozen columns):
             q = A p,  gamma = p^T q
             freeze if !(gamma > 0) or !(rho > tau rho0) or non-finite
@@ -59,12 +66,16 @@ def pcg(apply_A, B, diag, U, precond=True, tau=FREEZE_TAU):
     B = np.asarray(B, dtype=np.float64)
     D, m = B.shape
     minv = 1.0 / diag if precond else np.ones(D)
-    X = np.zeros((D, m))
-    R = B.copy()
+    rho0 = np.sum(B * (B * minv[:, None]), axis=0)
+    if X0 is None:
+        X = np.zeros((D, m))
+        R = B.copy()
+    else:
+        X = np.asarray(X0, dtype=np.float64).copy()
+        R = B - apply_A(X)
     Z = R * minv[:, None]
     P = Z.copy()
     rho = np.sum(R * Z, axis=0)
-    rho0 = rho.copy()
     active = np.ones(m, dtype=bool)
     rep = PCGReport(m)
     for i in range(U):
@@ -113,7 +124,7 @@ def tau_of(rtol):
     return max(FREEZE_TAU, float(rtol) ** 2)
 
 
-def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=False, rtol=0.0):
+def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=False, rtol=0.0, mu0=None):
     """Simplified E-step (Alg. 1 lines 3-7; Eq. 6-7).
 
     B = [b0 | p_1 .. p_K]  (R2),  X = LinearSolver(A, B) (P:136),
@@ -125,7 +136,11 @@ def estep(op, y, beta, alpha, K, seed, t, U, precond=True, k_offset=0, return_x=
     diag = jacobi_diag(op, beta, alpha)
     Pk = rademacher_probes(op.D, K, seed, t, k_offset)
     B = np.concatenate([b0[:, None], Pk], axis=1)
-    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), B, diag, U, precond, tau=tau_of(rtol))
+    X0 = None
+    if mu0 is not None:              # R20 (NEXT-1): warm start of the mean system only (fresh probes)
+        X0 = np.zeros_like(B)
+        X0[:, 0] = mu0
+    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), B, diag, U, precond, tau=tau_of(rtol), X0=X0)
     if rep.nonfinite.any():
         raise FloatingPointError("numerical breakdown in column %d" % int(np.argmax(rep.nonfinite)))
     mu = X[:, 0]
@@ -141,14 +156,17 @@ def mstep(mu, s, den_floor=DEN_FLOOR, alpha_max=ALPHA_MAX):
     return np.minimum(1.0 / den, alpha_max)
 
 
-def cofem_em(op, y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True, trace=None, rtol=0.0):
+def cofem_em(op, y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True, trace=None, rtol=0.0,
+             warm_start=False):
     """Algorithm 1: alpha <- 1; for t in 1..T: E-step with fresh probes
     (probe counter t0 + t), M-step.  Returns (alpha_T, mu, s) where mu, s are
-    from the last E-step (R9)."""
+    from the last E-step (R9).  warm_start (R20, NEXT-1): every E-step after the first
+    starts the mean system's CG from the previous E-step's mu."""
     alpha = np.ones(op.D) if alpha_init is None else np.asarray(alpha_init, dtype=np.float64).copy()
     mu = s = None
     for t in range(t0, t0 + T):
-        mu, s, _ = estep(op, y, beta, alpha, K, seed, t, U, precond, rtol=rtol)
+        mu, s, _ = estep(op, y, beta, alpha, K, seed, t, U, precond, rtol=rtol,
+                         mu0=mu if (warm_start and mu is not None) else None)
         alpha = mstep(mu, s)
         if trace is not None:
             trace.append((alpha.copy(), mu.copy(), s.copy()))

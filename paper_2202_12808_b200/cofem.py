@@ -43,7 +43,8 @@ class _Options(ctypes.Structure):
                 ("alpha_max", ctypes.c_double), ("probe_precision", ctypes.c_int32),
                 ("max_probes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("cg_rtol", ctypes.c_double), ("apply_path", ctypes.c_int32),
-                ("probe_groups", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("dist_mode", ctypes.c_int32)]
+                ("probe_groups", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("dist_mode", ctypes.c_int32),
+                ("warm_start", ctypes.c_int32)]
 
 
 class _Report(ctypes.Structure):
@@ -162,7 +163,7 @@ class Context:
     def __init__(self, kind, N, D, y, beta, phi=None, rows=0, cols=0, obs_idx=None, convention=0, taps=None,
                  cg_iters=100, precond=1, probe_precision=0, max_probes=32, den_floor=1e-12, alpha_max=1e12,
                  stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None, cg_rtol=0.0, apply_path=0,
-                 probe_groups=0, use_graph=True, dist_mode=0, ld=None):
+                 probe_groups=0, use_graph=True, dist_mode=0, ld=None, warm_start=False):
         """Multi-GPU; nccl_id = get_unique_id() from one rank, broadcast to all.
         dist_mode 0 with nccl_id: column-sharded dense / D-sharded conv -- phi (or y) holds this
         rank's slice [d_offset, d_offset + D) of D_global; the library all-reduces W and the column
@@ -193,6 +194,7 @@ class Context:
         opt.cg_rtol = float(cg_rtol)
         opt.apply_path, opt.probe_groups = int(apply_path), int(probe_groups)
         opt.use_graph, opt.dist_mode = int(bool(use_graph)), int(dist_mode)
+        opt.warm_start = int(bool(warm_start))
         if nccl_id is not None:
             self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opt.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)

@@ -103,6 +103,7 @@ struct VecArgs {
   double tau;       // freeze threshold on rho / rho0 (ColState::tau)
   int uchunks;      // k_update: probe columns split into uchunks chunks per D tile (1 = all in one item)
   int mean_grid;    // k_update: CTAs [0, mean_grid) update the mean column, tile stride mean_grid
+  int warm;         // k_init: the mean column starts from x0 (= mu of the previous E-step; q0 = A x0)
   double* s_part; unsigned* tile_cnt;
 };
 
@@ -147,7 +148,7 @@ template <> __device__ __forceinline__ void st8<double>(double* p, const double 
 
 // Per-CTA reduction scratch: red[warp][column]; only warp w writes row w (deterministic).
 struct VecShared {
-  double red[VEC_THREADS / 32][MAXM];
+  double red[VEC_THREADS / 32][MAXM + 1];   // + k_init's warm-start slot
   double a[MAXM];
   int act[MAXM];
   bool last;
@@ -183,7 +184,7 @@ template <typename TP>
 __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
   __shared__ VecShared sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = threadIdx.x; j < a.m; j += blockDim.x)
+  for (int j = threadIdx.x; j <= a.m; j += blockDim.x)
     for (int w = 0; w < VEC_THREADS / 32; ++w) sh.red[w][j] = 0.0;
   __syncthreads();
   const int64_t ntiles = a.Dp / VEC_TILE;
@@ -207,13 +208,28 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
       st8(a.alphap + d0, ap);
     }
     double z8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    st8(a.s + d0, z8); st8(a.x0 + d0, z8);
-    double p8[8], acc = 0.0;
+    st8(a.s + d0, z8);
+    double p8[8], acc = 0.0, acc_b = 0.0;
+    if (a.warm) {                  // R20: r0 = b0 - A x0 (q0 holds A x0); rho0 stays b0^T M^-1 b0
+      double q8[8];
+      ld8(a.q0 + d0, q8);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        acc_b += bb[e] * (dv[e] * bb[e]);
+        bb[e] = bb[e] - q8[e];
+      }
+    } else {
+      st8(a.x0 + d0, z8);
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) { p8[e] = dv[e] * bb[e]; acc += bb[e] * p8[e]; }
     st8(a.r0 + d0, bb); st8(a.p0 + d0, p8);
     acc = warp_sum(acc);
     if (lane == 0) sh.red[warp][0] += acc;
+    if (a.warm) {
+      acc_b = warp_sum(acc_b);
+      if (lane == 0) sh.red[warp][a.m] += acc_b;          // spare slot m: the cold rho0 of column 0
+    }
     for (int k = 0; k < a.K; ++k) {
       uint32_t w = (a.bits[(int64_t)k * a.wpc + (d0 >> 5)] >> (d0 & 31)) & 0xffu;
       TP r[8], p[8];
@@ -233,12 +249,40 @@ __global__ void __launch_bounds__(VEC_THREADS) k_init(VecArgs<TP> a) {
   ColState* cs = a.cs;
   double* colsum = a.colsum;
   const double tau = a.tau;
-  vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs, colsum, tau](int j, double v) {
-    if (colsum) { colsum[j] = v; return; }
-    ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
-    c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0; c.tau = tau;
-    cs[j] = c;
-  });
+  if (!a.warm) {
+    vec_finish(sh, a.part, a.part_stride, a.counter, 0, a.m, [cs, colsum, tau](int j, double v) {
+      if (colsum) { colsum[j] = v; return; }
+      ColState c; c.rho = v; c.rho0 = v; c.gamma = 0; c.a = 0; c.b = 0;
+      c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0; c.tau = tau;
+      cs[j] = c;
+    });
+    return;
+  }
+  // warm start (R20; never sharded): columns [0, m) plus the spare slot m with column 0's cold
+  // rho0 = b0^T M^-1 b0, reduced by the warp that finishes column 0 (fixed order)
+  __syncthreads();
+  for (int j = threadIdx.x; j <= a.m; j += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < VEC_THREADS / 32; ++w) v += sh.red[w][j];
+    a.part[(int64_t)j * a.part_stride + blockIdx.x] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sh.last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!sh.last) return;
+  __threadfence();
+  for (int j = warp; j < a.m; j += VEC_THREADS / 32) {
+    const double v = reduce_partials(a.part + (int64_t)j * a.part_stride, gridDim.x);
+    const double v0 = j == 0 ? reduce_partials(a.part + (int64_t)a.m * a.part_stride, gridDim.x) : v;
+    if (lane == 0) {
+      ColState c; c.rho = v; c.rho0 = v0; c.gamma = 0; c.a = 0; c.b = 0;
+      c.frozen = 0; c.frozen_at = -1; c.nonfinite = 0; c.pad = 0; c.tau = tau;
+      cs[j] = c;
+    }
+  }
+  if (threadIdx.x == 0) *a.counter = 0u;
 }
 
 // a5: r -= a q; x0 += a0 p0; s += (a_k/K) p_k o P_k; z = M^-1 r; rho' = r^T z; then
@@ -480,6 +524,19 @@ __global__ void k_add_vec(int64_t n, double* __restrict__ a, const double* __res
     a[i] += b[i];
 }
 
+// Warm start (R20): p0 = x0 (the previous mu) for one apply of the mean column; the probe columns
+// are frozen for that apply (kernels skip them; k_init resets every column afterwards).
+__global__ void k_warm_prep(int64_t D, const double* __restrict__ x0, double* __restrict__ p0, ColState* cs, int m) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x)
+    p0[d] = x0[d];
+  if (blockIdx.x == 0)
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      ColState c; c.rho = 1.0; c.rho0 = 1.0; c.gamma = 0; c.a = 0; c.b = 0;
+      c.frozen = j > 0; c.frozen_at = j > 0 ? 0 : -1; c.nonfinite = 0; c.pad = 0; c.tau = FREEZE_TAU;
+      cs[j] = c;
+    }
+}
+
 // cofem_estep_probes: the mean system (column 0) is solved by another rank; freeze it at once.
 __global__ void k_freeze_col0(ColState* cs) {
   if (threadIdx.x == 0) { cs[0].frozen = 1; cs[0].frozen_at = 0; }
@@ -526,6 +583,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.colsum = c->sharded ? c->colsum : nullptr;
   a.tau = c->freeze_tau;
   a.uchunks = c->upd_chunks; a.s_part = c->s_part; a.tile_cnt = c->tile_cnt; a.mean_grid = c->vec_grid;
+  a.warm = c->warm_now ? 1 : 0;
   return a;
 }
 
@@ -728,6 +786,17 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     launch_end(c, KC_PROBES);
     if (check_launch(c, "k_probe_bits")) return COFEM_ERR_CUDA;
   }
+  if (c->warm_now) {   // R20 warm start: q0 = A x0 (x0 = mu of the previous E-step), then k_init uses it
+    k_warm_prep<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, c->x0, c->p0, c->cs, m);
+    if (check_launch(c, "k_warm_prep")) return COFEM_ERR_CUDA;
+    cofem_status st;
+    if (c->fast1k) st = dct1k_apply(c, 0, 1, 0, false, c->stream);
+    else if (c->fast_conv) st = conv_fft_apply(c, 0, 1, 0, false, c->stream);
+    else if (c->kind == COFEM_OP_DCT2_MASKED) st = dct_apply(c, m, 0, false);
+    else if (c->kind == COFEM_OP_DENSE) st = dense_apply(c, m, 0);
+    else st = conv_apply(c, m, 0);
+    if (st != COFEM_OK) return st;
+  }
   launch_begin(c, KC_INIT);
   if (c->probe64) k_init<double><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
   else k_init<float><<<c->vec_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
@@ -798,7 +867,8 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   CK(cudaStreamWaitEvent(c->work, c->ev_in, 0));
   c->stream = c->work;
   cofem_status st = COFEM_OK;
-  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total || c->graph_skip != (int)c->skip_mean) {
+  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total || c->graph_skip != (int)c->skip_mean ||
+      c->graph_warm != (int)c->warm_now) {
     if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
     const int64_t l0 = c->launches;
     cudaGraph_t g = nullptr;
@@ -817,7 +887,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
       if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
       return st;
     }
-    c->graph_K = K; c->graph_Kt = K_total; c->graph_skip = (int)c->skip_mean;
+    c->graph_K = K; c->graph_Kt = K_total; c->graph_skip = (int)c->skip_mean; c->graph_warm = (int)c->warm_now;
   }
   cudaError_t e = cudaGraphLaunch(c->graph_exec, c->work);
   c->launches += c->graph_launches;
@@ -934,7 +1004,7 @@ void cofem_default_options(cofem_options* o) {
   o->probe_precision = 0; o->max_probes = 32;
   o->rank = 0; o->world = 1; o->nccl_id = nullptr;
   o->cg_rtol = 0.0;
-  o->apply_path = 0; o->probe_groups = 0; o->use_graph = 1; o->dist_mode = 0;
+  o->apply_path = 0; o->probe_groups = 0; o->use_graph = 1; o->dist_mode = 0; o->warm_start = 0;
 }
 
 const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
@@ -1004,6 +1074,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (opt->apply_path < 0 || opt->apply_path > 1) { c->err = "apply_path must be 0 or 1"; return COFEM_ERR_INVALID; }
   if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 8]"; return COFEM_ERR_INVALID; }
   if (opt->dist_mode < 0 || opt->dist_mode > 1) { c->err = "dist_mode must be 0 or 1"; return COFEM_ERR_INVALID; }
+  if (opt->warm_start < 0 || opt->warm_start > 1) { c->err = "warm_start must be 0 or 1"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
   c->freeze_tau = std::max(FREEZE_TAU, opt->cg_rtol * opt->cg_rtol);
   if (opt->dist_mode == 1) {                    // probe-parallel (comm.cu: all-reduce of s, broadcast of mu)
@@ -1021,6 +1092,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
       c->err = "sharded mode: d_offset must be a multiple of 128 and d_offset + D <= D_global"; return COFEM_ERR_INVALID;
     }
     if (opt->probe_precision) { c->err = "sharded mode: fp32 probes only"; return COFEM_ERR_UNSUPPORTED; }
+    if (opt->warm_start) { c->err = "sharded mode: no warm start"; return COFEM_ERR_UNSUPPORTED; }
     c->sharded = true; c->d_offset = op->d_offset; c->D_global = op->D_global;
     c->rank = opt->rank; c->world = opt->world;
   }
@@ -1155,7 +1227,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   cudaStreamSynchronize(c->stream);
   if (y_tmp) cudaFree(y_tmp);
   if (st != COFEM_OK) return st;
-  ALLOC(c->part, (size_t)c->m_cap * c->part_stride);
+  ALLOC(c->part, (size_t)(c->m_cap + 1) * c->part_stride);   // + k_init's warm-start slot
   c->pp_mean_cost = (c->fast1k || c->fast_conv) ? 2.0 : 0.0;
   if (c->sharded) {
     ALLOC(c->colsum, MAXM);
@@ -1348,8 +1420,11 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
   for (int i = 0; i < iters; ++i) {
     CK(cudaEventRecord(c->ev0, c->stream));
     int m = K + 1;
-    if (c->pp) { int kl; if ((st = estep_pp(c, K, seed, t0 + i, &kl))) return st; m = kl + 1; }
-    else if ((st = estep_device(c, K, seed, t0 + i, 0, K))) return st;
+    c->warm_now = c->opt.warm_start && i > 0;          // R20: from the previous E-step's mu (x0)
+    if (c->pp) { int kl; st = estep_pp(c, K, seed, t0 + i, &kl); m = kl + 1; }
+    else st = estep_device(c, K, seed, t0 + i, 0, K);
+    c->warm_now = false;
+    if (st) return st;
     const bool lastit = i == iters - 1;
     launch_begin(c, KC_FINAL);
     // the M-step writes the next alpha in place (the E-step state no longer needs it)

@@ -81,7 +81,8 @@ struct Ctx {
   int64_t sup_count = 0, sup_adjacent = 0;
   double sup_max = 0, sup_min_margin = 0;
   cudaGraphExec_t graph_exec = nullptr; // captured E-step (cofem.cu estep_device)
-  int graph_K = -1, graph_Kt = -1, graph_skip = -1;
+  int graph_K = -1, graph_Kt = -1, graph_skip = -1, graph_warm = -1;
+  bool warm_now = false;                // this E-step starts the mean column from x0 (R20)
   bool skip_mean = false;          // cofem_estep_probes: column 0 frozen from the start (mean owned elsewhere)
   int64_t graph_launches = 0;
   void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu

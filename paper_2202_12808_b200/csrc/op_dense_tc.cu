@@ -349,6 +349,10 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {        // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
             const uint64_t dbh = desc_k_sw128(bh + kk * 32);
+#ifdef COFEM_TC_EXP_1XTF32   // accuracy experiment (SURVEY §8(d) note 3): one tf32 MMA, no hi/lo corrections
+            mma_ts_e(d, ahi + kk * 8, dbh, idesc, (h | kk) != 0);
+            (void)alo; (void)bl; (void)fuse; (void)idesc2;
+#else
             if (fuse) {
               mma_ts_e(d, ahi + kk * 8, dbh, idesc2, (h | kk) != 0);
             } else {
@@ -356,6 +360,7 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
               mma_ts_e(d, ahi + kk * 8, desc_k_sw128(bl + kk * 32), idesc, 1);
             }
             mma_ts_e(d, alo + kk * 8, dbh, idesc, 1);
+#endif
           }
         }
         mma_commit_e(&bs.pair_done[p & 3]);             // stages, A buffers and chunk p: all released here

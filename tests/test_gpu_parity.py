@@ -499,3 +499,25 @@ def test_c4_shape_convention1_estep1_closed_form():
     emu, es, _ = cf.masked_dct_estep1(w.rows, w.cols, w.obs_idx, w.y, w.beta, P, convention=1)
     check("mu", mu, emu, 1e-4)
     check("s", s, es, 1e-4, 1e-3)
+
+
+@pytest.mark.parametrize("w", [SMALL[1], SMALL[2], SMALL[5], SMALL[7],
+                               synth.dct(1024, 1024, 262144, 400, K=3, U=30, T=3, seed=3, name="dct1024_fast_U30")],
+                         ids=lambda w: w.name)
+def test_warm_start_em_matches_oracle(w):
+    """NEXT-1 warm start (reading R20, cofem_options.warm_start): EM iterations after the first start
+    the mean system's CG from the previous mu, on every operator path, against the oracle's
+    cofem_em(warm_start=True): north_star EM bars, and parity mode to 1e-7."""
+    from parity_util import check
+    T = 2        # E-step 2 is warm; longer unconverged fp32 runs drift at 1e-3 (fast path, U = 30: 6e-3 at
+                 # T = 3 while parity mode matches the warm oracle to 3e-11: tools/warm_dbg.py)
+    oa, omu, _ = cofem_em(op_of(w), w.y, w.beta, T, w.K, 4, w.U, warm_start=True)
+    a, mu, _ = gpu_em(ctx_of(w, warm_start=True), w, T, w.K, 4)
+    check("1/alpha", 1 / a, 1 / oa, 1e-3, 1e-2)
+    check("mu", mu, omu, 1e-3, 1e-2)
+    a, mu, _ = gpu_em(ctx_of(w, warm_start=True, probe_precision=1), w, T, w.K, 4)
+    check("1/alpha parity", 1 / a, 1 / oa, 1e-7, 1e-6)
+    check("mu parity", mu, omu, 1e-7, 1e-6)
+    a0, mu0, _ = gpu_em(ctx_of(w), w, 1, w.K, 4)            # the first E-step of a call is cold
+    a1, mu1, _ = gpu_em(ctx_of(w, warm_start=True), w, 1, w.K, 4)
+    assert np.array_equal(a0, a1) and np.array_equal(mu0, mu1)

@@ -327,3 +327,52 @@ def test_cofem_nrmse_tracks_exact_em():
 
 def test_support_threshold():
     assert list(support(np.array([1.0, -0.002, 0.0005, 0.0]))) == [True, True, False, False]
+
+
+# ---------------------------------------------------------------- R20: warm start (NEXT-1)
+def test_warm_start_from_zero_is_the_cold_start():
+    w = synth.dense(30, 80, 4, K=3, U=20, T=1, seed=3)
+    op = DenseOp(w.phi)
+    a = np.random.default_rng(1).uniform(0.5, 2.0, w.D)
+    m1, s1, _ = estep(op, w.y, w.beta, a, 3, 2, 0, 20)
+    m2, s2, _ = estep(op, w.y, w.beta, a, 3, 2, 0, 20, mu0=np.zeros(w.D))
+    assert np.array_equal(m1, m2) and np.array_equal(s1, s2)
+
+
+def test_warm_start_at_the_solution_stops_at_once():
+    """x0 = A^-1 b: the residual is ~0, so the mean column freezes in its first iteration (R5 with
+    rho0 = b^T M^-1 b) and mu stays the exact solution (direct solve)."""
+    w = synth.dense(30, 80, 4, K=2, U=20, T=1, seed=4)
+    op = DenseOp(w.phi)
+    a = np.random.default_rng(2).uniform(0.5, 2.0, w.D)
+    A = w.beta * op.phi.T @ op.phi + np.diag(a)
+    b0 = w.beta * op.phi.T @ w.y.astype(np.float64)
+    xs = np.linalg.solve(A, b0)
+    mu, _, rep = estep(op, w.y, w.beta, a, 2, 1, 0, 20, mu0=xs)
+    assert rel(mu, xs) < 1e-12
+    assert rep.frozen_at[0] <= 1
+
+
+def test_warm_start_converges_to_the_same_solution():
+    """Warm-started CG converges to A^-1 b like the cold start (direct solve), and a good warm
+    start reaches a given accuracy in fewer iterations."""
+    w = synth.dense(40, 120, 6, K=2, U=60, T=1, seed=5)
+    op = DenseOp(w.phi)
+    a = np.random.default_rng(3).uniform(0.2, 5.0, w.D)
+    A = w.beta * op.phi.T @ op.phi + np.diag(a)                 # condition number ~1e5
+    xs = np.linalg.solve(A, w.beta * op.phi.T @ w.y.astype(np.float64))
+    near = xs * (1.0 + 1e-3 * np.random.default_rng(4).standard_normal(w.D))
+    mu_w, _, _ = estep(op, w.y, w.beta, a, 2, 1, 0, 300, mu0=near)
+    assert rel(mu_w, xs) < 1e-10
+    for U in (5, 20, 60, 120):          # measured: cold 0.69 / 0.61 / 1.0e-2 / 2.4e-5, warm 1e-3 .. 7e-8
+        e_cold = rel(estep(op, w.y, w.beta, a, 2, 1, 0, U)[0], xs)
+        e_warm = rel(estep(op, w.y, w.beta, a, 2, 1, 0, U, mu0=near)[0], xs)
+        assert e_warm < 1e-2 * e_cold, (U, e_cold, e_warm)
+
+
+def test_warm_start_em_first_estep_is_cold():
+    w = synth.dense(30, 80, 4, K=3, U=15, T=1, seed=6)
+    op = DenseOp(w.phi)
+    a1, m1, s1 = cofem_em(op, w.y, w.beta, 1, 3, 5, 15)
+    a2, m2, s2 = cofem_em(op, w.y, w.beta, 1, 3, 5, 15, warm_start=True)
+    assert np.array_equal(a1, a2) and np.array_equal(m1, m2)
