@@ -88,7 +88,7 @@ def paper_dense(D, f, seed=0, sigma=0.005, K=20, U=400, T=50):
                     phi=phi, seed=seed)
 
 
-def dct(rows, cols, N, nnz, K, U, T, seed=0, convention=0, name=None):
+def dct(rows, cols, N, nnz, K, U, T, seed=0, convention=0, name=None, sigma=SIGMA):
     """Orthonormal 2D DCT on a rows x cols grid, uniform random N-pixel mask (config 4)."""
     rng = np.random.default_rng(seed)
     D = rows * cols
@@ -96,9 +96,19 @@ def dct(rows, cols, N, nnz, K, U, T, seed=0, convention=0, name=None):
     z = _sparse_z(rng, D, nnz)
     img = z.reshape(rows, cols)
     pix = sfft.idctn(img, norm="ortho") if convention == 0 else sfft.dctn(img, norm="ortho")
-    y = (pix.ravel()[obs] + SIGMA * rng.standard_normal(N)).astype(np.float32)
-    return Workload(name or "dct_%dx%d" % (rows, cols), "dct2_masked", N, D, K, U, T, BETA, y, z,
+    y = (pix.ravel()[obs] + sigma * rng.standard_normal(N)).astype(np.float32)
+    return Workload(name or "dct_%dx%d" % (rows, cols), "dct2_masked", N, D, K, U, T, 1.0 / sigma ** 2, y, z,
                     rows=rows, cols=cols, obs_idx=obs, convention=convention, seed=seed)
+
+
+def paper_dct(p, seed=0, frac=0.04, K=20, U=400, T=30):
+    """The paper's structured setup (§4.2): D = 2^p DCT coefficients on a 2^floor(p/2) x
+    2^ceil(p/2) grid (reading R11: 2D), N = D/4 observed pixels, d = floor(frac D) N(0, 1)
+    coefficients; the noise level is not restated in §4.2, so §4.1's sigma = 0.005 (beta = 1/sigma^2)."""
+    rows, cols = 1 << (p // 2), 1 << (p - p // 2)
+    D = rows * cols
+    return dct(rows, cols, D // 4, int(math.floor(frac * D)), K=K, U=U, T=T, seed=seed, sigma=0.005,
+               name="paper_dct_2^%d" % p)
 
 
 def circconv(D, ntaps, nnz, K, U, T, seed=0, name=None):
