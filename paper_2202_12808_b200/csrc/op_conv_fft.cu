@@ -56,9 +56,17 @@ template <typename T> __device__ __forceinline__ CCol<T> ccol(const ConvArgs& a,
   return {(const T*)a.P + o, (T*)a.Pn + o, (const T*)a.R + o, (const T*)a.dinvp, al, (T*)a.Q + o};
 }
 
+#ifndef COFEM_CONV_STASH
+#define COFEM_CONV_STASH 0   // 1: fp32 interior windows keep the updated p of their valid outputs in shared memory (3 CTAs/SM: C5 196 -> 214 ms, not kept)
+#endif
+constexpr int STASH = 448;                 // complex points n in [32, 480): window positions [64, 960)
 template <typename T>
 #ifndef COFEM_CONV_MINB
+#if COFEM_CONV_STASH
+#define COFEM_CONV_MINB (sizeof(T) == 4 ? 3 : 2)   // fp32: 3 CTAs per SM (shared memory: the p stash)
+#else
 #define COFEM_CONV_MINB (sizeof(T) == 4 ? 4 : 2)   // fp32: 64 registers, 4 CTAs per SM (C5 228 -> 210 -> 196 ms; the gamma partials sized by the launch, not MAXM, make the 4th CTA fit)
+#endif
 #endif
 __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs a, int j0, int dir) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -67,6 +75,8 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
   // tables in dynamic shared memory, sized by the launch's columns (not MAXM)
   __shared__ struct { int frozen[MAXM]; double b[MAXM]; } ci;
   double* gsm = reinterpret_cast<double*>(smraw + NW * WREG * sizeof(T) + TTOTC * sizeof(cplx<T>));
+  // fp32: per-warp stash of the window's updated p at its valid outputs (after the gamma partials)
+  float2* stash = reinterpret_cast<float2*>(gsm + NW * a.ncols) + (threadIdx.x >> 5) * STASH;
   int act = 0;
   for (int jj = threadIdx.x; jj < a.ncols; jj += blockDim.x) {
     const ColState c = a.cs[j0 + jj];
@@ -97,6 +107,10 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
     const int64_t o0 = blk * V, w0 = o0 - HALO;                         // outputs [o0, o0+V), window [w0, w0+1024)
     const int nvalid = (int)min((int64_t)V, a.D - o0);
     const bool fast = w0 >= 0 && w0 + L <= a.D;
+    // fp32 interior window with V valid outputs: p kept in the stash, 8-byte stores / alpha loads
+    const bool st2 = COFEM_CONV_STASH && sizeof(T) == 4 && fast && !a.halo && nvalid == V;
+    if (st2 && lane < 28)                                               // alpha of the outputs -> L2 (3.5 KB)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(c.al + o0 + 32 * lane));
     const T* hal = nullptr;                                             // this column's halo records (sharded)
     int64_t hside = 0;
     if (a.halo) {
@@ -147,8 +161,19 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
         if (sl) vb[r] = {x0, x1}; else va[r] = {x0, x1};
       }
     }
-    // the direction update is stored by the block that owns the position (valid outputs)
-    if (dir) {
+    if (st2) {                       // valid outputs: stash p (same lane reads it back), p_new as float2
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          const int n = (sl ? jb : ja) + 64 * r;
+          if (n >= 32 && n < 32 + STASH) {
+            const cplx<T> v = sl ? vb[r] : va[r];
+            stash[n - 32] = make_float2((float)v.x, (float)v.y);
+            if (dir) *reinterpret_cast<float2*>(c.pn + o0 + 2 * n - HALO) = make_float2((float)v.x, (float)v.y);
+          }
+        }
+    } else if (dir) {                // the direction update is stored by the block that owns the position
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -182,6 +207,23 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
     const T beta = (T)a.beta;
     const T* pcur = dir ? c.pn : c.p;                                   // p of this iteration (own block: just written)
     double g = 0.0;
+    if (st2) {                       // p from the stash, alpha / q as float2
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          const int n = (sl ? jb : ja) + 64 * r;
+          if (n >= 32 && n < 32 + STASH) {
+            const cplx<T> y = sl ? vb[r] : va[r];
+            const int64_t i = o0 + 2 * n - HALO;
+            const float2 pv = stash[n - 32];
+            const float2 av = *reinterpret_cast<const float2*>(c.al + i);
+            const float q0 = (float)beta * (float)y.x + av.x * pv.x, q1 = (float)beta * (float)y.y + av.y * pv.y;   // a3
+            *reinterpret_cast<float2*>(c.q + i) = make_float2(q0, q1);
+            g += (double)pv.x * (double)q0 + (double)pv.y * (double)q1;                                           // a4
+          }
+        }
+    } else
 #pragma unroll
     for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -261,7 +303,8 @@ template <typename T> static std::vector<cplx<T>> build_conv_tables(const std::v
 }
 
 template <typename T> static size_t smem_bytes(int ncols) {
-  return (size_t)NW * WREG * sizeof(T) + (size_t)TTOTC * sizeof(cplx<T>) + (size_t)NW * ncols * sizeof(double);
+  return (size_t)NW * WREG * sizeof(T) + (size_t)TTOTC * sizeof(cplx<T>) + (size_t)NW * ncols * sizeof(double) +
+         (COFEM_CONV_STASH && sizeof(T) == 4 ? (size_t)NW * STASH * sizeof(float2) : 0);
 }
 
 }  // namespace cfft
