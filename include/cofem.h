@@ -189,6 +189,19 @@ cofem_status cofem_mstep(cofem_ctx ctx, const double* mu, const double* s, doubl
 cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, int32_t t0,
                       const double* alpha_init, double* alpha_out, double* mu_out, double* s_out);
 
+/* NEXT-4 multi-task SBL (P:179 names the extension; reading R22 in DESIGN.md): L tasks
+ * y_l = Phi z_l + noise share Phi, beta and the prior precisions alpha.  Sigma is then shared, so
+ * the E-step solves A x = beta Phi^T y_l for every task mean and the K probes give one s; the
+ * M-step is alpha = 1 / (mean_l mu_l o mu_l + s) (floor / clamp as Eq. 8).  `iters` EM iterations
+ * (probe counter t0 + i) from alpha_init (NULL: ones).
+ *   Y:      L x N fp32, row l = task l's observations (host or device)
+ *   MU_out: L x D fp64, row l = task l's mu (last E-step); alpha_out, s_out: D fp64; any may be NULL
+ * L = 1 is cofem_em.  The context's own y (cofem_setup) is unchanged afterwards.
+ * Errors: COFEM_ERR_INVALID (L < 1, K), COFEM_ERR_UNSUPPORTED (sharded / probe-parallel contexts,
+ * warm_start). */
+cofem_status cofem_em_multi(cofem_ctx ctx, int32_t L, const float* Y, int32_t iters, int32_t K, uint64_t seed,
+                            int32_t t0, const double* alpha_init, double* alpha_out, double* MU_out, double* s_out);
+
 typedef struct {
   int32_t cols;                   /* K + 1 columns of the last E-step (column 0 = mean, R2) */
   int32_t cg_iters;               /* U */

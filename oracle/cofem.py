@@ -29,6 +29,11 @@ Readings of silent/ambiguous passages:
       lists warm starts as unvalidated); with warm_start the mean system's CG starts from the
       previous E-step's mu (x = mu_prev, r = b0 - A mu_prev), the probes from 0 (they are fresh),
       and rho0 stays b^T M^-1 b so the freeze threshold is relative to b.  Off by default (R4).
+  R22 (NEXT-4) multi-task SBL (P:179 names it, no procedure): L tasks y_l = Phi z_l + noise share
+      Phi, beta and alpha (z_l ~ N(0, diag(alpha)^-1)); Sigma is shared, so one batched solve of
+      A X = [beta Phi^T y_1 .. beta Phi^T y_L | p_1 .. p_K] gives mu_l and the same estimator s,
+      and maximising sum_l E[log p(z_l | alpha)] gives alpha = L / sum_l (mu_l^2 + s)
+      = 1 / (mean_l mu_l^2 + s).  L = 1 is Algorithm 1.
 """
 import numpy as np
 
@@ -177,3 +182,38 @@ def support(mu, rel=1e-3):
     """Recovered support |mu_d| > rel * max|mu| (BASELINE.json north_star; reading R16)."""
     mu = np.asarray(mu)
     return np.abs(mu) > rel * np.max(np.abs(mu))
+
+
+def estep_multi(op, Y, beta, alpha, K, seed, t, U, precond=True):
+    """Multi-task E-step (R22): B = [beta Phi^T y_1 .. beta Phi^T y_L | p_1 .. p_K] (the task means
+    first, then the probes, R2), one column-independent PCG (R3), mu_l = x_l,
+    s = (1/K) sum_k p_k o x_{L+k} (Eq. 6).  Y: N x L.  Returns (MU (D x L), s, report)."""
+    Y = np.asarray(Y, dtype=np.float64)
+    if Y.ndim == 1:
+        Y = Y[:, None]
+    L = Y.shape[1]
+    alpha = np.asarray(alpha, dtype=np.float64)
+    B0 = beta * op.apply_T(Y)
+    diag = jacobi_diag(op, beta, alpha)
+    Pk = rademacher_probes(op.D, K, seed, t)
+    X, rep = pcg(lambda V: gram_apply(op, beta, alpha, V), np.concatenate([B0, Pk], axis=1), diag, U, precond)
+    if rep.nonfinite.any():
+        raise FloatingPointError("numerical breakdown in column %d" % int(np.argmax(rep.nonfinite)))
+    return X[:, :L], np.mean(Pk * X[:, L:], axis=1), rep
+
+
+def mstep_multi(MU, s, den_floor=DEN_FLOOR, alpha_max=ALPHA_MAX):
+    """alpha = 1 / (mean_l mu_l o mu_l + s) (R22), floored / clamped as Eq. 8 (R7)."""
+    MU = np.asarray(MU, dtype=np.float64)
+    den = np.maximum(np.mean(MU * MU, axis=1) + s, den_floor)
+    return np.minimum(1.0 / den, alpha_max)
+
+
+def cofem_em_multi(op, Y, beta, T, K, seed, U, alpha_init=None, t0=0, precond=True):
+    """Multi-task Algorithm 1 (R22): returns (alpha_T, MU (D x L) and s of the last E-step)."""
+    alpha = np.ones(op.D) if alpha_init is None else np.asarray(alpha_init, dtype=np.float64).copy()
+    MU = s = None
+    for t in range(t0, t0 + T):
+        MU, s, _ = estep_multi(op, Y, beta, alpha, K, seed, t, U, precond)
+        alpha = mstep_multi(MU, s)
+    return alpha, MU, s

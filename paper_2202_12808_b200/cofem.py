@@ -73,6 +73,9 @@ SYMBOLS = [
                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     ("cofem_em", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32,
                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    ("cofem_em_multi", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]),
     ("cofem_last_report", ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(_Report)]),
     ("cofem_probe_split", ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
                                          ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
@@ -263,6 +266,15 @@ class Context:
                                    _ptr(alpha_init, np.float64, D, "alpha_init"),
                                    _ptr(alpha_out, np.float64, D, "alpha_out"),
                                    _ptr(mu_out, np.float64, D, "mu_out"), _ptr(s_out, np.float64, D, "s_out")))
+
+    def em_multi(self, Y, iters, K, seed, t0=0, alpha_init=None, alpha_out=None, MU_out=None, s_out=None):
+        """Multi-task EM (NEXT-4, reading R22): Y is L x N fp32 (row l = task l's y), MU_out L x D."""
+        D = self.D
+        L = int(Y.shape[0])
+        self._check(lib().cofem_em_multi(self._h, L, _ptr(Y, np.float32, L * self.N, "Y"), int(iters), int(K),
+                                         int(seed), int(t0), _ptr(alpha_init, np.float64, D, "alpha_init"),
+                                         _ptr(alpha_out, np.float64, D, "alpha_out"),
+                                         _ptr(MU_out, np.float64, L * D, "MU_out"), _ptr(s_out, np.float64, D, "s_out")))
 
     def report(self):
         r = _Report()

@@ -519,6 +519,24 @@ __global__ void k_support_count(int64_t D, const double* __restrict__ mu, double
   }
 }
 
+// Multi-task M-step (reading R22): alpha = 1 / (mean_l mu_l^2 + s), floored / clamped as Eq. 8 (R7).
+// MU: L task means, [L][Dp]; the sum runs over l in order (deterministic).
+__global__ void k_mstep_multi(int64_t D, int64_t Dp, int L, const double* __restrict__ MU, const double* __restrict__ s,
+                              double* __restrict__ alpha_out, double den_floor, double alpha_max) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    double den;
+    if (L == 1) {                     // exactly k_finalize's expression (L = 1 is Algorithm 1)
+      const double m = MU[d];
+      den = m * m + s[d];
+    } else {
+      double acc = 0.0;
+      for (int l = 0; l < L; ++l) { const double m = MU[(int64_t)l * Dp + d]; acc += m * m; }
+      den = acc / (double)L + s[d];
+    }
+    alpha_out[d] = fmin(1.0 / fmax(den, den_floor), alpha_max);
+  }
+}
+
 __global__ void k_add_vec(int64_t n, double* __restrict__ a, const double* __restrict__ b) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a[i] += b[i];
@@ -717,7 +735,7 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
       if ((st = apply(c, 0, 1, it, it > 0, ms)) != COFEM_OK) return st;
       update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, ms, KC_MEAN);
     }
-    for (int g = 0; g < G; ++g) {
+    for (int g = 0; g < G && m > 1; ++g) {          // m = 1: the mean system alone (R22)
       cudaStream_t gst = g ? c->gstream[g] : c->stream;
       unsigned* tk = g ? c->counters + 3 * MAXM + gj[g] : c->counters + MAXM;   // per-group tickets
       if ((st = apply(c, gj[g], gj[g + 1], it, it > 0, gst)) != COFEM_OK) return st;
@@ -780,11 +798,13 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   const int64_t nblk128 = c->Dp / 128;
   {
     int64_t n = (int64_t)K * nblk128;
-    launch_begin(c, KC_PROBES);
-    k_probe_bits<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->bits, c->Dp / 32, K, nblk128,
-                                                                      (const ProbeParams*)c->dparams);
-    launch_end(c, KC_PROBES);
-    if (check_launch(c, "k_probe_bits")) return COFEM_ERR_CUDA;
+    if (n > 0) {       // K = 0: the mean system alone (multi-task EM, R22)
+      launch_begin(c, KC_PROBES);
+      k_probe_bits<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(c->bits, c->Dp / 32, K, nblk128,
+                                                                        (const ProbeParams*)c->dparams);
+      launch_end(c, KC_PROBES);
+      if (check_launch(c, "k_probe_bits")) return COFEM_ERR_CUDA;
+    }
   }
   if (c->warm_now) {   // R20 warm start: q0 = A x0 (x0 = mu of the previous E-step), then k_init uses it
     k_warm_prep<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, c->x0, c->p0, c->cs, m);
@@ -867,9 +887,13 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   CK(cudaStreamWaitEvent(c->work, c->ev_in, 0));
   c->stream = c->work;
   cofem_status st = COFEM_OK;
-  if (!c->graph_exec || c->graph_K != K || c->graph_Kt != K_total || c->graph_skip != (int)c->skip_mean ||
-      c->graph_warm != (int)c->warm_now) {
-    if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+  Ctx::GraphSlot* gs = nullptr;
+  for (auto& s : c->gslot)
+    if (s.exec && s.K == K && s.Kt == K_total && s.skip == (int)c->skip_mean && s.warm == (int)c->warm_now) gs = &s;
+  if (!gs) {           // capture into the least recently used slot
+    gs = &c->gslot[0];
+    for (auto& s : c->gslot) if (s.used < gs->used) gs = &s;
+    if (gs->exec) { cudaGraphExecDestroy(gs->exec); gs->exec = nullptr; }
     const int64_t l0 = c->launches;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal);
@@ -877,20 +901,21 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
       st = estep_body(c, K, K_total);
       e = cudaStreamEndCapture(c->work, &g);
     }
-    if (e == cudaSuccess && st == COFEM_OK) e = cudaGraphInstantiate(&c->graph_exec, g, 0);
+    if (e == cudaSuccess && st == COFEM_OK) e = cudaGraphInstantiate(&gs->exec, g, 0);
     if (g) cudaGraphDestroy(g);
-    c->graph_launches = c->launches - l0;
+    gs->launches = c->launches - l0;
     c->launches = l0;
     if (e != cudaSuccess || st != COFEM_OK) {
       c->stream = user;
       if (st == COFEM_OK) { c->err = std::string("CUDA graph capture: ") + cudaGetErrorString(e); st = COFEM_ERR_CUDA; }
-      if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+      if (gs->exec) { cudaGraphExecDestroy(gs->exec); gs->exec = nullptr; }
       return st;
     }
-    c->graph_K = K; c->graph_Kt = K_total; c->graph_skip = (int)c->skip_mean; c->graph_warm = (int)c->warm_now;
+    gs->K = K; gs->Kt = K_total; gs->skip = (int)c->skip_mean; gs->warm = (int)c->warm_now;
   }
-  cudaError_t e = cudaGraphLaunch(c->graph_exec, c->work);
-  c->launches += c->graph_launches;
+  gs->used = ++c->gclock;
+  cudaError_t e = cudaGraphLaunch(gs->exec, c->work);
+  c->launches += gs->launches;
   c->stream = user;
   if (e != cudaSuccess) { c->err = std::string("cudaGraphLaunch: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
   CK(cudaEventRecord(c->ev_out, c->work));
@@ -1020,7 +1045,7 @@ static void free_all(Ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->work) cudaStreamSynchronize(c->work);
   if (c->side) cudaStreamSynchronize(c->side);
-  if (c->graph_exec) { cudaGraphExecDestroy(c->graph_exec); c->graph_exec = nullptr; }
+  for (auto& s : c->gslot) if (s.exec) { cudaGraphExecDestroy(s.exec); s.exec = nullptr; }
   comm_destroy(c);
   dense_tc_free(c);
   if (c->phi && !c->phi_owned) c->phi = nullptr;   // borrowed from the caller
@@ -1030,7 +1055,7 @@ static void free_all(Ctx* c) {
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
                   c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt,
-                  c->flow_state, c->flow_part2};
+                  c->flow_state, c->flow_part2, c->mt_b0, c->mt_mu, c->b0_saved, c->obs_dev};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (int g = 1; g < Ctx::MAXG; ++g) if (c->gs[g]) cudaFree(c->gs[g]);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -1044,7 +1069,6 @@ static void free_all(Ctx* c) {
     if (c->gstream[g]) cudaStreamDestroy(c->gstream[g]);
     if (c->gjoin[g]) cudaEventDestroy(c->gjoin[g]);
   }
-  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->work) cudaStreamDestroy(c->work);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_out) cudaEventDestroy(c->ev_out);
@@ -1444,6 +1468,89 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
   CK(cudaStreamSynchronize(c->stream));
   prof_collect(c);
   return COFEM_OK;
+}
+
+// NEXT-4 multi-task SBL (reading R22): L tasks share Phi, beta and alpha.  Per EM iteration the
+// task means are solved one after another through the E-step machinery (tasks 1..L-1 as
+// mean-only E-steps, K = 0; task 0 with the K probes, which give s), then alpha = 1 / (mean_l mu_l^2
+// + s).  Each task's b0 = beta Phi^T y_l comes from the operator's own setup arithmetic.
+static cofem_status em_multi_impl(Ctx* c, int L, const float* Y, int iters, int K, uint64_t seed, int t0,
+                                  const double* alpha_init, double* alpha_out, double* MU_out, double* s_out) {
+  if (L < 1 || !Y) { c->err = "multi-task: need L >= 1 and Y"; return COFEM_ERR_INVALID; }
+  if (iters < 1) { c->err = "iters must be >= 1"; return COFEM_ERR_INVALID; }
+  if (c->sharded || c->pp) { c->err = "multi-task: single-GPU contexts only"; return COFEM_ERR_UNSUPPORTED; }
+  if (c->opt.warm_start) { c->err = "multi-task: no warm start"; return COFEM_ERR_UNSUPPORTED; }
+  cofem_status st;
+  if ((st = check_K(c, K))) return st;
+  const int64_t Dp = c->Dp;
+  if (L > c->mt_cap) {
+    if (c->mt_b0) cudaFree(c->mt_b0);
+    if (c->mt_mu) cudaFree(c->mt_mu);
+    c->mt_b0 = c->mt_mu = nullptr; c->mt_cap = 0;
+    ALLOC(c->mt_b0, (size_t)L * Dp); ALLOC(c->mt_mu, (size_t)L * Dp);
+    c->mt_cap = L;
+  }
+  if (!c->b0_saved) ALLOC(c->b0_saved, Dp);
+  CK(cudaMemcpyAsync(c->b0_saved, c->b0, Dp * 8, cudaMemcpyDeviceToDevice, c->stream));
+  {   // b0 of every task
+    float* ydev = nullptr;
+    const bool ydv = is_device_ptr(Y);
+    if (!ydv) {
+      CK(cudaMalloc(&ydev, (size_t)c->N * sizeof(float)));
+    }
+    for (int l = 0; l < L && st == COFEM_OK; ++l) {
+      const float* yl = Y + (size_t)l * c->N;
+      if (!ydv) { CK(cudaMemcpyAsync(ydev, yl, c->N * sizeof(float), cudaMemcpyHostToDevice, c->stream)); yl = ydev; }
+      double* out = c->mt_b0 + (size_t)l * Dp;
+      st = c->kind == COFEM_OP_DENSE ? dense_b0(c, yl, out) : c->kind == COFEM_OP_DCT2_MASKED ? dct_b0(c, yl, out)
+                                                                                          : conv_b0(c, yl, out);
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    if (ydev) cudaFree(ydev);
+    if (st != COFEM_OK) return st;
+  }
+  if (alpha_init) {
+    const double* a_dev;
+    if ((st = stage_in(c, alpha_init, c->alpha, &a_dev))) return st;
+    if (a_dev != c->alpha) CK(cudaMemcpyAsync(c->alpha, a_dev, c->D * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if ((st = validate_alpha(c, c->alpha))) return st;
+  } else {
+    std::vector<double> ones(c->D, 1.0);
+    CK(cudaMemcpyAsync(c->alpha, ones.data(), c->D * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  for (int i = 0; i < iters; ++i) {
+    CK(cudaEventRecord(c->ev0, c->stream));
+    for (int l = L - 1; l >= 0; --l) {      // task 0 last: its E-step (with the probes) leaves s
+      CK(cudaMemcpyAsync(c->b0, c->mt_b0 + (size_t)l * Dp, Dp * 8, cudaMemcpyDeviceToDevice, c->stream));
+      if ((st = estep_device(c, l ? 0 : K, seed, t0 + i, 0, l ? 1 : K))) return st;
+      CK(cudaMemcpyAsync(c->mt_mu + (size_t)l * Dp, c->x0, Dp * 8, cudaMemcpyDeviceToDevice, c->stream));
+      if (l && (st = estep_report(c, 1, false))) return st;
+    }
+    launch_begin(c, KC_FINAL);
+    k_mstep_multi<<<c->num_sms * 4, 256, 0, c->stream>>>(c->D, Dp, L, c->mt_mu, c->s, c->alpha, c->opt.den_floor,
+                                                          c->opt.alpha_max);
+    launch_end(c, KC_FINAL);
+    if (check_launch(c, "k_mstep_multi")) return COFEM_ERR_CUDA;
+    CK(cudaEventRecord(c->ev1, c->stream));
+    st = estep_report(c, K + 1, i == iters - 1);
+    float ms = 0; cudaEventElapsedTime(&ms, c->ev0, c->ev1); c->estep_ms = ms;
+    if (st != COFEM_OK) return st;
+  }
+  CK(cudaMemcpyAsync(c->b0, c->b0_saved, Dp * 8, cudaMemcpyDeviceToDevice, c->stream));   // the context's own y again
+  if (alpha_out) CK(cudaMemcpyAsync(alpha_out, c->alpha, c->D * 8, cudaMemcpyDefault, c->stream));
+  if (s_out) CK(cudaMemcpyAsync(s_out, c->s, c->D * 8, cudaMemcpyDefault, c->stream));
+  if (MU_out) CK(cudaMemcpy2DAsync(MU_out, c->D * 8, c->mt_mu, Dp * 8, c->D * 8, L, cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  prof_collect(c);
+  return COFEM_OK;
+}
+
+cofem_status cofem_em_multi(cofem_ctx ctx, int32_t L, const float* Y, int32_t iters, int32_t K, uint64_t seed,
+                            int32_t t0, const double* alpha_init, double* alpha_out, double* MU_out, double* s_out) {
+  if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
+  ctx->c.err.clear();
+  return em_multi_impl(&ctx->c, L, Y, iters, K, seed, t0, alpha_init, alpha_out, MU_out, s_out);
 }
 
 cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out) {

@@ -80,11 +80,18 @@ struct Ctx {
   void* sup_stats = nullptr; void* sup_host = nullptr;   // support certificate (device / pinned host)
   int64_t sup_count = 0, sup_adjacent = 0;
   double sup_max = 0, sup_min_margin = 0;
-  cudaGraphExec_t graph_exec = nullptr; // captured E-step (cofem.cu estep_device)
-  int graph_K = -1, graph_Kt = -1, graph_skip = -1, graph_warm = -1;
+  // captured E-steps (cofem.cu estep_device), a small LRU cache keyed by the launch shape (the
+  // multi-task EM alternates mean-only and full E-steps)
+  struct GraphSlot { cudaGraphExec_t exec = nullptr; int K = -1, Kt = -1, skip = -1, warm = -1; int64_t launches = 0; uint64_t used = 0; };
+  static constexpr int NGRAPH = 4;
+  GraphSlot gslot[NGRAPH];
+  uint64_t gclock = 0;
   bool warm_now = false;                // this E-step starts the mean column from x0 (R20)
   bool skip_mean = false;          // cofem_estep_probes: column 0 frozen from the start (mean owned elsewhere)
-  int64_t graph_launches = 0;
+  // multi-task EM (cofem_em_multi, reading R22): beta Phi^T y_l and mu_l of every task
+  double* mt_b0 = nullptr; double* mt_mu = nullptr; double* b0_saved = nullptr; int mt_cap = 0;
+  int64_t* obs_dev = nullptr;           // DCT2: mask indices kept on the device (b0 of other y)
+  double conv_sumsq = 0;                // CIRCCONV: sum h^2 (b0 of other y)
   void* dct_tab32 = nullptr;            // DCT2 twiddle tables (float), see op_dct.cu
   void* dct_tab64 = nullptr;            // (double)
   int ntaps = 0;                        // CIRCCONV
@@ -267,6 +274,9 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev);
 cofem_status dct_apply(Ctx* c, int m, int iter, bool dir);   // direction update fused into pass A
 cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host);
 cofem_status conv_apply(Ctx* c, int m, int iter);
+cofem_status dense_b0(Ctx* c, const float* y_dev, double* out);   // beta Phi^T y of another y (R22)
+cofem_status dct_b0(Ctx* c, const float* y_dev, double* out);
+cofem_status conv_b0(Ctx* c, const float* y_dev, double* out);
 
 bool dct1k_eligible(const Ctx* c);
 cofem_status dct1k_setup(Ctx* c);

@@ -91,6 +91,15 @@ __global__ void __launch_bounds__(CONV_THREADS) k_conv_apply(int64_t D, int64_t 
 
 static size_t conv_smem() { return (size_t)(2 * CONV_MAXH + 2 + CONV_TILE + 2 * CONV_MAXH) * sizeof(double); }
 
+// b0 = beta Phi^T y for another observation vector (multi-task EM, R22; unsharded)
+cofem_status conv_b0(Ctx* c, const float* y_dev, double* out) {
+  launch_begin(c, KC_SETUP);
+  k_conv_setup<<<c->num_sms * 8, 256, 0, c->stream>>>(c->taps, c->ntaps, y_dev, c->D, c->D, c->beta, c->conv_sumsq, out,
+                                                      c->colsq);
+  launch_end(c, KC_SETUP);
+  return check_launch(c, "conv_b0") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
 cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host) {
   const int T = c->ntaps, H = T - 1;
   std::vector<double> g(2 * H + 1);
@@ -111,6 +120,7 @@ cofem_status conv_setup(Ctx* c, const float* y_dev, const float* taps_host) {
     double* gp; cudaMalloc(&gp, g.size() * 8); cudaMemcpy(gp, g.data(), g.size() * 8, cudaMemcpyHostToDevice);
     cudaFree(c->g32); c->g32 = reinterpret_cast<float*>(gp);
   }
+  c->conv_sumsq = sumsq;
   const float* y_use = y_dev;
   float* y_ext = nullptr;
   int64_t Dwrap = c->D;

@@ -467,6 +467,32 @@ static cofem_status set_attrs(Ctx* c) {
   return check_launch(c, "dct attrs") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
+// b0 = beta Phi^T y (Eq. 5): scatter y into a zero image, then the forward 2D DCT C_r Y C_c^T
+// (convention 1: Phi^T = C2^T S^T, C_r^T Y C_c), fp64 -- at setup and for the further observation
+// vectors of the multi-task EM (R22)
+cofem_status dct_b0(Ctx* c, const float* y_dev, double* out) {
+  const int rows = c->rows, cols = c->cols;
+  const int64_t D = c->D;
+  double *Cr = nullptr, *Cc = nullptr, *tmp = nullptr, *img = nullptr;
+  if (cudaMalloc(&tmp, D * 8) != cudaSuccess || cudaMalloc(&img, D * 8) != cudaSuccess ||
+      cudaMalloc(&Cr, (size_t)rows * rows * 8) != cudaSuccess || cudaMalloc(&Cc, (size_t)cols * cols * 8) != cudaSuccess) {
+    c->err = "cudaMalloc dct b0"; return COFEM_ERR_OOM;
+  }
+  cudaMemsetAsync(img, 0, D * 8, c->stream);
+  launch_begin(c, KC_SETUP);
+  k_y_scatter<<<c->num_sms * 4, 256, 0, c->stream>>>(c->obs_dev, c->N, y_dev, img);
+  launch_end(c, KC_SETUP);
+  std::vector<double> h;
+  dct_matrix(h, rows, false); cudaMemcpyAsync(Cr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
+  dct_matrix(h, cols, false); cudaMemcpyAsync(Cc, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
+  const int tcv = c->conv ? 0 : 1, tr = c->conv ? 1 : 0;
+  gemm64(c, rows, cols, cols, img, cols, 0, Cc, cols, tcv, tmp, cols, 1.0);
+  gemm64(c, rows, cols, rows, Cr, rows, tr, tmp, cols, 0, out, cols, c->beta);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(tmp); cudaFree(img); cudaFree(Cr); cudaFree(Cc);
+  return check_launch(c, "dct_b0") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
 cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   const int rows = c->rows, cols = c->cols;
   const int64_t D = c->D;
@@ -498,7 +524,6 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   if (c->conv == 0) k_mask_vvT<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, rows, cols, c->mask_vvT);
   else k_mask_T<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, rows, cols, c->mask_vvT);
   k_mask_to_double<<<c->num_sms * 4, 256, 0, c->stream>>>(mask, D, md);
-  k_y_scatter<<<c->num_sms * 4, 256, 0, c->stream>>>(obs_dev, c->N, y_dev, img);
   launch_end(c, KC_SETUP);
   // colsq = Q_r M Q_c^T with Q = C o C (diag of C2 M C2^T)
   std::vector<double> h;
@@ -508,14 +533,15 @@ cofem_status dct_setup(Ctx* c, const float* y_dev, const int64_t* obs_dev) {
   const int tcv = c->conv ? 0 : 1, tr = c->conv ? 1 : 0;
   gemm64(c, rows, cols, cols, md, cols, 0, Cc, cols, tcv, tmp, cols, 1.0);        // M Q_c^T  (conv. 1: M Q_c)
   gemm64(c, rows, cols, rows, Cr, rows, tr, tmp, cols, 0, c->colsq, cols, 1.0);   // Q_r (.)  (conv. 1: Q_r^T (.))
-  // b0 = beta C_r Y C_c^T (Phi^T y: scatter, forward 2D DCT), fp64
-  dct_matrix(h, rows, false); cudaMemcpyAsync(Cr, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
-  dct_matrix(h, cols, false); cudaMemcpyAsync(Cc, h.data(), h.size() * 8, cudaMemcpyHostToDevice, c->stream); cudaStreamSynchronize(c->stream);
-  // convention 1: Phi^T y = C2^T (S^T y) = C_r^T Y C_c
-  gemm64(c, rows, cols, cols, img, cols, 0, Cc, cols, tcv, tmp, cols, 1.0);
-  gemm64(c, rows, cols, rows, Cr, rows, tr, tmp, cols, 0, c->b0, cols, c->beta);
   cudaStreamSynchronize(c->stream);
   cudaFree(mask); cudaFree(md); cudaFree(tmp); cudaFree(img); cudaFree(Cr); cudaFree(Cc);
+  // the mask indices stay on the device (b0 of further observation vectors, multi-task EM)
+  if (cudaMalloc(&c->obs_dev, c->N * sizeof(int64_t)) != cudaSuccess) { c->err = "cudaMalloc obs"; return COFEM_ERR_OOM; }
+  cudaMemcpyAsync(c->obs_dev, obs_dev, c->N * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream);
+  {
+    cofem_status sb = dct_b0(c, y_dev, c->b0);
+    if (sb != COFEM_OK) return sb;
+  }
   if (check_launch(c, "dct setup")) return COFEM_ERR_CUDA;
   // partial-sum stride: pass C grid.x
   int rpc = 1;

@@ -276,6 +276,14 @@ static cofem_status dense_apply_t(Ctx* c, int m, int iter) {
   return COFEM_OK;
 }
 
+// b0 = beta Phi^T y for another observation vector (multi-task EM, R22); colsq is recomputed as is
+cofem_status dense_b0(Ctx* c, const float* y_dev, double* out) {
+  launch_begin(c, KC_SETUP);
+  k_dense_setup<<<(unsigned)((c->D + 255) / 256), 256, 0, c->stream>>>(c->phi, c->N, c->D, c->ld, y_dev, c->beta, out, c->colsq);
+  launch_end(c, KC_SETUP);
+  return check_launch(c, "dense_b0") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
 cofem_status dense_apply(Ctx* c, int m, int iter) {
   if (c->dense_tc) return dense_tc_apply(c, m, iter);     // tcgen05 3xTF32 path (op_dense_tc.cu)
   return c->probe64 ? dense_apply_t<double>(c, m, iter) : dense_apply_t<float>(c, m, iter);

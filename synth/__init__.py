@@ -125,6 +125,34 @@ def circconv(D, ntaps, nnz, K, U, T, seed=0, name=None):
     return Workload(name or "conv_%d" % D, "circconv", D, D, K, U, T, BETA, y, z, taps=h, seed=seed)
 
 
+def tasks(w, L, seed=1, shared_support=True):
+    """Observation vectors of L tasks on workload w's dictionary (multi-task SBL, R22): task 0 is
+    w.y; tasks 1..L-1 draw new N(0, 1) values (on w's support when shared_support, the multi-task
+    model's shared sparsity profile) and y_l = Phi z_l + sigma e with library routines, as above.
+    Returns (Y fp32 [L, N], Z fp64 [L, D])."""
+    rng = np.random.default_rng(1000 + seed)
+    sigma = 1.0 / math.sqrt(w.beta)
+    sup = np.nonzero(w.z_true)[0]
+    Y, Z = [w.y], [w.z_true]
+    for _ in range(1, L):
+        z = np.zeros(w.D)
+        idx = sup if shared_support else rng.choice(w.D, sup.size, replace=False)
+        z[idx] = rng.standard_normal(idx.size)
+        if w.kind == "dense":
+            y = w.phi.astype(np.float64) @ z
+        elif w.kind == "dct2_masked":
+            img = z.reshape(w.rows, w.cols)
+            pix = sfft.idctn(img, norm="ortho") if w.convention == 0 else sfft.dctn(img, norm="ortho")
+            y = pix.ravel()[w.obs_idx]
+        else:
+            hp = np.zeros(w.D)
+            hp[:w.taps.size] = w.taps.astype(np.float64)
+            y = np.fft.irfft(np.fft.rfft(hp) * np.fft.rfft(z), n=w.D)
+        Y.append((y + sigma * rng.standard_normal(y.size)).astype(np.float32))
+        Z.append(z)
+    return np.ascontiguousarray(np.stack(Y)), np.stack(Z)
+
+
 def preset(name, seed=0):
     """BASELINE.json configs C1..C5 at full size."""
     if name == "C1":

@@ -521,3 +521,30 @@ def test_warm_start_em_matches_oracle(w):
     a0, mu0, _ = gpu_em(ctx_of(w), w, 1, w.K, 4)            # the first E-step of a call is cold
     a1, mu1, _ = gpu_em(ctx_of(w, warm_start=True), w, 1, w.K, 4)
     assert np.array_equal(a0, a1) and np.array_equal(mu0, mu1)
+
+
+@pytest.mark.parametrize("w", [SMALL[1], SMALL[2], SMALL[5], SMALL[7], synth.preset("C1"),
+                               synth.dct(1024, 1024, 262144, 400, K=3, U=20, T=2, seed=3, name="dct1024_fast_U20")],
+                         ids=lambda w: w.name)
+def test_multitask_em_matches_oracle(w):
+    """NEXT-4 multi-task SBL (reading R22, cofem_em_multi): three tasks sharing Phi and alpha, against
+    the oracle's cofem_em_multi -- fast mode at the north_star EM bars, parity mode to 1e-7 -- and L = 1
+    equals cofem_em bit for bit."""
+    from oracle.cofem import cofem_em_multi
+    from parity_util import check
+    Y, _ = synth.tasks(w, 3, seed=2)
+    T = 2
+    oa, OMU, os_ = cofem_em_multi(op_of(w), Y.T.astype(np.float64), w.beta, T, w.K, 6, w.U)
+    for p64, bar in ((0, 1e-3), (1, 1e-6)):      # parity: fp64 rounding through the unconverged CG (C1: 4.7e-7)
+        ctx = ctx_of(w, probe_precision=p64)
+        a, MU, s = dev(w.D), torch.empty(3 * w.D, dtype=torch.float64, device="cuda"), dev(w.D)
+        ctx.em_multi(torch.as_tensor(Y, device="cuda"), T, w.K, 6, 0, None, a, MU, s)
+        MU = MU.cpu().numpy().reshape(3, w.D)
+        check("1/alpha", 1 / a.cpu().numpy(), 1 / oa, bar, 10 * bar)
+        for l in range(3):
+            check("mu_%d" % l, MU[l], OMU[:, l], bar, 10 * bar)
+    ctx = ctx_of(w)
+    a1, m1, s1 = dev(w.D), dev(w.D), dev(w.D)
+    ctx.em_multi(torch.as_tensor(Y[:1], device="cuda"), T, w.K, 6, 0, None, a1, m1, s1)
+    ref = gpu_em(ctx_of(w), w, T, w.K, 6)
+    assert np.array_equal(a1.cpu().numpy(), ref[0]) and np.array_equal(m1.cpu().numpy(), ref[1])

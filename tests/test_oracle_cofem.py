@@ -376,3 +376,63 @@ def test_warm_start_em_first_estep_is_cold():
     a1, m1, s1 = cofem_em(op, w.y, w.beta, 1, 3, 5, 15)
     a2, m2, s2 = cofem_em(op, w.y, w.beta, 1, 3, 5, 15, warm_start=True)
     assert np.array_equal(a1, a2) and np.array_equal(m1, m2)
+
+
+# ---------------------------------------------------------------- R22: multi-task SBL (NEXT-4)
+def test_multitask_one_task_is_algorithm1():
+    from oracle.cofem import cofem_em_multi, estep_multi
+    w = synth.dense(30, 80, 4, K=3, U=20, T=1, seed=7)
+    op = DenseOp(w.phi)
+    mu, s, _ = estep(op, w.y, w.beta, np.ones(w.D), 3, 5, 0, 20)
+    MU, s2, _ = estep_multi(op, w.y[:, None], w.beta, np.ones(w.D), 3, 5, 0, 20)
+    assert np.array_equal(MU[:, 0], mu) and np.array_equal(s2, s)
+    a1, m1, _ = cofem_em(op, w.y, w.beta, 3, 3, 5, 20)
+    a2, M2, _ = cofem_em_multi(op, w.y[:, None], w.beta, 3, 3, 5, 20)
+    assert np.array_equal(a1, a2) and np.array_equal(M2[:, 0], m1)
+
+
+def test_multitask_diagonal_closed_form():
+    """Phi with orthogonal columns (A diagonal, Jacobi PCG exact in one iteration): every task's
+    mu_l,d = beta (Phi^T y_l)_d / lam_d, s_d = 1/lam_d, and the multi-task M-step is
+    alpha_d = 1 / (mean_l mu_l,d^2 + 1/lam_d), lam = beta c + alpha (R22)."""
+    from oracle.cofem import cofem_em_multi
+    rng = np.random.default_rng(11)
+    D, N, L = 10, 14, 3
+    Q, _ = np.linalg.qr(rng.standard_normal((N, D)))
+    c = rng.uniform(0.5, 2.0, D)
+    phi = Q * np.sqrt(c)[None, :]
+    Y = rng.standard_normal((N, L))
+    beta = 3.0
+    a, MU, s = cofem_em_multi(DenseOp(phi), Y, beta, 1, 2, 0, 1, alpha_init=np.full(D, 0.7))
+    lam = beta * c + 0.7
+    u = beta * (Q.T @ Y) * np.sqrt(c)[:, None]              # beta Phi^T Y
+    assert np.allclose(MU, u / lam[:, None], rtol=1e-10, atol=0)
+    assert np.allclose(s, 1.0 / lam, rtol=1e-10, atol=0)
+    assert np.allclose(a, 1.0 / (np.mean((u / lam[:, None]) ** 2, axis=1) + 1.0 / lam), rtol=1e-10, atol=0)
+
+
+def test_multitask_matches_exact_multitask_em():
+    """Converged CG at D = 40 and many probes: the multi-task CoFEM EM tracks the exact multi-task
+    EM (Cholesky: Sigma shared, alpha = L / sum_l (mu_l^2 + Sigma_dd))."""
+    from oracle.cofem import cofem_em_multi
+    from oracle.exact import exact_posterior
+    rng = np.random.default_rng(12)
+    D, N, L = 40, 20, 4
+    phi = rng.standard_normal((N, D)) / np.sqrt(N)
+    Y = rng.standard_normal((N, L))
+    beta = 50.0
+    alpha = np.ones(D)
+    for _ in range(3):
+        MUe = []
+        for l in range(L):
+            mu, Sig = exact_posterior(phi, beta, alpha, Y[:, l])
+            MUe.append(mu)
+        MUe = np.array(MUe).T
+        alpha = L / np.sum(MUe ** 2 + np.diag(Sig)[:, None], axis=1)
+    from oracle.cofem import estep_multi
+    MU1, _, _ = estep_multi(DenseOp(phi), Y, beta, np.ones(D), 8, 1, 0, 200)
+    MU1e = np.array([exact_posterior(phi, beta, np.ones(D), Y[:, l])[0] for l in range(L)]).T
+    assert rel(MU1, MU1e) < 1e-8                # E-step 1: the task means do not depend on the probes
+    a, MU, s = cofem_em_multi(DenseOp(phi), Y, beta, 3, 4000, 1, 200)
+    assert rel(1 / a, 1 / alpha) < 0.05         # s is the K-probe estimate of diag(Sigma)
+    assert rel(MU, MUe) < 0.05
