@@ -26,8 +26,14 @@ template <typename T> struct Geo { static constexpr int RT = sizeof(T) == 8 ? 4 
 //                            X[k+M] = Re(W_k R3_k) + Re(conj(W_{M-k}) R4_k)
 // with the orthonormal scales, the 1/M of the inverse FFT and the even/odd split folded in
 // (k < M; the entries are derived in build_tables below).
+#ifdef COFEM_1K_TAB6   // round-1 layout: six complex tables per k (P, Q pre; R1..R4 post)
 constexpr int TW2 = 0, TW3 = 64, TP = TW3 + 512, TQ = TP + M, TR1 = TQ + M, TR2 = TR1 + M, TR3 = TR2 + M,
               TR4 = TR3 + M, TTOT = TR4 + M;   // offsets in complex entries
+constexpr int TPRE = TR1;                      // pass A's prefix
+#else                   // two tables per k, Ahat and Bhat (op_dct1k.cu build_tables): pre and post derive from them
+constexpr int TW2 = 0, TW3 = 64, TA = TW3 + 512, TB = TA + M, TTOT = TB + M;
+constexpr int TPRE = TTOT;
+#endif
 template <typename T> struct Tw { const cplx<T>* base; };
 
 template <typename T>

@@ -32,6 +32,7 @@
 namespace cofem {
 namespace d1k {
 
+#ifdef COFEM_1K_TAB6
 // DCT-III (orthonormal inverse) pre-processing for one k: W[k] = u1 P_k + u2 Q_k.
 template <typename T>
 __device__ __forceinline__ cplx<T> dct3_pre(int k, T Xk, T XLk, T XkM, T XMk, const Tw<T>& tb) {
@@ -47,6 +48,28 @@ __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const T
   lo = Wk.x * R1.x - Wk.y * R1.y + Wm.x * R2.x + Wm.y * R2.y;
   hi = Wk.x * R3.x - Wk.y * R3.y + Wm.x * R4.x + Wm.y * R4.y;
 }
+#else
+// With Ahat = sc q1 (1 - i h)/2 and Bhat = sc q2 (1 + i h)/2 (build_tables), the six round-1 tables
+// are P = conj(Ahat) (x sqrt 2 at k = 0), Q = conj(Bhat), R1 = Ahat, R2 = e^{i pi/4} Bhat, R3 = Bhat,
+// R4 = e^{-i pi/4} Ahat (x 1/sqrt 2 on R1, R2 at k = 0), since q2 = e^{-i pi/4} q1 and s / sc = 2M/L = 1:
+// two shared-memory loads per k instead of six; the k = 0 factors are applied by the caller.
+// DCT-III (orthonormal inverse) pre-processing for one k: W[k] = (Xk - i XLk) P + (XkM - i XMk) Q.
+template <typename T>
+__device__ __forceinline__ cplx<T> dct3_pre(int k, T Xk, T XLk, T XkM, T XMk, const Tw<T>& tb) {
+  const cplx<T> A = tb.base[TA + k], B = tb.base[TB + k];
+  return {Xk * A.x - XLk * A.y + XkM * B.x - XMk * B.y, -Xk * A.y - XLk * A.x - XkM * B.y - XMk * B.x};
+}
+
+// DCT-II post-processing for one k from W[k], W[(M-k) mod M]: orthonormal X[k], X[k+M].
+template <typename T>
+__device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const Tw<T>& tb, T& lo, T& hi) {
+  const cplx<T> A = tb.base[TA + k], B = tb.base[TB + k];
+  const T h = (T)0.70710678118654752440;
+  const T u = h * (Wm.x + Wm.y), v = h * (Wm.x - Wm.y);     // e^{-i pi/4} Wm = (u, -v), e^{i pi/4} Wm = (v, u)
+  lo = Wk.x * A.x - Wk.y * A.y + u * B.x - v * B.y;
+  hi = Wk.x * B.x - Wk.y * B.y + v * A.x + u * A.y;
+}
+#endif
 
 // Packed spectra of the DCT-III of a line held canonically in A, B, C, E.
 template <typename T>
@@ -59,7 +82,11 @@ __device__ __forceinline__ void pre_all(int lane, const T (&A)[8], const T (&B)[
     // slot a, k = ja + 64 r: X[M-k], X[L-k]
     const T aMk = l0 ? (r ? A[(8 - r) & 7] : C[0]) : B[7 - r];
     const T aLk = l0 ? (r ? C[(8 - r) & 7] : (T)0) : E[7 - r];
+#ifdef COFEM_1K_TAB6
     va[r] = dct3_pre<T>(ja + 64 * r, A[r], aLk, C[r], aMk, tb);
+#else
+    va[r] = dct3_pre<T>(ja + 64 * r, (l0 && r == 0) ? A[0] * (T)1.41421356237309504880 : A[r], aLk, C[r], aMk, tb);
+#endif
     // slot b, k = jb + 64 r
     const T bMk = l0 ? B[7 - r] : A[7 - r];
     const T bLk = l0 ? E[7 - r] : C[7 - r];
@@ -77,6 +104,9 @@ __device__ __forceinline__ void post_all(int lane, const cplx<T> (&va)[8], const
   for (int r = 0; r < 8; ++r) {
     const cplx<T> wa = l0 ? va[(8 - r) & 7] : vb[7 - r];
     dct2_post<T>(ja + 64 * r, va[r], wa, tb, A[r], C[r]);
+#ifndef COFEM_1K_TAB6
+    if (l0 && r == 0) A[0] *= (T)0.70710678118654752440;     // k = 0: s0 / s = 1 / sqrt 2
+#endif
     const cplx<T> wb = l0 ? vb[7 - r] : va[7 - r];
     dct2_post<T>(jb + 64 * r, vb[r], wb, tb, B[r], E[r]);
   }
@@ -172,8 +202,8 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_INV
     pf_line(cn.p + rn);
     if (dir) pf_line(cn.r + rn);
   }
-  // pass A needs the FFT twiddles and the DCT-III pre tables only: the [0, TR1) prefix (12.8 KB in fp32)
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG), TR1);   // + barrier
+  // pass A needs the FFT twiddles and the DCT-III pre tables only: the [0, TPRE) prefix (12.8 KB in fp32)
+  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG), TPRE);   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
@@ -909,7 +939,7 @@ template <typename T> static size_t smem_bytes(int ntab = TTOT) {
 
 template <typename T> static void set_attrs() {
   const int s = (int)smem_bytes<T>();
-  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(TR1));
+  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(TPRE));
   cudaFuncSetAttribute(k1k_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
   cudaFuncSetAttribute(k1k_rows_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
 }
@@ -942,12 +972,18 @@ template <typename T> static std::vector<cplx<T>> build_tables() {
   for (int k = 0; k < M; ++k) {
     const C q1 = e(-PI * k / (2.0 * L)), q2 = e(-PI * (k + M) / (2.0 * L)), hh = e(-2 * PI * k / L);
     const double sck = k == 0 ? sc0 : sc, sk = k == 0 ? s0 : s;
+#ifdef COFEM_1K_TAB6
     put(TP + k, sck * std::conj(q1) * (1.0 + I * std::conj(hh)) / 2.0);
     put(TQ + k, sc * std::conj(q2) * (1.0 - I * std::conj(hh)) / 2.0);
     const C r1 = sk * q1 * (1.0 - I * hh) / 2.0, r2 = sk * q1 * (1.0 + I * hh) / 2.0;
     const C r3 = s * q2 * (1.0 + I * hh) / 2.0, r4 = s * q2 * (1.0 - I * hh) / 2.0;
     // lo = Re(Wk r1) + Re(conj(Wm) r2) = Wk.x r1.x - Wk.y r1.y + Wm.x r2.x + Wm.y r2.y
     put(TR1 + k, r1); put(TR2 + k, r2); put(TR3 + k, r3); put(TR4 + k, r4);
+#else
+    (void)sck; (void)sk; (void)s; (void)s0;
+    put(TA + k, sc * q1 * (1.0 - I * hh) / 2.0);
+    put(TB + k, sc * q2 * (1.0 + I * hh) / 2.0);
+#endif
   }
   return h;
 }
@@ -1029,7 +1065,7 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const dim3 blk(RT * 32);
   const bool mean = j0 == 0;        // the fp64 mean column is timed as its own class
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
-  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(TR1)), blk, smem_bytes<T>(TR1), st>>>(
+  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(TPRE)), blk, smem_bytes<T>(TPRE), st>>>(
       a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_COLS, st);
