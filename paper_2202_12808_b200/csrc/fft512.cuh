@@ -30,9 +30,16 @@ template <typename T> struct Geo { static constexpr int RT = sizeof(T) == 8 ? 4 
 constexpr int TW2 = 0, TW3 = 64, TP = TW3 + 512, TQ = TP + M, TR1 = TQ + M, TR2 = TR1 + M, TR3 = TR2 + M,
               TR4 = TR3 + M, TTOT = TR4 + M;   // offsets in complex entries
 constexpr int TPRE = TR1;                      // pass A's prefix
-#else                   // two tables per k, Ahat and Bhat (op_dct1k.cu build_tables): pre and post derive from them
-constexpr int TW2 = 0, TW3 = 64, TA = TW3 + 512, TB = TA + M, TTOT = TB + M;
+#else                   // Ahat_k, Bhat_k (op_dct1k.cu build_tables): pre and post derive from them
+constexpr int TW2 = 0, TW3 = 64, TAB2 = TW3 + 512, TTOT = TAB2 + 2 * M;
 constexpr int TPRE = TTOT;
+#ifdef COFEM_1K_AB_INTERLEAVE   // [A_0 B_0 A_1 B_1 ..]: one 16-byte load per k (measured +0.7 ms on C4)
+__host__ __device__ constexpr int ia(int k) { return 2 * k; }
+__host__ __device__ constexpr int ib(int k) { return 2 * k + 1; }
+#else                           // [A_0 .. A_{M-1} | B_0 .. B_{M-1}]
+__host__ __device__ constexpr int ia(int k) { return k; }
+__host__ __device__ constexpr int ib(int k) { return M + k; }
+#endif
 #endif
 template <typename T> struct Tw { const cplx<T>* base; };
 
@@ -81,11 +88,34 @@ __device__ __forceinline__ void fft512(cplx<T> (&va)[8], cplx<T> (&vb)[8], int l
 #pragma unroll
     for (int r = 0; r < 8; ++r) { va[r] = x[ba + 8 * r]; vb[r] = x[bb + 8 * r]; }
     const cplx<T>* w3 = tw.base + TW3;
+#ifdef COFEM_FFT_W3_TABLE
 #pragma unroll
     for (int r = 1; r < 8; ++r) {
       twid<T, SIGN>(va[r], w3[r * 64 + ja]);
       twid<T, SIGN>(vb[r], w3[r * 64 + jb]);
     }
+#else
+    // W^{r jb} = W^{64 r} conj(W^{r ja}) = W_8^r conj(W^{r ja}) for jb = 64 - ja (lane > 0); lane 0's
+    // jb = 32 twiddle W_16^r is a constant: one table load per r instead of two
+    const T h = (T)0.70710678118654752440;
+    constexpr double c16[8] = {1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173, 0.0,
+                               -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128675613};
+#pragma unroll
+    for (int r = 1; r < 8; ++r) {
+      const cplx<T> wa = w3[r * 64 + ja];
+      cplx<T> wb;
+      if (r == 1) wb = {h * (wa.x - wa.y), -h * (wa.x + wa.y)};          // W_8^r conj(wa), W_8 = e^{-i pi/4}
+      else if (r == 2) wb = {-wa.y, -wa.x};
+      else if (r == 3) wb = {-h * (wa.x + wa.y), h * (wa.y - wa.x)};
+      else if (r == 4) wb = {-wa.x, wa.y};
+      else if (r == 5) wb = {h * (wa.y - wa.x), h * (wa.x + wa.y)};
+      else if (r == 6) wb = {wa.y, wa.x};
+      else wb = {h * (wa.x + wa.y), h * (wa.x - wa.y)};
+      if (lane == 0) wb = {(T)c16[r], -(T)c16[r <= 4 ? 4 - r : r - 4]};   // W_16^r = e^{-i pi r / 8}
+      twid<T, SIGN>(va[r], wa);
+      twid<T, SIGN>(vb[r], wb);
+    }
+#endif
   }
   dft8<SIGN>(va); dft8<SIGN>(vb);
   __syncwarp();                                         // exchange region free again

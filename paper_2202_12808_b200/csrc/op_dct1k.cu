@@ -54,16 +54,28 @@ __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const T
 // R4 = e^{-i pi/4} Ahat (x 1/sqrt 2 on R1, R2 at k = 0), since q2 = e^{-i pi/4} q1 and s / sc = 2M/L = 1:
 // two shared-memory loads per k instead of six; the k = 0 factors are applied by the caller.
 // DCT-III (orthonormal inverse) pre-processing for one k: W[k] = (Xk - i XLk) P + (XkM - i XMk) Q.
+template <typename T> __device__ __forceinline__ void ld_ab(const Tw<T>& tb, int k, cplx<T>& A, cplx<T>& B) {
+#ifdef COFEM_1K_AB_INTERLEAVE
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = *reinterpret_cast<const float4*>(tb.base + TAB2 + 2 * k);
+    A = {v.x, v.y}; B = {v.z, v.w};
+    return;
+  }
+#endif
+  A = tb.base[TAB2 + ia(k)]; B = tb.base[TAB2 + ib(k)];
+}
 template <typename T>
 __device__ __forceinline__ cplx<T> dct3_pre(int k, T Xk, T XLk, T XkM, T XMk, const Tw<T>& tb) {
-  const cplx<T> A = tb.base[TA + k], B = tb.base[TB + k];
+  cplx<T> A, B;
+  ld_ab(tb, k, A, B);
   return {Xk * A.x - XLk * A.y + XkM * B.x - XMk * B.y, -Xk * A.y - XLk * A.x - XkM * B.y - XMk * B.x};
 }
 
 // DCT-II post-processing for one k from W[k], W[(M-k) mod M]: orthonormal X[k], X[k+M].
 template <typename T>
 __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const Tw<T>& tb, T& lo, T& hi) {
-  const cplx<T> A = tb.base[TA + k], B = tb.base[TB + k];
+  cplx<T> A, B;
+  ld_ab(tb, k, A, B);
   const T h = (T)0.70710678118654752440;
   const T u = h * (Wm.x + Wm.y), v = h * (Wm.x - Wm.y);     // e^{-i pi/4} Wm = (u, -v), e^{i pi/4} Wm = (v, u)
   lo = Wk.x * A.x - Wk.y * A.y + u * B.x - v * B.y;
@@ -325,8 +337,11 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
 template <typename T, bool CG = false>
 __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
 
+#ifndef COFEM_1K_COLS_MINB
+#define COFEM_1K_COLS_MINB 3   // fp32: 3 CTAs (24 warps) per SM
+#endif
 template <typename T>
-__global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_cols(DctArgs a, int j0, int ncols) {
+__global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_COLS_MINB : 1) k1k_cols(DctArgs a, int j0, int ncols) {
   constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
@@ -981,8 +996,8 @@ template <typename T> static std::vector<cplx<T>> build_tables() {
     put(TR1 + k, r1); put(TR2 + k, r2); put(TR3 + k, r3); put(TR4 + k, r4);
 #else
     (void)sck; (void)sk; (void)s; (void)s0;
-    put(TA + k, sc * q1 * (1.0 - I * hh) / 2.0);
-    put(TB + k, sc * q2 * (1.0 + I * hh) / 2.0);
+    put(TAB2 + ia(k), sc * q1 * (1.0 - I * hh) / 2.0);       // Ahat_k
+    put(TAB2 + ib(k), sc * q2 * (1.0 + I * hh) / 2.0);       // Bhat_k
 #endif
   }
   return h;
