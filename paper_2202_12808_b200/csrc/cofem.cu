@@ -1055,7 +1055,7 @@ static void free_all(Ctx* c) {
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
                   c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt,
-                  c->flow_state, c->flow_part2, c->mt_b0, c->mt_mu, c->b0_saved, c->obs_dev};
+                  c->flow_state, c->flow_part2, c->mt_b0, c->mt_mu, c->b0_saved, c->obs_dev, c->maskH, c->twh};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (int g = 1; g < Ctx::MAXG; ++g) if (c->gs[g]) cudaFree(c->gs[g]);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }

@@ -60,6 +60,8 @@ struct Ctx {
   int rows = 0, cols = 0, conv = 0;     // DCT2
   uint8_t* mask_vvT = nullptr;          // DCT2: mask in v-order, transposed [cols][rows]
   uint32_t* maskL = nullptr;            // DCT2 1024 fast path: lane-packed mask (op_dct1k.cu)
+  void* maskH = nullptr;                // its half-warp column pass: [line][16] uint64 mask (fft512h.cuh layout)
+  void* twh = nullptr;                  //   and the W_512^{t k1} tables
   void* tab1k32 = nullptr; void* tab1k64 = nullptr;   // its twiddle tables (float / double)
   bool fast1k = false;                  // DCT2 1024 x 1024: fast path, mean column on `side`
   void* flow_state = nullptr;           // k1k_flow (dataflow probe kernel): dispenser / counters

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "fft512.cuh"
+#include "fft512h.cuh"
 
 namespace cofem {
 namespace d1k {
@@ -407,6 +408,151 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
     st32B<T, RT>(out + (int64_t)row * L + tile * RT, v);
   }
   bar_rt<RT>();
+}
+
+
+// ---------------------------------------------------------------- pass B, half-warp FFTs (fp32 probes)
+// EXPERIMENT (build switch COFEM_1K_COLS_HALF, not the default): correct, but 128 registers (16 warps
+// per SM instead of 24) outweigh its 18 % fewer shared-memory wavefronts: C4 fixed-alpha E-step
+// 42.6 -> 44.9 ms.
+// The column pass with the radix-16 x 32 half-warp FFT pair (fft512h.cuh): 16 lanes per T^T line,
+// two lines per warp, 16 lines per CTA item; one exchange per transform (two per line instead of
+// four), and the two lines of a warp read the same DCT table and twiddle entries (broadcast).
+// Lane (h, t) of warp w owns line 2 w + h of the item and the positions {ka, kb, M + ka, M + kb} +
+// 32 k2 (k2 < 16), ka = t, kb = 32 - t (16 for t = 0): the k <-> M - k and k <-> L - k partners of its
+// spectral points are its own.
+namespace colsh {
+constexpr int NL = 16;                             // lines per CTA item
+constexpr int NTH = L / NL;                        // items per column
+constexpr int TROW = L + 16;                       // tile row stride (floats): the two half-warps of a warp write disjoint banks
+constexpr size_t SMEM_X = (size_t)8 * 2 * d1kh::XREG * sizeof(cplx<float>);   // exchange (aliases the tile)
+constexpr size_t SMEM_TILE = (size_t)NL * TROW * sizeof(float);
+constexpr size_t SMEM_XT = SMEM_X > SMEM_TILE ? SMEM_X : SMEM_TILE;
+constexpr size_t SMEM = SMEM_XT + (size_t)2 * M * sizeof(cplx<float>) + (size_t)d1kh::TWTOT * sizeof(cplx<float>);
+}
+
+// maskH[line][t] bit 2 m + e = mask at v-order row 2 (t + 16 m) + e (the n-layout of fft512h.cuh)
+__global__ void k1k_mask_half(const uint8_t* __restrict__ maskT, unsigned long long* __restrict__ maskH) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= L * 16) return;
+  const int line = idx >> 4, t = idx & 15;
+  const uint8_t* m = maskT + (int64_t)line * L;
+  unsigned long long w = 0;
+  for (int mm = 0; mm < 32; ++mm)
+    for (int e = 0; e < 2; ++e) w |= (unsigned long long)(m[2 * (t + 16 * mm) + e] != 0) << (2 * mm + e);
+  maskH[idx] = w;
+}
+
+#ifndef COFEM_1K_COLSH_MINB
+#define COFEM_1K_COLSH_MINB 2
+#endif
+__global__ void __launch_bounds__(256, COFEM_1K_COLSH_MINB) k1k_cols_h(DctArgs a, int j0, int ncols,
+                                                                      const unsigned long long* __restrict__ maskH,
+                                                                      const cplx<float>* __restrict__ twh) {
+  using namespace colsh;
+  using T = float;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float* tile = reinterpret_cast<float*>(smraw);
+  cplx<T>* xall = reinterpret_cast<cplx<T>*>(smraw);
+  cplx<T>* ab = reinterpret_cast<cplx<T>*>(smraw + SMEM_XT);                 // Ahat | Bhat (2 M)
+  cplx<T>* tw = ab + 2 * M;                                                    // wk | wt
+  __shared__ ColFlags ci;
+  load_colinfo(ci, a.cs, j0, ncols);
+  if (!any_active(ci, ncols)) return;
+  {
+    const cplx<T>* g = (const cplx<T>*)a.tab1k32 + TAB2;
+    for (int i = threadIdx.x; i < 2 * M; i += blockDim.x) ab[i] = g[i];
+    for (int i = threadIdx.x; i < d1kh::TWTOT; i += blockDim.x) tw[i] = twh[i];
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, t = lane & 15;
+  const int ka = t, kb = d1kh::kb_of(t);
+  const bool l0 = t == 0;
+  const int lrow = warp * 2 + h;                       // this half-warp's line within the item
+  cplx<T>* x = xall + (warp * 2 + h) * d1kh::XREG;
+  auto A_ = [&](int k) { return ab[ia(k)]; };
+  auto B_ = [&](int k) { return ab[ib(k)]; };
+  for (int w = blockIdx.x; w < ncols * NTH; w += gridDim.x) {
+    const int jj = w / NTH;
+    if (ci.frozen[jj]) continue;
+    const int tileidx = w % NTH, line = tileidx * NL + lrow;     // v-order image column cv
+    const DctCol<T> c = col_of<T>(a, j0 + jj);
+    const T* __restrict__ ln = c.t1 + (int64_t)line * L;
+    T A[16], B[16], C[16], E[16];
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      A[k2] = ln[ka + 32 * k2]; B[k2] = ln[kb + 32 * k2]; C[k2] = ln[M + ka + 32 * k2]; E[k2] = ln[M + kb + 32 * k2];
+    }
+    cplx<T> va[16], vb[16];
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {                  // DCT-III pre (dct3_pre's arithmetic, Ahat / Bhat tables)
+      const int r = 15 - k2;
+      T xLa = E[r], xMa = B[r], xLb = C[r], xMb = A[r];
+      if (l0) {
+        xLa = k2 ? C[16 - k2] : (T)0; xMa = k2 ? A[16 - k2] : C[0];
+        xLb = E[r]; xMb = B[r];
+      }
+      const T xa = (l0 && k2 == 0) ? A[0] * (T)1.41421356237309504880 : A[k2];
+      {
+        const cplx<T> Aa = A_(ka + 32 * k2), Ba = B_(ka + 32 * k2);
+        va[k2] = {xa * Aa.x - xLa * Aa.y + C[k2] * Ba.x - xMa * Ba.y, -xa * Aa.y - xLa * Aa.x - C[k2] * Ba.y - xMa * Ba.x};
+      }
+      {
+        const cplx<T> Ab = A_(kb + 32 * k2), Bb = B_(kb + 32 * k2);
+        vb[k2] = {B[k2] * Ab.x - xLb * Ab.y + E[k2] * Bb.x - xMb * Bb.y, -B[k2] * Ab.y - xLb * Ab.x - E[k2] * Bb.y - xMb * Bb.x};
+      }
+    }
+    cplx<T> v[32];
+    d1kh::ifft_k2n(va, vb, v, t, x, tw);
+    {                                                   // mask (v-order pixel rows of this column)
+      const unsigned long long mb = maskH[line * 16 + t];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        if (!((mb >> (2 * m)) & 1ull)) v[m].x = (T)0;
+        if (!((mb >> (2 * m + 1)) & 1ull)) v[m].y = (T)0;
+      }
+    }
+    d1kh::fft_n2k(v, va, vb, t, x, tw);
+    // DCT-II post into this line's tile row (natural order); the exchange region aliases the tile,
+    // so every half-warp has finished its FFTs first
+    bar_rt<8>();
+    float* trow = tile + lrow * TROW;
+    const T hh = (T)0.70710678118654752440;
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      const int r = 15 - k2;
+      {   // slot a: k = ka + 32 k2
+        const cplx<T> Wk = va[k2], Wm = l0 ? va[k2 ? 16 - k2 : 0] : vb[r];
+        const cplx<T> Aa = A_(ka + 32 * k2), Ba = B_(ka + 32 * k2);
+        const T u = hh * (Wm.x + Wm.y), vv = hh * (Wm.x - Wm.y);
+        T lo = Wk.x * Aa.x - Wk.y * Aa.y + u * Ba.x - vv * Ba.y;
+        const T hi = Wk.x * Ba.x - Wk.y * Ba.y + vv * Aa.x + u * Aa.y;
+        if (l0 && k2 == 0) lo *= (T)0.70710678118654752440;
+        trow[ka + 32 * k2] = lo; trow[M + ka + 32 * k2] = hi;
+      }
+      {   // slot b: k = kb + 32 k2
+        const cplx<T> Wk = vb[k2], Wm = l0 ? vb[r] : va[r];
+        const cplx<T> Ab = A_(kb + 32 * k2), Bb = B_(kb + 32 * k2);
+        const T u = hh * (Wm.x + Wm.y), vv = hh * (Wm.x - Wm.y);
+        const T lo = Wk.x * Ab.x - Wk.y * Ab.y + u * Bb.x - vv * Bb.y;
+        const T hi = Wk.x * Bb.x - Wk.y * Bb.y + vv * Ab.x + u * Ab.y;
+        trow[kb + 32 * k2] = lo; trow[M + kb + 32 * k2] = hi;
+      }
+    }
+    bar_rt<8>();
+    T* __restrict__ out = c.t2;                        // T2[row][cv]: 64-byte segments of 16 v-order columns
+#pragma unroll
+    for (int it = 0; it < L / 256; ++it) {
+      const int row = it * 256 + threadIdx.x;
+      float v16[16];
+#pragma unroll
+      for (int i = 0; i < NL; ++i) v16[i] = tile[i * TROW + row];
+      float4* o4 = reinterpret_cast<float4*>(out + (int64_t)row * L + tileidx * NL);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) o4[q] = make_float4(v16[4 * q], v16[4 * q + 1], v16[4 * q + 2], v16[4 * q + 3]);
+    }
+    bar_rt<8>();
+  }
 }
 
 // ---------------------------------------------------------------- pass C
@@ -1014,9 +1160,27 @@ cofem_status dct1k_setup(Ctx* c) {
     cudaMemcpy(c->tab1k64, h64.data(), h64.size() * sizeof(h64[0]), cudaMemcpyHostToDevice);
   }
   if (cudaMalloc(&c->maskL, (size_t)L * 32 * sizeof(uint32_t)) != cudaSuccess) { c->err = "cudaMalloc maskL"; return COFEM_ERR_OOM; }
+  if (cudaMalloc(&c->maskH, (size_t)L * 16 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&c->twh, (size_t)d1kh::TWTOT * sizeof(cplx<float>)) != cudaSuccess) {
+    c->err = "cudaMalloc half-warp FFT tables"; return COFEM_ERR_OOM;
+  }
+  {   // W_512^{t k1} in both layouts of fft512h.cuh (fp64 -> fp32)
+    std::vector<cplx<float>> hw(d1kh::TWTOT);
+    const double PI = 3.14159265358979323846;
+    for (int k1 = 0; k1 < 32; ++k1)
+      for (int t = 0; t < 16; ++t) {
+        const double ang = -2.0 * PI * t * k1 / 512.0;
+        const cplx<float> w{(float)cos(ang), (float)sin(ang)};
+        hw[d1kh::TWK + k1 * 16 + t] = w;
+        hw[d1kh::TWT + t * 32 + k1] = w;
+      }
+    cudaMemcpy(c->twh, hw.data(), hw.size() * sizeof(hw[0]), cudaMemcpyHostToDevice);
+  }
   launch_begin(c, KC_SETUP);
   k1k_mask_lanes<<<L * 32 / 256, 256, 0, c->stream>>>(c->mask_vvT, c->maskL);
+  k1k_mask_half<<<L * 16 / 256, 256, 0, c->stream>>>(c->mask_vvT, (unsigned long long*)c->maskH);
   launch_end(c, KC_SETUP);
+  cudaFuncSetAttribute(k1k_cols_h, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)colsh::SMEM);
   set_attrs<float>();
   set_attrs<double>();
   {   // dataflow probe kernel: dispenser state and rho' partials (allocated here: E-steps are captured)
@@ -1084,6 +1248,15 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
       a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_COLS, st);
+#ifdef COFEM_1K_COLS_HALF   // experiment build: the half-warp FFT column pass (measured slower)
+  if constexpr (sizeof(T) == 4) {
+    const int items = ncols * colsh::NTH;
+    int g = grid_of((const void*)k1k_cols_h, colsh::SMEM);
+    g = std::min(g, items);
+    k1k_cols_h<<<std::max(1, g), 256, colsh::SMEM, st>>>(a, j0, ncols, (const unsigned long long*)c->maskH,
+                                                         (const cplx<float>*)c->twh);
+  } else
+#endif
   k1k_cols<T><<<grid_of((const void*)k1k_cols<T>, sm), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_COLS, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
