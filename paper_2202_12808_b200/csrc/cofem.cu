@@ -17,6 +17,8 @@
 
 #include <algorithm>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for profilers (no cost without a tool)
+
 #include "internal.cuh"
 
 namespace cofem {
@@ -1273,7 +1275,9 @@ cofem_status cofem_setup(cofem_ctx* out, const cofem_operator* op, const float* 
   *out = nullptr;
   cofem_ctx ctx = new cofem_ctx_s();
   ctx->c.stream = (cudaStream_t)cuda_stream;
+  nvtxRangePushA("cofem_setup");
   cofem_status st = setup_impl(&ctx->c, op, y, beta, opt);
+  nvtxRangePop();
   if (st != COFEM_OK) {
     g_err = ctx->c.err;
     free_all(&ctx->c);
@@ -1322,7 +1326,10 @@ cofem_status cofem_estep(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t
                          int32_t k_offset, int32_t K_total, double* mu, double* s) {
   if (!ctx) { g_err = "ctx is NULL"; return COFEM_ERR_INVALID; }
   ctx->c.err.clear();
-  return estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, mu, s);
+  nvtxRangePushA("cofem_estep");
+  const cofem_status st = estep_impl(&ctx->c, alpha, K, seed, t, k_offset, K_total, mu, s);
+  nvtxRangePop();
+  return st;
 }
 
 cofem_status cofem_estep_probes(cofem_ctx ctx, const double* alpha, int32_t K, uint64_t seed, int32_t t,
@@ -1442,6 +1449,8 @@ cofem_status cofem_em(cofem_ctx ctx, int32_t iters, int32_t K, uint64_t seed, in
   const bool m_dev = mu_out && is_device_ptr(mu_out);
   const bool s_dev = s_out && is_device_ptr(s_out);
   for (int i = 0; i < iters; ++i) {
+    nvtxRangePushA("cofem EM iteration");
+    struct PopAtExit { ~PopAtExit() { nvtxRangePop(); } } pop_at_exit;
     CK(cudaEventRecord(c->ev0, c->stream));
     int m = K + 1;
     c->warm_now = c->opt.warm_start && i > 0;          // R20: from the previous E-step's mu (x0)

@@ -548,3 +548,40 @@ def test_multitask_em_matches_oracle(w):
     ctx.em_multi(torch.as_tensor(Y[:1], device="cuda"), T, w.K, 6, 0, None, a1, m1, s1)
     ref = gpu_em(ctx_of(w), w, T, w.K, 6)
     assert np.array_equal(a1.cpu().numpy(), ref[0]) and np.array_equal(m1.cpu().numpy(), ref[1])
+
+
+def test_round2_option_validation():
+    """The round-2 options reject what they do not support (COFEM_ERR_INVALID = 1, UNSUPPORTED = 6):
+    bad option values, warm start or multi-task in sharded / probe-parallel contexts, probe-parallel
+    calls with a local k_offset, cofem_estep_probes in the probe-parallel mode, L < 1."""
+    from paper_2202_12808_b200 import OP_DENSE, CofemError, Context, get_unique_id
+    w = SMALL[1]
+    for kw in ({"apply_path": 2}, {"probe_groups": 9}, {"dist_mode": 2}, {"warm_start": 1, "d_offset": 0,
+                                                                          "D_global": w.D, "nccl_id": None}):
+        bad = dict(kw)
+        if bad.get("nccl_id", 1) is None:
+            bad["nccl_id"] = get_unique_id()
+            bad["world"], bad["rank"] = 1, 0
+        with pytest.raises(CofemError) as e:
+            ctx_of(w, **bad)
+        assert e.value.status in (1, 6)
+    pp = ctx_of(w, rank=0, world=1, nccl_id=get_unique_id(), dist_mode=1)
+    a = torch.ones(w.D, dtype=torch.float64, device="cuda")
+    mu, s = dev(w.D), dev(w.D)
+    with pytest.raises(CofemError) as e:
+        pp.estep(a, w.K, 1, 0, mu, s, k_offset=2, K_total=w.K + 2)
+    assert e.value.status == 1
+    with pytest.raises(CofemError) as e:
+        pp.estep_probes(a, w.K, 1, 0, s)
+    assert e.value.status == 1
+    Y, _ = synth.tasks(w, 2, seed=1)
+    with pytest.raises(CofemError) as e:
+        pp.em_multi(torch.as_tensor(Y, device="cuda"), 1, w.K, 1, 0, None, dev(w.D), None, None)
+    assert e.value.status == 6
+    ws = ctx_of(w, warm_start=True)
+    with pytest.raises(CofemError) as e:
+        ws.em_multi(torch.as_tensor(Y, device="cuda"), 1, w.K, 1, 0, None, dev(w.D), None, None)
+    assert e.value.status == 6
+    ok = ctx_of(w)
+    with pytest.raises((CofemError, ValueError)):
+        ok.em_multi(torch.empty((0, w.N), dtype=torch.float32, device="cuda"), 1, w.K, 1)
