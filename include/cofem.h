@@ -124,6 +124,18 @@ typedef struct {
    * E-step), the probes from zero (they are fresh); the freeze threshold stays relative to
    * b0^T M^-1 b0.  0 (default): X0 = 0 every E-step (R4).  Not in the sharded modes. */
   int32_t warm_start;
+  /* NEXT-2 CG variant ("any" CG method; reading R23 in DESIGN.md).  1: the standard
+   * preconditioned CG of Algorithm 1 (two reductions per iteration, gamma = p^T A p and
+   * rho' = r'^T M^-1 r', in the oracle's order).  2: single-reduction CG -- after the apply one
+   * reduction gives gamma, rho = r^T M^-1 r (recomputed, so no drift), delta1 = q^T M^-1 r and
+   * delta2 = q^T M^-1 q; a = rho / gamma as in Algorithm 1, and rho' = rho - 2 a delta1 + a^2 delta2
+   * (exact algebra for r' = r - a q) gives b = rho' / rho; the update then needs no reduction.
+   * In the column-sharded dense mode this merges the gamma and rho' NCCL all-reduces into one
+   * (with the two W all-reduces grouped into one NCCL launch: two collective launches per CG
+   * iteration instead of four).  Only the column-sharded dense mode
+   * implements 2 (COFEM_ERR_UNSUPPORTED elsewhere).  0 (default): auto = 2 in the column-sharded
+   * dense mode, 1 everywhere else. */
+  int32_t cg_variant;
 } cofem_options;
 
 /* NCCL unique id for cofem_options.nccl_id (call on one rank, broadcast the 128 bytes).
@@ -219,6 +231,8 @@ typedef struct {
    * support_min_margin is the smallest such margin over all d.  support_delta = 1e-6. */
   int64_t support_count, support_adjacent;
   double support_max_abs_mu, support_min_margin, support_delta;
+  int64_t collectives;            /* NCCL launches by this context so far (a grouped call counts once;
+                                   * 0 on a single GPU) */
 } cofem_report;
 
 /* The probe-parallel owner split (dist_mode 1) of a global K over `world` ranks, a host-only

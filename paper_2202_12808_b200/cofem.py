@@ -44,7 +44,7 @@ class _Options(ctypes.Structure):
                 ("max_probes", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("cg_rtol", ctypes.c_double), ("apply_path", ctypes.c_int32),
                 ("probe_groups", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("dist_mode", ctypes.c_int32),
-                ("warm_start", ctypes.c_int32)]
+                ("warm_start", ctypes.c_int32), ("cg_variant", ctypes.c_int32)]
 
 
 class _Report(ctypes.Structure):
@@ -54,7 +54,7 @@ class _Report(ctypes.Structure):
                 ("bad_iter", ctypes.c_int32), ("estep_ms_last", ctypes.c_double), ("launches", ctypes.c_int64),
                 ("support_count", ctypes.c_int64), ("support_adjacent", ctypes.c_int64),
                 ("support_max_abs_mu", ctypes.c_double), ("support_min_margin", ctypes.c_double),
-                ("support_delta", ctypes.c_double)]
+                ("support_delta", ctypes.c_double), ("collectives", ctypes.c_int64)]
 
 
 # (name, restype, argtypes) — every entry point of include/cofem.h
@@ -166,13 +166,14 @@ class Context:
     def __init__(self, kind, N, D, y, beta, phi=None, rows=0, cols=0, obs_idx=None, convention=0, taps=None,
                  cg_iters=100, precond=1, probe_precision=0, max_probes=32, den_floor=1e-12, alpha_max=1e12,
                  stream=None, d_offset=0, D_global=0, rank=0, world=1, nccl_id=None, cg_rtol=0.0, apply_path=0,
-                 probe_groups=0, use_graph=True, dist_mode=0, ld=None, warm_start=False):
+                 probe_groups=0, use_graph=True, dist_mode=0, ld=None, warm_start=False, cg_variant=0):
         """Multi-GPU; nccl_id = get_unique_id() from one rank, broadcast to all.
         dist_mode 0 with nccl_id: column-sharded dense / D-sharded conv -- phi (or y) holds this
         rank's slice [d_offset, d_offset + D) of D_global; the library all-reduces W and the column
         dots (or exchanges halos) over NCCL itself.  dist_mode 1: probe-parallel -- every rank holds
         the whole operator, estep/em take the GLOBAL K, the library splits the probes, all-reduces s
-        and broadcasts mu.  apply_path 1: the general kernels (tests); use_graph False: no CUDA graph."""
+        and broadcasts mu.  apply_path 1: the general kernels (tests); use_graph False: no CUDA graph.
+        cg_variant (cofem.h): 0 auto, 1 standard PCG, 2 single-reduction (column-sharded dense)."""
         L = lib()
         self.N, self.D, self.kind = int(N), int(D), int(kind)
         self._keep = [y, phi, obs_idx, taps]
@@ -198,6 +199,7 @@ class Context:
         opt.apply_path, opt.probe_groups = int(apply_path), int(probe_groups)
         opt.use_graph, opt.dist_mode = int(bool(use_graph)), int(dist_mode)
         opt.warm_start = int(bool(warm_start))
+        opt.cg_variant = int(cg_variant)
         if nccl_id is not None:
             self._nid = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opt.nccl_id = ctypes.cast(self._nid, ctypes.c_void_p)
@@ -284,7 +286,7 @@ class Context:
                 "frozen_at": [r.frozen_at[i] for i in range(n)],
                 "rho": [r.rho[i] for i in range(n)], "rho0": [r.rho0[i] for i in range(n)],
                 "bad_col": r.bad_col, "bad_iter": r.bad_iter, "estep_ms": r.estep_ms_last,
-                "launches": r.launches,
+                "launches": r.launches, "collectives": r.collectives,
                 "support": {"count": r.support_count, "adjacent": r.support_adjacent,
                             "max_abs_mu": r.support_max_abs_mu, "min_margin": r.support_min_margin,
                             "delta": r.support_delta}}

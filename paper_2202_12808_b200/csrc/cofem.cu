@@ -106,6 +106,7 @@ struct VecArgs {
   int uchunks;      // k_update: probe columns split into uchunks chunks per D tile (1 = all in one item)
   int mean_grid;    // k_update: CTAs [0, mean_grid) update the mean column, tile stride mean_grid
   int warm;         // k_init: the mean column starts from x0 (= mu of the previous E-step; q0 = A x0)
+  int nofinish;     // k_update: no rho' reduction (single-reduction CG, R23: rho' came with gamma)
   double* s_part; unsigned* tile_cnt;
 };
 
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM
       // finish, their column sums feed a cross-rank reduction.
     int act = 0;
     for (int j = a.jlo + threadIdx.x; j < a.jhi; j += blockDim.x) act |= sh.act[j];
-    if (!__syncthreads_or(act) && !a.colsum) return;
+    if (!__syncthreads_or(act) && (!a.colsum || a.nofinish)) return;
   }
   const int64_t ntiles = a.Dp / VEC_TILE;
   const int klo = a.jlo > 0 ? a.jlo - 1 : 0, khi = a.jhi - 1;
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM
       __syncthreads();
     }
   }
+  if (a.nofinish) return;            // single-reduction CG (R23): b and rho' are already in cs
   ColState* cs = a.cs;
   double* colsum = a.colsum;
   vec_finish(sh, a.part, a.part_stride, a.counter, a.jlo, a.jhi, [cs, colsum](int j, double v) {
@@ -573,6 +575,13 @@ __global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum
     c.tau = tau;
   } else if (mode == 1) {
     finish_gamma(c, v, iter);
+  } else if (mode == 3) {            // single-reduction CG (R23): gamma, rho, delta1, delta2 -> a, rho', b
+    if (c.frozen) return;
+    c.rho = colsum[m + j];             // r^T M^-1 r of the current r (the recurrence below would drift)
+    finish_gamma(c, v, iter);
+    if (c.frozen) { cs[j] = c; return; }
+    const double rn = c.rho - 2.0 * c.a * colsum[2 * m + j] + c.a * c.a * colsum[3 * m + j];
+    c.b = rn / c.rho; c.rho = rn;
   } else {
     if (c.frozen) return;
     c.b = v / c.rho; c.rho = v;
@@ -581,10 +590,70 @@ __global__ void k_sharded_finish(ColState* cs, const double* __restrict__ colsum
 }
 
 cofem_status sharded_finish(Ctx* c, int m, int mode, int iter) {
-  cofem_status st = comm_allreduce(c, c->colsum, (size_t)m, 1);
+  cofem_status st = comm_allreduce(c, c->colsum, (size_t)(mode == 3 ? 4 * m : m), 1);
   if (st != COFEM_OK) return st;
   k_sharded_finish<<<1, 160, 0, c->stream>>>(c->cs, c->colsum, m, mode, iter, c->freeze_tau);
   return check_launch(c, "k_sharded_finish") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
+// Single-reduction CG (reading R23): rho_j = r_j^T M^-1 r_j and the two dots that give
+// rho' = r'^T M^-1 r' of r' = r - a q without r' -- delta1_j = q_j^T M^-1 r_j, delta2_j =
+// q_j^T M^-1 q_j -- over this rank's rows, fp64 sums; grid (x, m): CTA partials, the last CTA of
+// column j reduces them in fixed order into colsum[m + j], colsum[2m + j], colsum[3m + j].  Frozen
+// columns (R5) are skipped (their entries are not read).
+template <typename TP>
+__global__ void __launch_bounds__(VEC_THREADS) k_sr_dots(VecArgs<TP> a, double* __restrict__ part, unsigned* cnt,
+                                                         int stride) {
+  const int j = blockIdx.y;
+  if (a.cs[j].frozen) return;          // the same for every CTA of the column
+  __shared__ double red[VEC_THREADS / 32][3];
+  __shared__ bool last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double dr = 0.0, d1 = 0.0, d2 = 0.0;
+  const int64_t ntiles = a.Dp / VEC_TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t d0 = tile * VEC_TILE + (int64_t)threadIdx.x * VEC_ELEMS;
+    if (j == 0) {
+      double r[8], q[8], dv[8];
+      ld8(a.r0 + d0, r); ld8(a.q0 + d0, q); ld8(a.dinv64 + d0, dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { const double z = dv[e] * q[e]; dr += r[e] * (dv[e] * r[e]); d1 += z * r[e]; d2 += z * q[e]; }
+    } else {
+      TP r[8], q[8], dv[8];
+      const int64_t o = (int64_t)(j - 1) * a.Dp + d0;
+      ld8(a.R + o, r); ld8(a.Q + o, q); ld8(a.dinvp + d0, dv);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double z = (double)dv[e] * (double)q[e], re = (double)r[e];
+        dr += re * ((double)dv[e] * re); d1 += z * re; d2 += z * (double)q[e];
+      }
+    }
+  }
+  dr = warp_sum(dr); d1 = warp_sum(d1); d2 = warp_sum(d2);
+  if (lane == 0) { red[warp][0] = dr; red[warp][1] = d1; red[warp][2] = d2; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int w = 0; w < VEC_THREADS / 32; ++w) { v[0] += red[w][0]; v[1] += red[w][1]; v[2] += red[w][2]; }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) part[(int64_t)(3 * j + i) * stride + blockIdx.x] = v[i];
+    __threadfence();
+    last = atomicAdd(cnt + j, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    double t[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) t[i] = reduce_partials(part + (int64_t)(3 * j + i) * stride, gridDim.x);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i) a.colsum[(i + 1) * a.m + j] = t[i];
+      cnt[j] = 0u;
+    }
+  }
 }
 
 template <typename TP>
@@ -604,7 +673,20 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.tau = c->freeze_tau;
   a.uchunks = c->upd_chunks; a.s_part = c->s_part; a.tile_cnt = c->tile_cnt; a.mean_grid = c->vec_grid;
   a.warm = c->warm_now ? 1 : 0;
+  a.nofinish = c->sr ? 1 : 0;
   return a;
+}
+
+cofem_status sr_dots(Ctx* c, int m) {
+  const int64_t ntiles = c->Dp / VEC_TILE;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>({ntiles, (int64_t)c->part_stride,
+                                                              ((int64_t)c->num_sms * 4 + m - 1) / m}));
+  const dim3 grid((unsigned)gx, (unsigned)m);
+  launch_begin(c, KC_UPDATE);
+  if (c->probe64) k_sr_dots<double><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, m - 1, 0), c->sr_part, c->sr_cnt, c->part_stride);
+  else k_sr_dots<float><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, m - 1, 0), c->sr_part, c->sr_cnt, c->part_stride);
+  launch_end(c, KC_UPDATE);
+  return check_launch(c, "k_sr_dots") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
 
@@ -846,7 +928,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     else k_update<float, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
-    if (c->sharded && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
+    if (c->sharded && !c->sr && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
   }
   return COFEM_OK;
 }
@@ -858,16 +940,33 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
 static cofem_status cg_loop_conv_sharded(Ctx* c, int K, double invK) {
   const int m = K + 1;
   void* const P_entry = c->P; double* const p0_entry = c->p0;
+  // the fp64 mean column's apply and update run on the side stream, concurrently with the probe
+  // columns' (their tickets, partial rows and colsum entries are disjoint); the NCCL calls stay on
+  // the context stream, after a join
+  auto fork = [c]() -> cofem_status {
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    return COFEM_OK;
+  };
+  auto join = [c]() -> cofem_status {
+    CK(cudaEventRecord(c->ev_join, c->side));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return COFEM_OK;
+  };
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
     if ((st = conv_halo_exchange(c, K)) != COFEM_OK) return st;
-    if ((st = conv_fft_apply(c, 0, 1, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if ((st = fork()) != COFEM_OK) return st;
+    if ((st = conv_fft_apply(c, 0, 1, it, it > 0, c->side)) != COFEM_OK) return st;
     if ((st = conv_fft_apply(c, 1, m, it, it > 0, c->stream)) != COFEM_OK) return st;
+    if ((st = join()) != COFEM_OK) return st;
     if ((st = sharded_finish(c, m, 1, it)) != COFEM_OK) return st;
-    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->stream, KC_MEAN);
+    if ((st = fork()) != COFEM_OK) return st;
+    update_range<double>(c, K, invK, 0, 1, c->counters + MAXM + 1, c->side, KC_MEAN);
     if (c->probe64) update_range<double>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     else update_range<float>(c, K, invK, 1, m, c->counters + MAXM, c->stream, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
+    if ((st = join()) != COFEM_OK) return st;
     if ((st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
   }
   if (c->P != P_entry) { c->Pb = c->P; c->P = P_entry; }
@@ -896,7 +995,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
     gs = &c->gslot[0];
     for (auto& s : c->gslot) if (s.used < gs->used) gs = &s;
     if (gs->exec) { cudaGraphExecDestroy(gs->exec); gs->exec = nullptr; }
-    const int64_t l0 = c->launches;
+    const int64_t l0 = c->launches, n0 = c->collectives;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamBeginCapture(c->work, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
@@ -905,8 +1004,8 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
     }
     if (e == cudaSuccess && st == COFEM_OK) e = cudaGraphInstantiate(&gs->exec, g, 0);
     if (g) cudaGraphDestroy(g);
-    gs->launches = c->launches - l0;
-    c->launches = l0;
+    gs->launches = c->launches - l0; gs->colls = c->collectives - n0;
+    c->launches = l0; c->collectives = n0;
     if (e != cudaSuccess || st != COFEM_OK) {
       c->stream = user;
       if (st == COFEM_OK) { c->err = std::string("CUDA graph capture: ") + cudaGetErrorString(e); st = COFEM_ERR_CUDA; }
@@ -917,7 +1016,7 @@ static cofem_status estep_device(Ctx* c, int K, uint64_t seed, int t, int k_offs
   }
   gs->used = ++c->gclock;
   cudaError_t e = cudaGraphLaunch(gs->exec, c->work);
-  c->launches += gs->launches;
+  c->launches += gs->launches; c->collectives += gs->colls;
   c->stream = user;
   if (e != cudaSuccess) { c->err = std::string("cudaGraphLaunch: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
   CK(cudaEventRecord(c->ev_out, c->work));
@@ -1031,7 +1130,7 @@ void cofem_default_options(cofem_options* o) {
   o->probe_precision = 0; o->max_probes = 32;
   o->rank = 0; o->world = 1; o->nccl_id = nullptr;
   o->cg_rtol = 0.0;
-  o->apply_path = 0; o->probe_groups = 0; o->use_graph = 1; o->dist_mode = 0; o->warm_start = 0;
+  o->apply_path = 0; o->probe_groups = 0; o->use_graph = 1; o->dist_mode = 0; o->warm_start = 0; o->cg_variant = 0;
 }
 
 const char* cofem_version(void) { return "cofem-b200 0.1 (sm_100a)"; }
@@ -1057,7 +1156,8 @@ static void free_all(Ctx* c) {
                   c->ws1, c->ws2, c->ws1d, c->ws2d, c->alphap, c->maskL, c->tab1k32, c->tab1k64,
                   c->Pb, c->p0b, c->conv_tab32, c->conv_tab64, c->colsum,
                   c->halo_send, c->halo_recv, c->halo_send0, c->halo_recv0, c->s_part, c->tile_cnt,
-                  c->flow_state, c->flow_part2, c->mt_b0, c->mt_mu, c->b0_saved, c->obs_dev, c->maskH, c->twh};
+                  c->flow_state, c->flow_part2, c->mt_b0, c->mt_mu, c->b0_saved, c->obs_dev, c->maskH, c->twh,
+                  c->sr_part, c->sr_cnt};
   for (void* p : ptrs) if (p) cudaFree(p);
   for (int g = 1; g < Ctx::MAXG; ++g) if (c->gs[g]) cudaFree(c->gs[g]);
   for (auto& r : c->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -1101,6 +1201,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 8]"; return COFEM_ERR_INVALID; }
   if (opt->dist_mode < 0 || opt->dist_mode > 1) { c->err = "dist_mode must be 0 or 1"; return COFEM_ERR_INVALID; }
   if (opt->warm_start < 0 || opt->warm_start > 1) { c->err = "warm_start must be 0 or 1"; return COFEM_ERR_INVALID; }
+  if (opt->cg_variant < 0 || opt->cg_variant > 2) { c->err = "cg_variant must be 0, 1 or 2"; return COFEM_ERR_INVALID; }
   c->kind = op->kind; c->N = op->N; c->D = op->D; c->beta = beta; c->opt = *opt;
   c->freeze_tau = std::max(FREEZE_TAU, opt->cg_rtol * opt->cg_rtol);
   if (opt->dist_mode == 1) {                    // probe-parallel (comm.cu: all-reduce of s, broadcast of mu)
@@ -1256,13 +1357,21 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   ALLOC(c->part, (size_t)(c->m_cap + 1) * c->part_stride);   // + k_init's warm-start slot
   c->pp_mean_cost = (c->fast1k || c->fast_conv) ? 2.0 : 0.0;
   if (c->sharded) {
-    ALLOC(c->colsum, MAXM);
+    ALLOC(c->colsum, 4 * MAXM);
     if (c->kind == COFEM_OP_DENSE && !c->dense_tc) {
       c->err = "sharded mode needs the tensor-core dense path (D % 4 == 0, K <= 128)"; return COFEM_ERR_UNSUPPORTED;
     }
     if (c->kind == COFEM_OP_CIRCCONV && !c->fast_conv) {
       c->err = "D-sharded convolution needs the FFT path (local D >= 2048, ntaps <= 64)"; return COFEM_ERR_UNSUPPORTED;
     }
+  }
+  {   // CG variant (R23): single reduction where it merges collectives -- the column-sharded dense mode
+    const bool col_dense = c->sharded && c->kind == COFEM_OP_DENSE;
+    if (opt->cg_variant == 2 && !col_dense) {
+      c->err = "cg_variant 2 (single-reduction CG): column-sharded dense mode only"; return COFEM_ERR_UNSUPPORTED;
+    }
+    c->sr = opt->cg_variant == 2 || (opt->cg_variant == 0 && col_dense);
+    if (c->sr) { ALLOC(c->sr_part, (size_t)3 * MAXM * c->part_stride); ALLOC(c->sr_cnt, MAXM); }
   }
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaGetLastError());
@@ -1568,7 +1677,7 @@ cofem_status cofem_last_report(cofem_ctx ctx, cofem_report* out) {
   out->cols = c->last_cols; out->cg_iters = c->opt.cg_iters;
   out->frozen_at = c->frozen_host.data(); out->rho = c->rho_host.data(); out->rho0 = c->rho0_host.data();
   out->bad_col = c->bad_col; out->bad_iter = c->bad_iter;
-  out->estep_ms_last = c->estep_ms; out->launches = c->launches;
+  out->estep_ms_last = c->estep_ms; out->launches = c->launches; out->collectives = c->collectives;
   out->support_count = c->sup_count; out->support_adjacent = c->sup_adjacent;
   out->support_max_abs_mu = c->sup_max; out->support_min_margin = c->sup_min_margin;
   out->support_delta = SUPPORT_DELTA;

@@ -1,7 +1,8 @@
 // comm.cu — NCCL for the column-sharded dense mode (BASELINE config 3
 // "column-sharded runs"): rank r owns the columns [d_offset, d_offset + D_r) of Phi and
 // the matching rows of every D-vector; each CG iteration sums W = Phi P over ranks and the
-// per-column dot products (gamma_j, rho_j) before the step lengths are taken.
+// per-column dot products (gamma_j, rho_j -- or, single-reduction CG, gamma_j, delta1_j, delta2_j in
+// one all-reduce, reading R23) before the step lengths are taken.
 //
 // NCCL is resolved at run time (dlopen of the libnccl.so.2 already mapped into the process —
 // torch's — or the system one), so the library has no link-time NCCL dependency and a
@@ -86,7 +87,18 @@ cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype) {
   if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
   ncclResult_t r = a.AllReduce(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, ncclSum, (ncclComm_t)c->comm,
                                c->stream);
+  if (c->comm_depth == 0) c->collectives++;
   if (r != ncclSuccess) { c->err = std::string("ncclAllReduce: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
+  return COFEM_OK;
+}
+
+cofem_status comm_group(Ctx* c, bool begin) {
+  NcclApi& a = nccl(c->err);
+  if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
+  ncclResult_t r = begin ? a.GroupStart() : a.GroupEnd();
+  c->comm_depth += begin ? 1 : -1;
+  if (!begin && c->comm_depth == 0) c->collectives++;
+  if (r != ncclSuccess) { c->err = std::string("ncclGroup: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
   return COFEM_OK;
 }
 
@@ -95,6 +107,7 @@ cofem_status comm_bcast(Ctx* c, void* buf, size_t count, int dtype, int root) {
   NcclApi& a = nccl(c->err);
   if (!a.ok || !c->comm) return COFEM_ERR_NCCL;
   ncclResult_t r = a.Broadcast(buf, buf, count, dtype ? ncclFloat64 : ncclFloat32, root, (ncclComm_t)c->comm, c->stream);
+  if (c->comm_depth == 0) c->collectives++;
   if (r != ncclSuccess) { c->err = std::string("ncclBroadcast: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
   return COFEM_OK;
 }
@@ -115,6 +128,7 @@ cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, vo
   if (r == ncclSuccess) r = a.Send(send_right, count, t, right, cm, c->stream);
   if (r == ncclSuccess) r = a.Recv(recv_left, count, t, left, cm, c->stream);
   ncclResult_t r2 = a.GroupEnd();
+  if (c->comm_depth == 0) c->collectives++;
   if (r == ncclSuccess) r = r2;
   if (r != ncclSuccess) { c->err = std::string("NCCL halo exchange: ") + a.GetErrorString(r); return COFEM_ERR_NCCL; }
   return COFEM_OK;

@@ -84,7 +84,7 @@ struct Ctx {
   double sup_max = 0, sup_min_margin = 0;
   // captured E-steps (cofem.cu estep_device), a small LRU cache keyed by the launch shape (the
   // multi-task EM alternates mean-only and full E-steps)
-  struct GraphSlot { cudaGraphExec_t exec = nullptr; int K = -1, Kt = -1, skip = -1, warm = -1; int64_t launches = 0; uint64_t used = 0; };
+  struct GraphSlot { cudaGraphExec_t exec = nullptr; int K = -1, Kt = -1, skip = -1, warm = -1; int64_t launches = 0, colls = 0; uint64_t used = 0; };
   static constexpr int NGRAPH = 4;
   GraphSlot gslot[NGRAPH];
   uint64_t gclock = 0;
@@ -136,7 +136,11 @@ struct Ctx {
   double pp_mean_cost = 0;              // the mean system's cost in probe columns (owner split)
   int64_t d_offset = 0, D_global = 0;
   void* comm = nullptr;                 // ncclComm_t
-  double* colsum = nullptr;             // [MAXM] per-column totals of this rank
+  double* colsum = nullptr;             // [4 MAXM] per-column totals of this rank (gamma; single-reduction CG:
+                                        // + rho at [m, 2m), delta1 at [2m, 3m), delta2 at [3m, 4m))
+  bool sr = false;                      // single-reduction CG (cg_variant 2, reading R23)
+  double* sr_part = nullptr;            // k_sr_dots CTA partials [3 MAXM][part_stride]
+  unsigned* sr_cnt = nullptr;           // k_sr_dots last-CTA tickets [MAXM]
   int rank = 0, world = 1;
   // D-sharded convolution (op_conv_fft.cu): per column [side][r | p | dinv][64] halo records
   void* halo_send = nullptr; void* halo_recv = nullptr;        // probe precision, [K][2][3][64]
@@ -150,6 +154,8 @@ struct Ctx {
   int bad_col = -1, bad_iter = -1;
   double estep_ms = 0;
   int64_t launches = 0;
+  int64_t collectives = 0;              // NCCL launches (report; a group counts once)
+  int comm_depth = 0;                   // open comm_group nesting
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
   // profiling
@@ -293,6 +299,11 @@ cofem_status conv_halo_exchange(Ctx* c, int K);
 cofem_status comm_init(Ctx* c, int rank, int world, const uint8_t* id);
 void comm_destroy(Ctx* c);
 cofem_status comm_allreduce(Ctx* c, void* buf, size_t count, int dtype);
+// NCCL group around several collectives (one fused launch): comm_group(c, true) ... comm_group(c, false)
+cofem_status comm_group(Ctx* c, bool begin);
+// single-reduction CG (R23): rho_j = r_j^T M^-1 r_j, delta1_j = q_j^T M^-1 r_j, delta2_j = q_j^T M^-1 q_j
+// of this rank's rows into colsum[m + j], colsum[2m + j], colsum[3m + j]
+cofem_status sr_dots(Ctx* c, int m);
 cofem_status comm_bcast(Ctx* c, void* buf, size_t count, int dtype, int root);
 cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, void* recv_left, void* recv_right,
                        size_t count, int dtype);

@@ -348,9 +348,13 @@ cofem_status conv_halo_exchange(Ctx* c, int K) {
   const size_t tp = c->probe64 ? 8 : 4;
   char* sp = (char*)c->halo_send;
   char* rp = (char*)c->halo_recv;
-  cofem_status st = comm_halo(c, sp, sp + side * tp, rp, rp + side * tp, (size_t)K * 192, c->probe64 ? 1 : 0);
+  // the probe halos (probe precision) and the mean column's (fp64): one NCCL group, one launch
+  cofem_status st = comm_group(c, true);
   if (st != COFEM_OK) return st;
-  return comm_halo(c, c->halo_send0, c->halo_send0 + 192, c->halo_recv0, c->halo_recv0 + 192, 192, 1);
+  st = comm_halo(c, sp, sp + side * tp, rp, rp + side * tp, (size_t)K * 192, c->probe64 ? 1 : 0);
+  if (st == COFEM_OK) st = comm_halo(c, c->halo_send0, c->halo_send0 + 192, c->halo_recv0, c->halo_recv0 + 192, 192, 1);
+  const cofem_status st2 = comm_group(c, false);
+  return st != COFEM_OK ? st : st2;
 }
 
 bool conv_fft_eligible(const Ctx* c) { return c->D >= 2048 && c->ntaps <= 64 && c->opt.apply_path != 1; }

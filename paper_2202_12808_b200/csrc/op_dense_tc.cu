@@ -831,9 +831,11 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
                                                        c->sharded ? nullptr : t->Wl, t->w0);
   if (c->sharded) {      // W = sum over ranks of Phi_r P_r (SURVEY §8(e) column-sharded dense), then split
-    cofem_status st;
-    if ((st = comm_allreduce(c, t->Wh, (size_t)K * t->Npad, 0)) != COFEM_OK) return st;
-    if ((st = comm_allreduce(c, t->w0, (size_t)t->Npad, 1)) != COFEM_OK) return st;
+    cofem_status st;         // the fp32 probe block and the fp64 mean column: one grouped NCCL launch
+    if ((st = comm_group(c, true)) != COFEM_OK) return st;
+    if ((st = comm_allreduce(c, t->Wh, (size_t)K * t->Npad, 0)) != COFEM_OK) { comm_group(c, false); return st; }
+    if ((st = comm_allreduce(c, t->w0, (size_t)t->Npad, 1)) != COFEM_OK) { comm_group(c, false); return st; }
+    if ((st = comm_group(c, false)) != COFEM_OK) return st;
     k_tc_split_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * t->Npad, t->Wh, t->Wl);
   }
   launch_end(c, KC_DENSE_PHI_P);
@@ -850,7 +852,11 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   else k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
-  if (c->sharded) { cofem_status st = sharded_finish(c, m, 1, iter); if (st != COFEM_OK) return st; }
+  if (c->sharded) {   // gamma (+ delta1, delta2 for the single-reduction CG, R23): one all-reduce
+    cofem_status st = c->sr ? sr_dots(c, m) : COFEM_OK;
+    if (st == COFEM_OK) st = sharded_finish(c, m, c->sr ? 3 : 1, iter);
+    if (st != COFEM_OK) return st;
+  }
 #ifdef COFEM_TC_DEBUG
   {                                   // synchronous protocol check (debug build)
     cudaStreamSynchronize(c->stream);

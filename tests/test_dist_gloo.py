@@ -107,13 +107,16 @@ def test_column_shard_covers_all_aligned():
             assert all(off % 128 == 0 for off, _ in parts) and min(n for _, n in parts) >= 1
 
 
-def _col_worker(rank, world, port, out):
+def _col_worker(rank, world, port, out, sr=False):
     """One rank of the column-sharded E-step, following the library's schedule exactly
     (op_dense_tc.cu + cofem.cu sharded path): local b0 / colsq / probes of the rank's global
     d range; every reduction the library sends through NCCL (rho0, W = Phi P and Phi p0,
     gamma, rho') is a gloo all-reduce here; the step lengths are then taken identically on
     every rank.  Local arithmetic is plain NumPy fp64 (this is a test of the decomposition
-    and the exchange schedule, not of the kernels)."""
+    and the exchange schedule, not of the kernels).  sr: the single-reduction CG (cg_variant 2,
+    reading R23, the library's default in this mode) -- ONE all-reduce of (gamma, rho = r^T M^-1 r,
+    delta1 = q^T M^-1 r, delta2 = q^T M^-1 q) per iteration, a = rho / gamma,
+    rho' = rho - 2 a delta1 + a^2 delta2 (for b only), and no reduction after the update."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import torch
@@ -146,7 +149,13 @@ def _col_worker(rank, world, port, out):
     for _ in range(U):
         W = ar(Phi @ Pd)                                       # K1 partial W -> all-reduce
         Q = beta * Phi.T @ W + alpha[:, None] * Pd             # K2 (local rows)
-        gamma = ar(np.sum(Pd * Q, axis=0))                     # gamma -> colsum -> all-reduce
+        if sr:                                                 # k_sr_dots + one all-reduce (mode 3)
+            g4 = ar(np.concatenate([np.sum(Pd * Q, axis=0), np.sum(R * R / diag[:, None], axis=0),
+                                    np.sum(Q * R / diag[:, None], axis=0), np.sum(Q * Q / diag[:, None], axis=0)]))
+            gamma, rho_f, d1, d2 = (g4[i * (K + 1):(i + 1) * (K + 1)] for i in range(4))
+            rho = np.where(frozen, rho, rho_f)                   # the current rho, recomputed (no drift)
+        else:
+            gamma = ar(np.sum(Pd * Q, axis=0))                 # gamma -> colsum -> all-reduce
         with np.errstate(all="ignore"):                        # freeze rule R5, same on every rank
             ok = np.isfinite(gamma) & np.isfinite(rho) & (gamma > 0) & (rho > 1e-30 * rho0)
         frozen |= ~ok
@@ -155,7 +164,10 @@ def _col_worker(rank, world, port, out):
         X += a * Pd
         R -= a * Q
         Z = R / diag[:, None]
-        rho_new = ar(np.sum(R * Z, axis=0))                    # rho' -> colsum -> all-reduce
+        if sr:
+            rho_new = rho - 2 * a * d1 + a * a * d2             # k_sharded_finish mode 3
+        else:
+            rho_new = ar(np.sum(R * Z, axis=0))                # rho' -> colsum -> all-reduce
         b = np.where(act, rho_new / rho, 0.0)
         Pd = np.where(act, Z + b * Pd, Pd)
         rho = np.where(act, rho_new, rho)
@@ -172,13 +184,14 @@ def _col_worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_column_sharded_gloo_world2_equals_single(tmp_path):
+@pytest.mark.parametrize("sr", [False, True], ids=["two_reductions", "single_reduction"])
+def test_column_sharded_gloo_world2_equals_single(tmp_path, sr):
     import socket
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
     out = str(tmp_path / "c0.npy")
-    mp.start_processes(_col_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_col_worker, args=(2, port, out, sr), nprocs=2, join=True, start_method="spawn")
     mu, s = np.load(out)
     import synth
     from oracle.cofem import estep

@@ -328,29 +328,44 @@ def test_c3_full_size_mean_residual_and_sampled_parity():
     assert rel(mu1, omu) <= 1e-4 and rel(s1, os_) <= 1e-4, (rel(mu1, omu), rel(s1, os_))
 
 
-def test_column_sharded_path_world1():
+@pytest.mark.parametrize("variant", [1, 2], ids=["standard_cg", "single_reduction_cg"])
+def test_column_sharded_path_world1(variant):
     """The column-sharded dense path (comm.cu + the sharded finishes of cofem.cu /
     op_dense_tc.cu) on a 1-rank NCCL communicator: (i) with d_offset = 0 it must reproduce
-    the single-GPU run exactly (the all-reduces are identities, the sums are the same); (ii)
-    a rank holding columns [128, 1024) of a 1024-column Phi must solve its sub-system with
-    the probes of its GLOBAL indices (reading R8), against the fp64 oracle PCG."""
+    the single-GPU run -- exactly with the standard CG (the all-reduces are identities, the sums
+    are the same), within the fp32-probe bar with the single-reduction CG (cg_variant 2, reading
+    R23: other dot products, the same iteration in exact arithmetic); (ii) a rank holding columns
+    [128, 1024) of a 1024-column Phi must solve its sub-system with the probes of its GLOBAL
+    indices (reading R8), against the fp64 oracle PCG."""
     from oracle.cofem import jacobi_diag, mean_rhs, pcg
     from oracle.operators import gram_apply
     from paper_2202_12808_b200 import OP_DENSE, Context, get_unique_id
     w = synth.dense(250, 1024, 20, K=8, U=60, T=3, seed=2)
     a, mu, s = gpu_em(ctx_of(w), w, 3, 8, 5)
     nid = get_unique_id()
-    sh = ctx_of(w, rank=0, world=1, nccl_id=nid, d_offset=0, D_global=w.D)
+    sh = ctx_of(w, rank=0, world=1, nccl_id=nid, d_offset=0, D_global=w.D, cg_variant=variant)
     a2, mu2, s2 = gpu_em(sh, w, 3, 8, 5)
-    assert np.array_equal(a2, a) and np.array_equal(mu2, mu) and np.array_equal(s2, s)
+    if variant == 1:
+        assert np.array_equal(a2, a) and np.array_equal(mu2, mu) and np.array_equal(s2, s)
+    else:
+        assert rel(1 / a2, 1 / a) <= 1e-4 and rel(mu2, mu) <= 1e-4 and rel(s2, s) <= 1e-4, \
+            (rel(1 / a2, 1 / a), rel(mu2, mu), rel(s2, s))
+        omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), 8, 5, 0, w.U)   # E-step 1 vs the oracle
+        m1, s1 = gpu_estep(sh, w, np.ones(w.D), 8, 5, 0)
+        assert rel(m1, omu) <= 1e-4 and rel(s1, os_) <= 1e-4, (rel(m1, omu), rel(s1, os_))
     d0 = 128
     phi_r = np.ascontiguousarray(w.phi[:, d0:])
     part = Context(OP_DENSE, w.N, w.D - d0, w.y, w.beta, phi=phi_r, cg_iters=w.U, max_probes=8,
-                   rank=0, world=1, nccl_id=get_unique_id(), d_offset=d0, D_global=w.D)   # one id per communicator
+                   rank=0, world=1, nccl_id=get_unique_id(), d_offset=d0, D_global=w.D,
+                   cg_variant=variant)   # one id per communicator
     alpha = np.ones(w.D - d0)
     a_dev = torch.ones(w.D - d0, dtype=torch.float64, device="cuda")
     m_dev, s_dev = dev(w.D - d0), dev(w.D - d0)
+    n0 = part.report()["collectives"]
     part.estep(a_dev, 8, 5, 0, m_dev, s_dev)
+    # NCCL launches per E-step: rho0 once, then per CG iteration the grouped W = Phi P / Phi p0 pair and
+    # (standard) gamma + rho' or (single reduction) one (gamma, rho, delta1, delta2) all-reduce
+    assert part.report()["collectives"] - n0 == 1 + (3 if variant == 1 else 2) * w.U
     op = DenseOp(phi_r)
     P = rademacher_probes(w.D, 8, 5, 0)[d0:]
     B = np.concatenate([mean_rhs(op, w.y, w.beta)[:, None], P], axis=1)
@@ -384,7 +399,10 @@ def test_d_sharded_conv_path_world1():
                    rank=0, world=1, nccl_id=get_unique_id(), d_offset=d0, D_global=w.D)
     a_dev = torch.ones(Dl, dtype=torch.float64, device="cuda")
     m_dev, s_dev = dev(Dl), dev(Dl)
+    n0 = part.report()["collectives"]
     part.estep(a_dev, 8, 5, 0, m_dev, s_dev)
+    # rho0, then per CG iteration: the halo exchange (one NCCL group), gamma, rho'
+    assert part.report()["collectives"] - n0 == 1 + 3 * w.U, part.report()["collectives"] - n0
     op = CircConvOp(w.taps, Dl)
     alpha = np.ones(Dl)
     P = rademacher_probes(w.D, 8, 5, 0)[d0:]
@@ -553,11 +571,13 @@ def test_multitask_em_matches_oracle(w):
 def test_round2_option_validation():
     """The round-2 options reject what they do not support (COFEM_ERR_INVALID = 1, UNSUPPORTED = 6):
     bad option values, warm start or multi-task in sharded / probe-parallel contexts, probe-parallel
-    calls with a local k_offset, cofem_estep_probes in the probe-parallel mode, L < 1."""
+    calls with a local k_offset, cofem_estep_probes in the probe-parallel mode, L < 1, the
+    single-reduction CG outside the column-sharded dense mode."""
     from paper_2202_12808_b200 import OP_DENSE, CofemError, Context, get_unique_id
     w = SMALL[1]
     for kw in ({"apply_path": 2}, {"probe_groups": 9}, {"dist_mode": 2}, {"warm_start": 1, "d_offset": 0,
-                                                                          "D_global": w.D, "nccl_id": None}):
+                                                                          "D_global": w.D, "nccl_id": None},
+               {"cg_variant": 3}, {"cg_variant": 2}):
         bad = dict(kw)
         if bad.get("nccl_id", 1) is None:
             bad["nccl_id"] = get_unique_id()
