@@ -56,6 +56,15 @@ template <typename T> __device__ __forceinline__ CCol<T> ccol(const ConvArgs& a,
   return {(const T*)a.P + o, (T*)a.Pn + o, (const T*)a.R + o, (const T*)a.dinvp, al, (T*)a.Q + o};
 }
 
+// two consecutive samples of the window (positions 2n, 2n+1 = packed point n), one 8- / 16-byte access
+template <typename T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+
+#ifndef COFEM_CONV_VEC
+#define COFEM_CONV_VEC 1     // 0: every window through the general per-sample path (A/B switch)
+#endif
+
 #ifndef COFEM_CONV_STASH
 #define COFEM_CONV_STASH 0   // 1: fp32 interior windows keep the updated p of their valid outputs in shared memory (3 CTAs/SM: C5 196 -> 214 ms, not kept)
 #endif
@@ -120,8 +129,35 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
       } else { hal = (const T*)a.halo + (int64_t)(j - 1) * 192; hside = a.halo_side; }
     }
     const T bb = (T)ci.b[jj];
-    // ---- load the window as packed complex z[n] (n = ja + 64 r, jb + 64 r), fused direction update
+    // interior window of a full block (no wrap, no halo records, V valid outputs): packed point n
+    // is one vector access at w0 + 2n; the valid outputs [64, 960) are the points n in [32, 480):
+    // slot a (n = ja + 64 r) for r >= 1, slot b (n = jb + 64 r) for r <= 6, for every lane.  The
+    // pointers do not alias (P / Pn ping-pong, R, 1/diag, alpha, Q), so loads of later points are
+    // issued ahead of earlier points' stores (the general path below serialises them).
+    using V2 = typename Vec2<T>::type;
+    const bool vfast = COFEM_CONV_VEC && !COFEM_CONV_STASH && fast && !hal && nvalid == V;
     cplx<T> va[8], vb[8];
+    if (vfast) {
+      const V2* __restrict__ p2 = reinterpret_cast<const V2*>(c.p + w0);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const V2 xa = p2[ja + 64 * r], xb = p2[jb + 64 * r];
+        va[r] = {xa.x, xa.y}; vb[r] = {xb.x, xb.y};
+      }
+      if (dir) {                                                        // a6: p = M^-1 r + b p
+        const V2* __restrict__ r2 = reinterpret_cast<const V2*>(c.r + w0);
+        const V2* __restrict__ d2 = reinterpret_cast<const V2*>(c.dinv + w0);
+        V2* __restrict__ pn2 = reinterpret_cast<V2*>(c.pn + w0);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const V2 ra = r2[ja + 64 * r], da = d2[ja + 64 * r], rb = r2[jb + 64 * r], db = d2[jb + 64 * r];
+          va[r].x = da.x * ra.x + bb * va[r].x; va[r].y = da.y * ra.y + bb * va[r].y;
+          vb[r].x = db.x * rb.x + bb * vb[r].x; vb[r].y = db.y * rb.y + bb * vb[r].y;
+          if (r >= 1) { V2 o; o.x = va[r].x; o.y = va[r].y; pn2[ja + 64 * r] = o; }   // own positions only
+          if (r <= 6) { V2 o; o.x = vb[r].x; o.y = vb[r].y; pn2[jb + 64 * r] = o; }
+        }
+      }
+    } else
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
 #pragma unroll
@@ -161,7 +197,8 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
         if (sl) vb[r] = {x0, x1}; else va[r] = {x0, x1};
       }
     }
-    if (st2) {                       // valid outputs: stash p (same lane reads it back), p_new as float2
+    if (vfast) {
+    } else if (st2) {                // valid outputs: stash p (same lane reads it back), p_new as float2
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -207,7 +244,24 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
     const T beta = (T)a.beta;
     const T* pcur = dir ? c.pn : c.p;                                   // p of this iteration (own block: just written)
     double g = 0.0;
-    if (st2) {                       // p from the stash, alpha / q as float2
+    if (vfast) {                     // vector epilogue over the 14 valid (r, slot) pairs of every lane
+      const V2* __restrict__ pc2 = reinterpret_cast<const V2*>(pcur + w0);
+      const V2* __restrict__ al2 = reinterpret_cast<const V2*>(c.al + w0);
+      V2* __restrict__ q2 = reinterpret_cast<V2*>(c.q + w0);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+          if (sl ? r > 6 : r < 1) continue;
+          const int n = (sl ? jb : ja) + 64 * r;
+          const cplx<T> y = sl ? vb[r] : va[r];
+          const V2 pv = pc2[n], av = al2[n];
+          V2 qv;
+          qv.x = beta * y.x + av.x * pv.x; qv.y = beta * y.y + av.y * pv.y;          // a3
+          q2[n] = qv;
+          g += (double)pv.x * (double)qv.x + (double)pv.y * (double)qv.y;            // a4
+        }
+    } else if (st2) {                // p from the stash, alpha / q as float2
 #pragma unroll
       for (int r = 0; r < 8; ++r)
 #pragma unroll
