@@ -65,6 +65,12 @@ template <> struct Vec2<double> { using type = double2; };
 #define COFEM_CONV_VEC 1     // 0: every window through the general per-sample path (A/B switch)
 #endif
 
+#ifndef COFEM_CONV_RB
+#define COFEM_CONV_RB 4      // vector path: window points per slot whose r and 1/diag loads are batched
+                             // (C5 fixed-alpha E-step: 1 139.5 ms, 2 136.4, 4 135.2, 8 135.2; an L2
+                             // prefetch of each warp's next window on top: 148 ms, not kept)
+#endif
+
 #ifndef COFEM_CONV_STASH
 #define COFEM_CONV_STASH 0   // 1: fp32 interior windows keep the updated p of their valid outputs in shared memory (3 CTAs/SM: C5 196 -> 214 ms, not kept)
 #endif
@@ -148,13 +154,24 @@ __global__ void __launch_bounds__(NW * 32, COFEM_CONV_MINB) k_conv_fft(ConvArgs 
         const V2* __restrict__ r2 = reinterpret_cast<const V2*>(c.r + w0);
         const V2* __restrict__ d2 = reinterpret_cast<const V2*>(c.dinv + w0);
         V2* __restrict__ pn2 = reinterpret_cast<V2*>(c.pn + w0);
+        // r and 1/diag in batches of RB points per slot, all of a batch's loads before its stores
+        constexpr int RB = COFEM_CONV_RB;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const V2 ra = r2[ja + 64 * r], da = d2[ja + 64 * r], rb = r2[jb + 64 * r], db = d2[jb + 64 * r];
-          va[r].x = da.x * ra.x + bb * va[r].x; va[r].y = da.y * ra.y + bb * va[r].y;
-          vb[r].x = db.x * rb.x + bb * vb[r].x; vb[r].y = db.y * rb.y + bb * vb[r].y;
-          if (r >= 1) { V2 o; o.x = va[r].x; o.y = va[r].y; pn2[ja + 64 * r] = o; }   // own positions only
-          if (r <= 6) { V2 o; o.x = vb[r].x; o.y = vb[r].y; pn2[jb + 64 * r] = o; }
+        for (int h = 0; h < 8; h += RB) {
+          V2 ra[RB], da[RB], rb[RB], db[RB];
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            ra[i] = r2[ja + 64 * (h + i)]; da[i] = d2[ja + 64 * (h + i)];
+            rb[i] = r2[jb + 64 * (h + i)]; db[i] = d2[jb + 64 * (h + i)];
+          }
+#pragma unroll
+          for (int i = 0; i < RB; ++i) {
+            const int r = h + i;
+            va[r].x = da[i].x * ra[i].x + bb * va[r].x; va[r].y = da[i].y * ra[i].y + bb * va[r].y;
+            vb[r].x = db[i].x * rb[i].x + bb * vb[r].x; vb[r].y = db[i].y * rb[i].y + bb * vb[r].y;
+            if (r >= 1) { V2 o; o.x = va[r].x; o.y = va[r].y; pn2[ja + 64 * r] = o; }   // own positions only
+            if (r <= 6) { V2 o; o.x = vb[r].x; o.y = vb[r].y; pn2[jb + 64 * r] = o; }
+          }
         }
       }
     } else
