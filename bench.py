@@ -158,6 +158,8 @@ def algorithmic_bytes(cls, w, K_local, D_local=None):
         return w.N * D * 4 + D * (8 * K + 16 + 8)
     if cls == "dense_phi_p":
         return w.N * D * 4 + D * (4 * K + 8)
+    if cls == "dense_cluster":     # the whole CG loop in one cluster: Phi and the state once per E-step
+        return w.N * D * 4 + D * (12 * K + 64)
     return None
 
 
@@ -372,7 +374,8 @@ def main():
     # ---- device-timed region (inputs resident in HBM; the library replays one captured
     # CUDA graph per E-step)
     classes = ["dct_rows_inv", "dct_cols", "dct_rows_fwd", "pcg_update", "pcg_direction", "conv_apply",
-               "dense_phi_p", "dense_phiT_w", "pcg_init", "probe_bits", "finalize_mstep", "mean_column"]
+               "dense_phi_p", "dense_phiT_w", "pcg_init", "probe_bits", "finalize_mstep", "mean_column",
+               "dense_cluster"]
     # the profiled pass and the e2e pass below replay exactly these EM iterations (same t, same
     # starting alpha): later iterations freeze more columns and run faster
     t_timed, alpha_timed = t, alpha.clone()
@@ -570,6 +573,22 @@ def main():
                             "(probe classes; the fp64 mean column is not counted)"},
             "share_of_step": share, "busy_share_of_step": busy_share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
             args.prof_steps}
+    if dom == "dense_cluster":
+        # the whole CG loop in one 8-CTA cluster, state in shared memory (op_dense_cluster.cu): the
+        # bound is FP32 issue and the cluster barriers, not memory.  FP32 SIMT peak = SMs x 128 lanes
+        # x 2 flop x max SM clock (B200_PROFILING unit counts); the kernel runs on 8 SMs by design
+        probe_ex = sum(sum(w.U if f < 0 else min(f + 1, w.U) for f in fz[1:]) for fz in frozen)
+        props = torch.cuda.get_device_properties(local)
+        fmax = (clocks or {}).get("sm_max_mhz") or 1965.0
+        fp32_peak = props.multi_processor_count * 128 * 2 * fmax * 1e6 / 1e12
+        fl = 2 * 2 * w.N * D * probe_ex
+        ach = fl / (busy_ms / 1000.0) / 1e12
+        roof.update({"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": ach / fp32_peak, "peak_source": "%d SMs x 128 FP32 lanes x 2 x %.0f MHz" %
+                     (props.multi_processor_count, fmax),
+                     "frac_of_cluster_sms": ach / (fp32_peak * 8 / props.multi_processor_count),
+                     "achieved_def": "FP32 flops of the probe columns' two products (2 x 2 N D per executed "
+                                     "column-iteration; the fp64 mean column not counted) / busy time"})
     if w.kind == "dense" and flush is not None:
         # Phi fits in L2 (C1, C2): the dense GEMMs are bound by the tensor pipe, not HBM.  3xTF32 =
         # 3 tf32 MMAs per product, 2 N D flops per column per GEMM; tf32 peak = measured bf16 x 1/2

@@ -26,7 +26,7 @@ namespace cofem {
 static const char* kClassNames[KC_COUNT] = {
     "probe_bits", "pcg_init", "pcg_direction", "pcg_update", "finalize_mstep",
     "dense_phi_p", "dense_phiT_w", "dct_rows_inv", "dct_cols", "dct_rows_fwd",
-    "conv_apply", "mean_column", "setup", "dct_flow"};
+    "conv_apply", "mean_column", "setup", "dct_flow", "dense_cluster"};
 
 // ------------------------------------------------------------------ bookkeeping
 static cudaEvent_t pool_get(Ctx* c) {
@@ -911,6 +911,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
 #ifdef COFEM_1K_FLOW   // experiment build: the dataflow probe kernel (measured slower)
   if (c->fast1k && !c->probe64) return cg_loop_flow(c, K, K_total, invK);
 #endif
+  if (c->dense_cluster) return dense_cluster_cg(c, K, invK);
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
   if (c->fast_conv && c->sharded) return cg_loop_conv_sharded(c, K, invK);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
@@ -1197,7 +1198,7 @@ static cofem_status setup_impl(Ctx* c, const cofem_operator* op, const float* y,
   if (!(opt->cg_rtol >= 0.0 && opt->cg_rtol < 1.0)) { c->err = "cg_rtol must be in [0, 1)"; return COFEM_ERR_INVALID; }
   if (opt->max_probes < 1 || opt->max_probes + 1 > MAXM) { c->err = "max_probes must be in [1, 128]"; return COFEM_ERR_INVALID; }
   if (opt->den_floor <= 0 || opt->alpha_max <= 0) { c->err = "den_floor and alpha_max must be > 0"; return COFEM_ERR_INVALID; }
-  if (opt->apply_path < 0 || opt->apply_path > 1) { c->err = "apply_path must be 0 or 1"; return COFEM_ERR_INVALID; }
+  if (opt->apply_path < 0 || opt->apply_path > 2) { c->err = "apply_path must be 0, 1 or 2"; return COFEM_ERR_INVALID; }
   if (opt->probe_groups < 0 || opt->probe_groups > Ctx::MAXG) { c->err = "probe_groups must be in [0, 8]"; return COFEM_ERR_INVALID; }
   if (opt->dist_mode < 0 || opt->dist_mode > 1) { c->err = "dist_mode must be 0 or 1"; return COFEM_ERR_INVALID; }
   if (opt->warm_start < 0 || opt->warm_start > 1) { c->err = "warm_start must be 0 or 1"; return COFEM_ERR_INVALID; }

@@ -22,7 +22,7 @@ enum KernelClass : int {
   KC_PROBES = 0, KC_INIT, KC_DIR, KC_UPDATE, KC_FINAL,
   KC_DENSE_PHI_P, KC_DENSE_PHIT_W,
   KC_DCT_ROWS_INV, KC_DCT_COLS, KC_DCT_ROWS_FWD,
-  KC_CONV_APPLY, KC_MEAN, KC_SETUP, KC_DCT_FLOW, KC_COUNT
+  KC_CONV_APPLY, KC_MEAN, KC_SETUP, KC_DCT_FLOW, KC_DENSE_CLUSTER, KC_COUNT
 };
 
 // Per-column CG scalars (device).  Column 0 = mean system (R2).
@@ -130,6 +130,7 @@ struct Ctx {
   double* ws1d = nullptr; double* ws2d = nullptr;   // mean-column scratch
   int dense_splits = 1;
   void* dense_tc = nullptr;             // tensor-core dense path state (op_dense_tc.cu), NULL: SIMT
+  bool dense_cluster = false;           // small dense: the CG loop in one thread-block cluster (op_dense_cluster.cu)
   // column-sharded dense mode (comm.cu): per-column sums go through colsum + an NCCL all-reduce
   bool sharded = false;
   bool pp = false;                      // probe-parallel mode (dist_mode 1): probes split over ranks
@@ -275,6 +276,9 @@ __device__ __forceinline__ double block_sum(double v) {
 // every apply computes Q = A P for all active columns and finishes gamma_j / a_j.
 cofem_status dense_setup(Ctx* c, const float* y_dev);
 cofem_status dense_apply(Ctx* c, int m, int iter);
+bool dense_cluster_eligible(const Ctx* c);
+cofem_status dense_cluster_setup(Ctx* c);
+cofem_status dense_cluster_cg(Ctx* c, int K, double invK);
 cofem_status dense_tc_setup(Ctx* c);
 cofem_status dense_tc_apply(Ctx* c, int m, int iter);
 void dense_tc_free(Ctx* c);

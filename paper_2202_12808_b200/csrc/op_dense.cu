@@ -243,7 +243,9 @@ cofem_status dense_setup(Ctx* c, const float* y_dev) {
     cudaFuncSetAttribute(k_dense_phiP<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
     cudaFuncSetAttribute(k_dense_phiTW<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
   }
-  return dense_tc_setup(c);
+  cofem_status st = dense_tc_setup(c);
+  if (st == COFEM_OK && dense_cluster_eligible(c)) st = dense_cluster_setup(c);
+  return st;
 }
 
 template <typename TP>

@@ -1,0 +1,365 @@
+// op_dense_cluster.cu — the whole CG loop of a SMALL dense problem (Alg. 1 lines 3-7 after the
+// probes and k_init; BASELINE config 1, N x D = 100 x 400) in ONE thread-block cluster.
+//
+// At this size every kernel of the per-iteration path (W = Phi P, Q = beta Phi^T W + alpha o P,
+// the update, the direction) is a few microseconds of latency around almost no work, so the graph
+// of ~6 launches per CG iteration costs ~46 us per iteration (C1).  Here the NC CTAs of one cluster
+// each hold a column slice of Phi (and the matching rows of every vector) in shared memory for the
+// whole E-step, and the three reductions of a CG iteration run through distributed shared memory
+// (DSMEM) between cluster barriers instead of through HBM and kernel boundaries:
+//   W = sum_c Phi_c P_c     : each CTA writes its partial [N][K], then CTA c sums rows [c N/NC, ..)
+//                             over the NC partials in fixed order and stores them into EVERY CTA's W
+//   gamma_j, rho'_j         : per-CTA partials, every CTA sums the NC partials in fixed order and
+//                             takes the same step lengths / freeze decisions (R5) on its own copy
+// Four cluster barriers per CG iteration, no global memory traffic inside the loop.
+//
+// Arithmetic mirrors the SIMT kernels (op_dense.cu) and k_update / k_dir (cofem.cu): probe columns
+// in probe precision TP with fp32 Phi, the mean column in fp64 (fp32 Phi promoted exactly), gamma,
+// rho', s in fp64; the same freeze rule (finish_gamma).  Used when the problem fits one cluster's
+// shared memory (dense_cluster_eligible), cofem_options.apply_path = 0, single GPU / probe-parallel.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace cofem {
+namespace dcl {
+
+namespace cg = cooperative_groups;
+
+#ifndef COFEM_DCL_EXP
+#define COFEM_DCL_EXP 0   // timing experiments only (results invalid): 1 no GEMM loops, 2 also no DSMEM W
+#endif
+#ifndef COFEM_DCL_NC
+#define COFEM_DCL_NC 8
+#endif
+#ifndef COFEM_DCL_THREADS
+#define COFEM_DCL_THREADS 256
+#endif
+#ifndef COFEM_DCL_KG
+#define COFEM_DCL_KG 8
+#endif
+constexpr int NC = COFEM_DCL_NC;            // CTAs per cluster (8: the portable maximum)
+constexpr int THREADS = COFEM_DCL_THREADS;
+constexpr int KG = COFEM_DCL_KG;            // probe columns per thread work unit (register accumulators)
+
+struct Args {
+  const float* phi; int64_t ld;
+  int N, D, Dc, DcP, K, U;
+  double beta, invK;
+  const double* alpha; const double* dinv64; const void* dinvp;
+  double* x0; const double* r0; const double* p0;
+  const void* R; const void* P;
+  double* s; const uint32_t* bits; int64_t Dp, wpc;
+  ColState* cs;
+};
+
+// Shared-memory layout (bytes, 16-aligned pieces), sized for K probe columns.
+struct Layout {
+  size_t phi, Pp, Rp, Qp, dvp, x, r, p, q, dv, al, sacc, wpart, wfull, w0part, w0full, gpart, rpart, cs, sgn, total;
+};
+__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+__host__ __device__ inline Layout layout(int N, int Dc, int DcP, int K, size_t tp) {
+  Layout L;
+  size_t o = 0;
+  L.phi = o; o = al16(o + (size_t)N * DcP * 4);
+  L.Pp = o; o = al16(o + (size_t)K * Dc * tp);
+  L.Rp = o; o = al16(o + (size_t)K * Dc * tp);
+  L.Qp = o; o = al16(o + (size_t)K * Dc * tp);
+  L.dvp = o; o = al16(o + (size_t)Dc * tp);
+  L.x = o; o = al16(o + (size_t)Dc * 8);
+  L.r = o; o = al16(o + (size_t)Dc * 8);
+  L.p = o; o = al16(o + (size_t)Dc * 8);
+  L.q = o; o = al16(o + (size_t)Dc * 8);
+  L.dv = o; o = al16(o + (size_t)Dc * 8);
+  L.al = o; o = al16(o + (size_t)Dc * 8);
+  L.sacc = o; o = al16(o + (size_t)Dc * 8);
+  L.wpart = o; o = al16(o + (size_t)N * K * tp);
+  L.wfull = o; o = al16(o + (size_t)N * K * tp);
+  L.w0part = o; o = al16(o + (size_t)N * 8);
+  L.w0full = o; o = al16(o + (size_t)N * 8);
+  L.gpart = o; o = al16(o + (size_t)(K + 1) * 8);
+  L.rpart = o; o = al16(o + (size_t)(K + 1) * 8);
+  L.cs = o; o = al16(o + (size_t)(K + 1) * sizeof(ColState));
+  L.sgn = o; o = al16(o + (size_t)K * Dc);
+  L.total = o;
+  return L;
+}
+
+template <typename TP>
+__global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cluster_cg(Args a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const int N = a.N, K = a.K, m = K + 1, Dc = a.Dc, DcP = a.DcP;
+  const Layout L = layout(N, Dc, DcP, K, sizeof(TP));
+  float* phs = reinterpret_cast<float*>(smraw + L.phi);     // [N][DcP]
+  TP* Ps = reinterpret_cast<TP*>(smraw + L.Pp);             // [K][Dc]
+  TP* Rs = reinterpret_cast<TP*>(smraw + L.Rp);
+  TP* Qs = reinterpret_cast<TP*>(smraw + L.Qp);
+  TP* dvp = reinterpret_cast<TP*>(smraw + L.dvp);           // [Dc] 1/diag in probe precision
+  double* xs = reinterpret_cast<double*>(smraw + L.x);      // mean column [Dc]
+  double* rs = reinterpret_cast<double*>(smraw + L.r);
+  double* ps = reinterpret_cast<double*>(smraw + L.p);
+  double* qs = reinterpret_cast<double*>(smraw + L.q);
+  double* dv = reinterpret_cast<double*>(smraw + L.dv);
+  double* als = reinterpret_cast<double*>(smraw + L.al);
+  double* sacc = reinterpret_cast<double*>(smraw + L.sacc);
+  TP* wpart = reinterpret_cast<TP*>(smraw + L.wpart);       // [N][K]
+  TP* wfull = reinterpret_cast<TP*>(smraw + L.wfull);
+  double* w0part = reinterpret_cast<double*>(smraw + L.w0part);
+  double* w0full = reinterpret_cast<double*>(smraw + L.w0full);
+  double* gpart = reinterpret_cast<double*>(smraw + L.gpart);
+  double* rpart = reinterpret_cast<double*>(smraw + L.rpart);
+  ColState* cs = reinterpret_cast<ColState*>(smraw + L.cs);
+  uint8_t* sgn = smraw + L.sgn;                             // [K][Dc] probe bit (1: -1) of this slice
+  const int warp = tid >> 5, lane = tid & 31;
+
+  // ---- this CTA's slice d in [d0, d0 + Dl) of Phi and of every vector (state after k_init)
+  const int d0 = rank * Dc;
+  const int Dl = max(0, min(Dc, a.D - d0));
+  for (int i = tid; i < N * DcP; i += THREADS) {
+    const int n = i / DcP, dl = i % DcP;
+    phs[i] = dl < Dl ? a.phi[(int64_t)n * a.ld + d0 + dl] : 0.0f;
+  }
+  const TP* Pg = reinterpret_cast<const TP*>(a.P);
+  const TP* Rg = reinterpret_cast<const TP*>(a.R);
+  const TP* dvg = reinterpret_cast<const TP*>(a.dinvp);
+  for (int i = tid; i < K * Dc; i += THREADS) {
+    const int k = i / Dc, dl = i % Dc;
+    const bool v = dl < Dl;
+    Ps[i] = v ? Pg[(int64_t)k * a.Dp + d0 + dl] : (TP)0;
+    Rs[i] = v ? Rg[(int64_t)k * a.Dp + d0 + dl] : (TP)0;
+    Qs[i] = (TP)0;
+    const int d = d0 + dl;
+    sgn[i] = v ? (uint8_t)((a.bits[(int64_t)k * a.wpc + (d >> 5)] >> (d & 31)) & 1u) : (uint8_t)0;
+  }
+  for (int dl = tid; dl < Dc; dl += THREADS) {
+    const bool v = dl < Dl;
+    const int d = d0 + dl;
+    dvp[dl] = v ? dvg[d] : (TP)0;
+    xs[dl] = v ? a.x0[d] : 0.0; rs[dl] = v ? a.r0[d] : 0.0; ps[dl] = v ? a.p0[d] : 0.0; qs[dl] = 0.0;
+    dv[dl] = v ? a.dinv64[d] : 0.0; als[dl] = v ? a.alpha[d] : 0.0; sacc[dl] = v ? a.s[d] : 0.0;
+  }
+  for (int j = tid; j < m; j += THREADS) cs[j] = a.cs[j];
+  const int G = (K + KG - 1) / KG;                 // probe column groups
+  const int Nr = (N + NC - 1) / NC, n_lo = min(N, rank * Nr), n_hi = min(N, n_lo + Nr);
+  cl.sync();
+
+  for (int it = 0; it < a.U; ++it) {
+    // every column frozen (R5): nothing left to do (the state is the same in every CTA)
+    int act = 0;
+    for (int j = tid; j < m; j += THREADS) act |= !cs[j].frozen;
+    if (!__syncthreads_or(act)) break;
+    // ---- 1. W partial = Phi_c P_c (probe precision) and Phi_c p0 (fp64)
+    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : N * (G + 1)); u += THREADS) {
+      const int n = u % N, g = u / N;
+      const float* ph = phs + n * DcP;
+      if (g < G) {
+        const int k0 = g * KG;
+        TP acc[KG];
+#pragma unroll
+        for (int i = 0; i < KG; ++i) acc[i] = (TP)0;
+        for (int dl = 0; dl < Dl; ++dl) {
+          const TP f = (TP)ph[dl];
+#pragma unroll
+          for (int i = 0; i < KG; ++i)
+            if (k0 + i < K) acc[i] += f * Ps[(k0 + i) * Dc + dl];
+        }
+#pragma unroll
+        for (int i = 0; i < KG; ++i)
+          if (k0 + i < K) wpart[n * K + k0 + i] = acc[i];
+      } else {
+        double acc0 = 0.0;
+        for (int dl = 0; dl < Dl; ++dl) acc0 += (double)ph[dl] * ps[dl];
+        w0part[n] = acc0;
+      }
+    }
+    cl.sync();
+    // ---- 2. rows [n_lo, n_hi): sum the NC partials in rank order, store into every CTA's W
+    for (int i = tid; i < (COFEM_DCL_EXP >= 2 ? 0 : (n_hi - n_lo) * (K + 1)); i += THREADS) {
+      const int n = n_lo + i / (K + 1), k = i % (K + 1);
+      if (k < K) {
+        TP x[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(wpart, c)[n * K + k];
+        TP v = (TP)0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v += x[c];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cl.map_shared_rank(wfull, c)[n * K + k] = v;
+      } else {
+        double x[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(w0part, c)[n];
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v += x[c];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) cl.map_shared_rank(w0full, c)[n] = v;
+      }
+    }
+    cl.sync();
+    // ---- 3. Q = beta Phi_c^T W + alpha o P (a3), q0 likewise in fp64; gamma partials (a4)
+    const TP betat = (TP)a.beta;
+    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : Dl * (G + 1)); u += THREADS) {
+      const int dl = u % Dl, g = u / Dl;
+      if (g < G) {
+        const int k0 = g * KG;
+        TP acc[KG];
+#pragma unroll
+        for (int i = 0; i < KG; ++i) acc[i] = (TP)0;
+        for (int n = 0; n < N; ++n) {
+          const TP f = (TP)phs[n * DcP + dl];
+#pragma unroll
+          for (int i = 0; i < KG; ++i)
+            if (k0 + i < K) acc[i] += f * wfull[n * K + k0 + i];
+        }
+        const TP alt = (TP)als[dl];
+#pragma unroll
+        for (int i = 0; i < KG; ++i)
+          if (k0 + i < K) Qs[(k0 + i) * Dc + dl] = betat * acc[i] + alt * Ps[(k0 + i) * Dc + dl];
+      } else {
+        double acc0 = 0.0;
+        for (int n = 0; n < N; ++n) acc0 += (double)phs[n * DcP + dl] * w0full[n];
+        qs[dl] = a.beta * acc0 + als[dl] * ps[dl];
+      }
+    }
+    __syncthreads();
+    for (int j = warp; j < m; j += THREADS / 32) {   // one warp per column: lane-strided, then the tree
+      double g = 0.0;
+      if (j == 0) for (int dl = lane; dl < Dl; dl += 32) g += ps[dl] * qs[dl];
+      else for (int dl = lane; dl < Dl; dl += 32) g += (double)Ps[(j - 1) * Dc + dl] * (double)Qs[(j - 1) * Dc + dl];
+      g = warp_sum(g);
+      if (lane == 0) gpart[j] = g;
+    }
+    cl.sync();
+    // ---- 4. gamma_j over the cluster (rank order); freeze rule and a_j on every CTA's copy
+    for (int j = tid; j < m; j += THREADS) {
+      double x[NC], v = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(gpart, c)[j];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v += x[c];
+      if (COFEM_DCL_EXP == 0) finish_gamma(cs[j], v, it);
+    }
+    __syncthreads();
+    // ---- 5. a5: x0 += a0 p0, r -= a q, s += (a_k / K) p_k o z_k; rho' partials
+    for (int u = tid; u < K * Dl; u += THREADS) {
+      const int k = u / Dl, dl = u % Dl;
+      if (cs[k + 1].frozen) continue;
+      const TP akt = (TP)cs[k + 1].a;
+      Rs[k * Dc + dl] = Rs[k * Dc + dl] - akt * Qs[k * Dc + dl];
+    }
+    if (!cs[0].frozen) {
+      const double a0 = cs[0].a;
+      for (int dl = tid; dl < Dl; dl += THREADS) {
+        xs[dl] = fma(a0, ps[dl], xs[dl]);
+        rs[dl] = fma(-a0, qs[dl], rs[dl]);
+      }
+    }
+    for (int dl = tid; dl < Dl; dl += THREADS) {    // the probe estimator, columns in order (k_update)
+      double sv = 0.0;
+      bool any = false;
+      for (int k = 0; k < K; ++k) {
+        if (cs[k + 1].frozen) continue;
+        any = true;
+        const double aks = cs[k + 1].a * a.invK;
+        const double pe = (double)Ps[k * Dc + dl];
+        sv += sgn[k * Dc + dl] ? -aks * pe : aks * pe;
+      }
+      if (any) sacc[dl] += sv;
+    }
+    __syncthreads();
+    for (int j = warp; j < m; j += THREADS / 32) {
+      double v = 0.0;
+      if (!cs[j].frozen) {
+        if (j == 0) {
+          for (int dl = lane; dl < Dl; dl += 32) v += rs[dl] * (dv[dl] * rs[dl]);
+        } else {
+          const TP* rr = Rs + (j - 1) * Dc;
+          for (int dl = lane; dl < Dl; dl += 32) { const TP z = dvp[dl] * rr[dl]; v += (double)rr[dl] * (double)z; }
+        }
+      }
+      v = warp_sum(v);
+      if (lane == 0) rpart[j] = v;
+    }
+    cl.sync();
+    // ---- 6. rho'_j over the cluster; b_j; direction p = M^-1 r + b p (a6) for the next iteration
+    for (int j = tid; j < m; j += THREADS) {
+      if (cs[j].frozen) continue;
+      double x[NC], v = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(rpart, c)[j];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v += x[c];
+      cs[j].b = v / cs[j].rho;
+      cs[j].rho = v;
+    }
+    __syncthreads();
+    for (int u = tid; u < K * Dl; u += THREADS) {
+      const int k = u / Dl, dl = u % Dl;
+      if (cs[k + 1].frozen) continue;
+      const TP bt = (TP)cs[k + 1].b;
+      Ps[k * Dc + dl] = dvp[dl] * Rs[k * Dc + dl] + bt * Ps[k * Dc + dl];
+    }
+    if (!cs[0].frozen) {
+      const double b0 = cs[0].b;
+      for (int dl = tid; dl < Dl; dl += THREADS) ps[dl] = fma(b0, ps[dl], dv[dl] * rs[dl]);
+    }
+    __syncthreads();
+  }
+  // ---- results: mu slice, s slice; the column states (identical in every CTA) from rank 0
+  for (int dl = tid; dl < Dl; dl += THREADS) { a.x0[d0 + dl] = xs[dl]; a.s[d0 + dl] = sacc[dl]; }
+  if (rank == 0)
+    for (int j = tid; j < m; j += THREADS) a.cs[j] = cs[j];
+  cl.sync();                         // no CTA leaves while others may still read its shared memory
+}
+
+}  // namespace dcl
+
+static size_t dcl_smem(const Ctx* c, int K) {
+  const int Dc = (int)((c->D + dcl::NC - 1) / dcl::NC);
+  return dcl::layout((int)c->N, Dc, Dc | 1, K, c->probe64 ? 8 : 4).total;
+}
+
+bool dense_cluster_eligible(const Ctx* c) {
+  if (c->kind != COFEM_OP_DENSE || c->sharded || c->opt.apply_path != 0) return false;
+  if (c->D < dcl::NC || c->N > (1 << 16)) return false;
+  return dcl_smem(c, c->Kcap) <= (size_t)200 * 1024;
+}
+
+cofem_status dense_cluster_setup(Ctx* c) {
+  const int sm = (int)dcl_smem(c, c->Kcap);
+  if (dcl::NC > 8) {
+    cudaFuncSetAttribute(dcl::k_dense_cluster_cg<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(dcl::k_dense_cluster_cg<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  cudaError_t e = c->probe64
+      ? cudaFuncSetAttribute(dcl::k_dense_cluster_cg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)
+      : cudaFuncSetAttribute(dcl::k_dense_cluster_cg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  if (e != cudaSuccess) { c->err = std::string("dense cluster setup: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
+  c->dense_cluster = true;
+  return COFEM_OK;
+}
+
+// All U CG iterations of the E-step (state initialised by k_init) in one cluster launch.
+cofem_status dense_cluster_cg(Ctx* c, int K, double invK) {
+  dcl::Args a;
+  a.phi = c->phi; a.ld = c->ld; a.N = (int)c->N; a.D = (int)c->D;
+  a.Dc = (int)((c->D + dcl::NC - 1) / dcl::NC); a.DcP = a.Dc | 1; a.K = K; a.U = c->opt.cg_iters;
+  a.beta = c->beta; a.invK = invK;
+  a.alpha = c->alpha; a.dinv64 = c->dinv64; a.dinvp = c->dinvp;
+  a.x0 = c->x0; a.r0 = c->r0; a.p0 = c->p0; a.R = c->R; a.P = c->P;
+  a.s = c->s; a.bits = c->bits; a.Dp = c->Dp; a.wpc = c->Dp / 32; a.cs = c->cs;
+  const size_t sm = dcl::layout(a.N, a.Dc, a.DcP, K, c->probe64 ? 8 : 4).total;
+  launch_begin(c, KC_DENSE_CLUSTER);
+  if (c->probe64) dcl::k_dense_cluster_cg<double><<<dcl::NC, dcl::THREADS, sm, c->stream>>>(a);
+  else dcl::k_dense_cluster_cg<float><<<dcl::NC, dcl::THREADS, sm, c->stream>>>(a);
+  launch_end(c, KC_DENSE_CLUSTER);
+  return check_launch(c, "k_dense_cluster_cg") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
+}
+
+}  // namespace cofem

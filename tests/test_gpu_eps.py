@@ -114,9 +114,11 @@ def test_eps_through_the_sharded_finishes_world1():
     from paper_2202_12808_b200 import Context, get_unique_id
     for w, eps in ((synth.dense(250, 1024, 20, K=8, U=200, T=1, seed=2), 1e-4),
                    (synth.circconv(20000, 64, 20, K=8, U=600, T=1, seed=4), 1e-3)):
-        base = Context.from_workload(w, cg_rtol=eps)
+        # the same kernels on both sides: the per-iteration tensor-core path (apply_path 2; the dense
+        # 250 x 1024 problem would otherwise take the cluster CG loop) and the standard CG (cg_variant 1)
+        base = Context.from_workload(w, cg_rtol=eps, apply_path=2)
         sh = Context.from_workload(w, cg_rtol=eps, rank=0, world=1, nccl_id=get_unique_id(), d_offset=0,
-                                   D_global=w.D)
+                                   D_global=w.D, cg_variant=1)
         out = []
         for c in (base, sh):
             a = torch.ones(w.D, dtype=torch.float64, device="cuda")

@@ -341,7 +341,7 @@ def test_column_sharded_path_world1(variant):
     from oracle.operators import gram_apply
     from paper_2202_12808_b200 import OP_DENSE, Context, get_unique_id
     w = synth.dense(250, 1024, 20, K=8, U=60, T=3, seed=2)
-    a, mu, s = gpu_em(ctx_of(w), w, 3, 8, 5)
+    a, mu, s = gpu_em(ctx_of(w, apply_path=2), w, 3, 8, 5)   # the sharded mode's kernels (not the cluster loop)
     nid = get_unique_id()
     sh = ctx_of(w, rank=0, world=1, nccl_id=nid, d_offset=0, D_global=w.D, cg_variant=variant)
     a2, mu2, s2 = gpu_em(sh, w, 3, 8, 5)
@@ -575,7 +575,7 @@ def test_round2_option_validation():
     single-reduction CG outside the column-sharded dense mode."""
     from paper_2202_12808_b200 import OP_DENSE, CofemError, Context, get_unique_id
     w = SMALL[1]
-    for kw in ({"apply_path": 2}, {"probe_groups": 9}, {"dist_mode": 2}, {"warm_start": 1, "d_offset": 0,
+    for kw in ({"apply_path": 3}, {"probe_groups": 9}, {"dist_mode": 2}, {"warm_start": 1, "d_offset": 0,
                                                                           "D_global": w.D, "nccl_id": None},
                {"cg_variant": 3}, {"cg_variant": 2}):
         bad = dict(kw)
@@ -605,3 +605,36 @@ def test_round2_option_validation():
     ok = ctx_of(w)
     with pytest.raises((CofemError, ValueError)):
         ok.em_multi(torch.empty((0, w.N), dtype=torch.float32, device="cuda"), 1, w.K, 1)
+
+
+@pytest.mark.parametrize("w", [synth.preset("C1"), synth.dense(37, 203, 4, K=5, U=40, T=3, seed=8),
+                               synth.dense(64, 1000, 12, K=33, U=80, T=2, seed=9)], ids=lambda w: w.name)
+def test_dense_cluster_cg_loop(w):
+    """The small-dense CG loop in one thread-block cluster (op_dense_cluster.cu; DSMEM reductions,
+    uneven column slices at D = 203 and 1000, K > 32): against the fp64 oracle (fp32 probes 1e-4,
+    fp64 probes 1e-7 as test_parity_mode_fp64_probes: the unconverged fp64 mean moves 3e-9 on C1 on
+    every path) and against the per-iteration tensor-core kernels (apply_path 2) over an EM;
+    one cluster launch per E-step (plus the probe and init kernels)."""
+    ctx = ctx_of(w, max_probes=w.K)
+    mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 3, 1, w.U)
+    # fp32 probes: the north_star bar, or (reading R21) twice what the general FP32 SIMT kernels
+    # deviate where fp32 rounding in the unconverged CG moves s more (37 x 203: 5e-4 on every path)
+    m1, s1 = gpu_estep(ctx_of(w, max_probes=w.K, apply_path=1), w, np.ones(w.D), w.K, 3, 1)
+    bar = max(1e-4, 2 * rel(s1, os_))
+    assert rel(mu, omu) <= 1e-4 and rel(s, os_) <= bar, (rel(mu, omu), rel(s, os_), bar)
+    l0 = ctx.launches
+    gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
+    assert ctx.launches - l0 <= 6, ctx.launches - l0
+    p64 = ctx_of(w, max_probes=w.K, probe_precision=1)
+    mu, s = gpu_estep(p64, w, np.ones(w.D), w.K, 3, 1)
+    # fp64 probes: 1e-7, or 10x the oracle's own move under alpha (1 + 1e-15 r) (reading R21) where
+    # the unconverged CG amplifies rounding (64 x 1000 at U = 80: the oracle moves s by ~5e-8)
+    r = np.random.default_rng(12345).choice([-1.0, 1.0], size=w.D)
+    pmu, ps_, _ = estep(op_of(w), w.y, w.beta, 1.0 + 1e-15 * r, w.K, 3, 1, w.U)
+    bm, bs = max(1e-7, 10 * rel(pmu, omu)), max(1e-7, 10 * rel(ps_, os_))
+    assert rel(mu, omu) <= bm and rel(s, os_) <= bs, (rel(mu, omu), rel(s, os_), bm, bs)
+    a, mu, s = gpu_em(ctx, w, w.T, w.K, 5)
+    a2, mu2, s2 = gpu_em(ctx_of(w, max_probes=w.K, apply_path=2), w, w.T, w.K, 5)
+    assert rel(1 / a, 1 / a2) <= 1e-3 and rel(mu, mu2) <= 1e-4, (rel(1 / a, 1 / a2), rel(mu, mu2))
+    assert ctx.report()["frozen_at"] is not None

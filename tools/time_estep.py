@@ -15,6 +15,8 @@ if os.environ.get("TIME_K"):          # emulate one rank of a probe-parallel run
     w.K = int(os.environ["TIME_K"])
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 kw = {"probe_groups": int(os.environ["TIME_GROUPS"])} if os.environ.get("TIME_GROUPS") else {}
+if os.environ.get("TIME_PATH"):       # cofem_options.apply_path (1: the general kernels)
+    kw["apply_path"] = int(os.environ["TIME_PATH"])
 if os.environ.get("TIME_NOGRAPH"):
     kw["use_graph"] = False
 if os.environ.get("TIME_U"):          # CG iterations per E-step (use with an existing alpha file)
