@@ -34,11 +34,13 @@ namespace cg = cooperative_groups;
 #ifndef COFEM_DCL_NC
 #define COFEM_DCL_NC 8
 #endif
+// C1 E-step (fixed alpha): KG 8 / 256 threads 1.61 ms, KG 4 / 256 1.51, KG 4 / 512 1.43, KG 4 / 384 1.38;
+// 16-CTA clusters measured slower
 #ifndef COFEM_DCL_THREADS
-#define COFEM_DCL_THREADS 256
+#define COFEM_DCL_THREADS 384
 #endif
 #ifndef COFEM_DCL_KG
-#define COFEM_DCL_KG 8
+#define COFEM_DCL_KG 4
 #endif
 constexpr int NC = COFEM_DCL_NC;            // CTAs per cluster (8: the portable maximum)
 constexpr int THREADS = COFEM_DCL_THREADS;
@@ -55,18 +57,23 @@ struct Args {
   ColState* cs;
 };
 
-// Shared-memory layout (bytes, 16-aligned pieces), sized for K probe columns.
+// Shared-memory layout (bytes, 16-aligned pieces), sized for K probe columns.  The probe arrays are
+// stored [d][KP] and W [n][KP] (KP = K rounded up to KG, zero columns): the KG columns of a work unit
+// are one 32- / 64-byte vector per d (or n) in the two products.
 struct Layout {
-  size_t phi, Pp, Rp, Qp, dvp, x, r, p, q, dv, al, sacc, wpart, wfull, w0part, w0full, gpart, rpart, cs, sgn, total;
+  size_t phi, Pp, Rp, Qp, dvp, x, r, p, q, dv, al, sacc, wpart, wfull, w0part, w0full, gpart, rpart, cs, coef, sgn,
+      total;
 };
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~size_t(15); }
+__host__ __device__ inline int kpad(int K) { return ((K + KG - 1) / KG) * KG; }
 __host__ __device__ inline Layout layout(int N, int Dc, int DcP, int K, size_t tp) {
   Layout L;
+  const int KP = kpad(K);
   size_t o = 0;
   L.phi = o; o = al16(o + (size_t)N * DcP * 4);
-  L.Pp = o; o = al16(o + (size_t)K * Dc * tp);
-  L.Rp = o; o = al16(o + (size_t)K * Dc * tp);
-  L.Qp = o; o = al16(o + (size_t)K * Dc * tp);
+  L.Pp = o; o = al16(o + (size_t)Dc * KP * tp);
+  L.Rp = o; o = al16(o + (size_t)Dc * KP * tp);
+  L.Qp = o; o = al16(o + (size_t)Dc * KP * tp);
   L.dvp = o; o = al16(o + (size_t)Dc * tp);
   L.x = o; o = al16(o + (size_t)Dc * 8);
   L.r = o; o = al16(o + (size_t)Dc * 8);
@@ -75,16 +82,35 @@ __host__ __device__ inline Layout layout(int N, int Dc, int DcP, int K, size_t t
   L.dv = o; o = al16(o + (size_t)Dc * 8);
   L.al = o; o = al16(o + (size_t)Dc * 8);
   L.sacc = o; o = al16(o + (size_t)Dc * 8);
-  L.wpart = o; o = al16(o + (size_t)N * K * tp);
-  L.wfull = o; o = al16(o + (size_t)N * K * tp);
+  L.wpart = o; o = al16(o + (size_t)N * KP * tp);
+  L.wfull = o; o = al16(o + (size_t)N * KP * tp);
   L.w0part = o; o = al16(o + (size_t)N * 8);
   L.w0full = o; o = al16(o + (size_t)N * 8);
   L.gpart = o; o = al16(o + (size_t)(K + 1) * 8);
   L.rpart = o; o = al16(o + (size_t)(K + 1) * 8);
   L.cs = o; o = al16(o + (size_t)(K + 1) * sizeof(ColState));
-  L.sgn = o; o = al16(o + (size_t)K * Dc);
+  L.coef = o; o = al16(o + (size_t)KP * 8);
+  L.sgn = o; o = al16(o + (size_t)Dc * KP);
   L.total = o;
   return L;
+}
+
+// KG consecutive values of probe precision from 16-byte-aligned shared memory
+template <typename TP> __device__ __forceinline__ void ldkg(const TP* p, TP (&v)[KG]) {
+  static_assert(KG % 4 == 0, "KG");
+  if constexpr (sizeof(TP) == 4) {
+#pragma unroll
+    for (int i = 0; i < KG / 4; ++i) {
+      const float4 x = reinterpret_cast<const float4*>(p)[i];
+      v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < KG / 2; ++i) {
+      const double2 x = reinterpret_cast<const double2*>(p)[i];
+      v[2 * i] = x.x; v[2 * i + 1] = x.y;
+    }
+  }
 }
 
 template <typename TP>
@@ -92,11 +118,11 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
   extern __shared__ __align__(16) unsigned char smraw[];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
-  const int tid = threadIdx.x;
-  const int N = a.N, K = a.K, m = K + 1, Dc = a.Dc, DcP = a.DcP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int N = a.N, K = a.K, m = K + 1, Dc = a.Dc, DcP = a.DcP, KP = kpad(K), G = KP / KG;
   const Layout L = layout(N, Dc, DcP, K, sizeof(TP));
   float* phs = reinterpret_cast<float*>(smraw + L.phi);     // [N][DcP]
-  TP* Ps = reinterpret_cast<TP*>(smraw + L.Pp);             // [K][Dc]
+  TP* Ps = reinterpret_cast<TP*>(smraw + L.Pp);             // [Dc][KP]
   TP* Rs = reinterpret_cast<TP*>(smraw + L.Rp);
   TP* Qs = reinterpret_cast<TP*>(smraw + L.Qp);
   TP* dvp = reinterpret_cast<TP*>(smraw + L.dvp);           // [Dc] 1/diag in probe precision
@@ -107,15 +133,15 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
   double* dv = reinterpret_cast<double*>(smraw + L.dv);
   double* als = reinterpret_cast<double*>(smraw + L.al);
   double* sacc = reinterpret_cast<double*>(smraw + L.sacc);
-  TP* wpart = reinterpret_cast<TP*>(smraw + L.wpart);       // [N][K]
+  TP* wpart = reinterpret_cast<TP*>(smraw + L.wpart);       // [N][KP]
   TP* wfull = reinterpret_cast<TP*>(smraw + L.wfull);
   double* w0part = reinterpret_cast<double*>(smraw + L.w0part);
   double* w0full = reinterpret_cast<double*>(smraw + L.w0full);
   double* gpart = reinterpret_cast<double*>(smraw + L.gpart);
   double* rpart = reinterpret_cast<double*>(smraw + L.rpart);
   ColState* cs = reinterpret_cast<ColState*>(smraw + L.cs);
-  uint8_t* sgn = smraw + L.sgn;                             // [K][Dc] probe bit (1: -1) of this slice
-  const int warp = tid >> 5, lane = tid & 31;
+  double* coef = reinterpret_cast<double*>(smraw + L.coef);   // [KP] a_k / K of the active columns, else 0
+  uint8_t* sgn = smraw + L.sgn;                             // [Dc][KP] probe bit (1: -1)
 
   // ---- this CTA's slice d in [d0, d0 + Dl) of Phi and of every vector (state after k_init)
   const int d0 = rank * Dc;
@@ -127,15 +153,16 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
   const TP* Pg = reinterpret_cast<const TP*>(a.P);
   const TP* Rg = reinterpret_cast<const TP*>(a.R);
   const TP* dvg = reinterpret_cast<const TP*>(a.dinvp);
-  for (int i = tid; i < K * Dc; i += THREADS) {
-    const int k = i / Dc, dl = i % Dc;
-    const bool v = dl < Dl;
-    Ps[i] = v ? Pg[(int64_t)k * a.Dp + d0 + dl] : (TP)0;
-    Rs[i] = v ? Rg[(int64_t)k * a.Dp + d0 + dl] : (TP)0;
-    Qs[i] = (TP)0;
+  for (int i = tid; i < Dc * KP; i += THREADS) {
+    const int dl = i / KP, k = i % KP;
+    const bool v = dl < Dl && k < K;
     const int d = d0 + dl;
+    Ps[i] = v ? Pg[(int64_t)k * a.Dp + d] : (TP)0;
+    Rs[i] = v ? Rg[(int64_t)k * a.Dp + d] : (TP)0;
+    Qs[i] = (TP)0;
     sgn[i] = v ? (uint8_t)((a.bits[(int64_t)k * a.wpc + (d >> 5)] >> (d & 31)) & 1u) : (uint8_t)0;
   }
+  for (int i = tid; i < N * KP; i += THREADS) { wpart[i] = (TP)0; wfull[i] = (TP)0; }
   for (int dl = tid; dl < Dc; dl += THREADS) {
     const bool v = dl < Dl;
     const int d = d0 + dl;
@@ -144,10 +171,10 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     dv[dl] = v ? a.dinv64[d] : 0.0; als[dl] = v ? a.alpha[d] : 0.0; sacc[dl] = v ? a.s[d] : 0.0;
   }
   for (int j = tid; j < m; j += THREADS) cs[j] = a.cs[j];
-  const int G = (K + KG - 1) / KG;                 // probe column groups
   const int Nr = (N + NC - 1) / NC, n_lo = min(N, rank * Nr), n_hi = min(N, n_lo + Nr);
   cl.sync();
 
+#pragma unroll 1
   for (int it = 0; it < a.U; ++it) {
     // every column frozen (R5): nothing left to do (the state is the same in every CTA)
     int act = 0;
@@ -158,19 +185,18 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
       const int n = u % N, g = u / N;
       const float* ph = phs + n * DcP;
       if (g < G) {
-        const int k0 = g * KG;
         TP acc[KG];
 #pragma unroll
         for (int i = 0; i < KG; ++i) acc[i] = (TP)0;
         for (int dl = 0; dl < Dl; ++dl) {
           const TP f = (TP)ph[dl];
+          TP pv[KG];
+          ldkg(Ps + dl * KP + g * KG, pv);
 #pragma unroll
-          for (int i = 0; i < KG; ++i)
-            if (k0 + i < K) acc[i] += f * Ps[(k0 + i) * Dc + dl];
+          for (int i = 0; i < KG; ++i) acc[i] += f * pv[i];
         }
 #pragma unroll
-        for (int i = 0; i < KG; ++i)
-          if (k0 + i < K) wpart[n * K + k0 + i] = acc[i];
+        for (int i = 0; i < KG; ++i) wpart[n * KP + g * KG + i] = acc[i];
       } else {
         double acc0 = 0.0;
         for (int dl = 0; dl < Dl; ++dl) acc0 += (double)ph[dl] * ps[dl];
@@ -184,12 +210,12 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
       if (k < K) {
         TP x[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(wpart, c)[n * K + k];
+        for (int c = 0; c < NC; ++c) x[c] = cl.map_shared_rank(wpart, c)[n * KP + k];
         TP v = (TP)0;
 #pragma unroll
         for (int c = 0; c < NC; ++c) v += x[c];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) cl.map_shared_rank(wfull, c)[n * K + k] = v;
+        for (int c = 0; c < NC; ++c) cl.map_shared_rank(wfull, c)[n * KP + k] = v;
       } else {
         double x[NC];
 #pragma unroll
@@ -207,20 +233,21 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : Dl * (G + 1)); u += THREADS) {
       const int dl = u % Dl, g = u / Dl;
       if (g < G) {
-        const int k0 = g * KG;
         TP acc[KG];
 #pragma unroll
         for (int i = 0; i < KG; ++i) acc[i] = (TP)0;
         for (int n = 0; n < N; ++n) {
           const TP f = (TP)phs[n * DcP + dl];
+          TP wv[KG];
+          ldkg(wfull + n * KP + g * KG, wv);
 #pragma unroll
-          for (int i = 0; i < KG; ++i)
-            if (k0 + i < K) acc[i] += f * wfull[n * K + k0 + i];
+          for (int i = 0; i < KG; ++i) acc[i] += f * wv[i];
         }
         const TP alt = (TP)als[dl];
+        TP pv[KG];
+        ldkg(Ps + dl * KP + g * KG, pv);
 #pragma unroll
-        for (int i = 0; i < KG; ++i)
-          if (k0 + i < K) Qs[(k0 + i) * Dc + dl] = betat * acc[i] + alt * Ps[(k0 + i) * Dc + dl];
+        for (int i = 0; i < KG; ++i) Qs[dl * KP + g * KG + i] = betat * acc[i] + alt * pv[i];
       } else {
         double acc0 = 0.0;
         for (int n = 0; n < N; ++n) acc0 += (double)phs[n * DcP + dl] * w0full[n];
@@ -231,7 +258,7 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     for (int j = warp; j < m; j += THREADS / 32) {   // one warp per column: lane-strided, then the tree
       double g = 0.0;
       if (j == 0) for (int dl = lane; dl < Dl; dl += 32) g += ps[dl] * qs[dl];
-      else for (int dl = lane; dl < Dl; dl += 32) g += (double)Ps[(j - 1) * Dc + dl] * (double)Qs[(j - 1) * Dc + dl];
+      else for (int dl = lane; dl < Dl; dl += 32) g += (double)Ps[dl * KP + j - 1] * (double)Qs[dl * KP + j - 1];
       g = warp_sum(g);
       if (lane == 0) gpart[j] = g;
     }
@@ -244,14 +271,15 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
 #pragma unroll
       for (int c = 0; c < NC; ++c) v += x[c];
       if (COFEM_DCL_EXP == 0) finish_gamma(cs[j], v, it);
+      if (j > 0) coef[j - 1] = cs[j].frozen ? 0.0 : cs[j].a * a.invK;
     }
     __syncthreads();
     // ---- 5. a5: x0 += a0 p0, r -= a q, s += (a_k / K) p_k o z_k; rho' partials
-    for (int u = tid; u < K * Dl; u += THREADS) {
-      const int k = u / Dl, dl = u % Dl;
+    for (int u = tid; u < Dl * K; u += THREADS) {
+      const int dl = u / K, k = u % K;
       if (cs[k + 1].frozen) continue;
       const TP akt = (TP)cs[k + 1].a;
-      Rs[k * Dc + dl] = Rs[k * Dc + dl] - akt * Qs[k * Dc + dl];
+      Rs[dl * KP + k] = Rs[dl * KP + k] - akt * Qs[dl * KP + k];
     }
     if (!cs[0].frozen) {
       const double a0 = cs[0].a;
@@ -262,15 +290,11 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     }
     for (int dl = tid; dl < Dl; dl += THREADS) {    // the probe estimator, columns in order (k_update)
       double sv = 0.0;
-      bool any = false;
       for (int k = 0; k < K; ++k) {
-        if (cs[k + 1].frozen) continue;
-        any = true;
-        const double aks = cs[k + 1].a * a.invK;
-        const double pe = (double)Ps[k * Dc + dl];
-        sv += sgn[k * Dc + dl] ? -aks * pe : aks * pe;
+        const double aks = coef[k], pe = (double)Ps[dl * KP + k];
+        sv += sgn[dl * KP + k] ? -aks * pe : aks * pe;
       }
-      if (any) sacc[dl] += sv;
+      sacc[dl] += sv;
     }
     __syncthreads();
     for (int j = warp; j < m; j += THREADS / 32) {
@@ -279,8 +303,10 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
         if (j == 0) {
           for (int dl = lane; dl < Dl; dl += 32) v += rs[dl] * (dv[dl] * rs[dl]);
         } else {
-          const TP* rr = Rs + (j - 1) * Dc;
-          for (int dl = lane; dl < Dl; dl += 32) { const TP z = dvp[dl] * rr[dl]; v += (double)rr[dl] * (double)z; }
+          for (int dl = lane; dl < Dl; dl += 32) {
+            const TP r = Rs[dl * KP + j - 1], z = dvp[dl] * r;
+            v += (double)r * (double)z;
+          }
         }
       }
       v = warp_sum(v);
@@ -299,11 +325,11 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
       cs[j].rho = v;
     }
     __syncthreads();
-    for (int u = tid; u < K * Dl; u += THREADS) {
-      const int k = u / Dl, dl = u % Dl;
+    for (int u = tid; u < Dl * K; u += THREADS) {
+      const int dl = u / K, k = u % K;
       if (cs[k + 1].frozen) continue;
       const TP bt = (TP)cs[k + 1].b;
-      Ps[k * Dc + dl] = dvp[dl] * Rs[k * Dc + dl] + bt * Ps[k * Dc + dl];
+      Ps[dl * KP + k] = dvp[dl] * Rs[dl * KP + k] + bt * Ps[dl * KP + k];
     }
     if (!cs[0].frozen) {
       const double b0 = cs[0].b;
