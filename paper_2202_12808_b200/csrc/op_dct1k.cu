@@ -199,6 +199,9 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
                                               const Tw<T>& tb);
 
 template <typename T>
+#ifndef COFEM_1K_INV_TMA
+#define COFEM_1K_INV_TMA 0    // pass A (fp32 probes) with TMA bulk staging of each warp's next row (A/B switch)
+#endif
 #ifndef COFEM_1K_INV_MINB
 #define COFEM_1K_INV_MINB 1   // explicit: nvcc then takes 96 registers (2 CTAs per SM): 47.7 -> 47.1 ms; 3: 47.6, 4: 48.4
 #endif
@@ -331,6 +334,153 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
 #pragma unroll
     for (int i = 0; i < RT; ++i) v[i] = sm[i * WREG + cv];
     st32B<T, RT>(out + (int64_t)cv * L + row0, v);
+  }
+}
+
+// ---------------------------------------------------------------- pass A, bulk-staged (fp32 probes)
+// each warp's NEXT image row of p and r is copied into shared memory by the TMA
+// bulk engine (cp.async.bulk, one 4 KB copy per array, completion on a per-warp mbarrier) while the
+// warp runs the current row's FFT, so the row loads leave the critical path whatever the number of
+// warps.  16 warps (rows) per CTA, one CTA per SM (212 KB of shared memory: 16 x 8 KB staging, the
+// exchange regions, the tables), i.e. the same 16 warps per SM as k1k_rows_inv.  Arithmetic identical
+// to rows_inv_item<float>.  Build switch COFEM_1K_INV_TMA (A/B).
+namespace rtma {
+#ifndef COFEM_1K_TMA_RT
+#define COFEM_1K_TMA_RT 16
+#endif
+#ifndef COFEM_1K_TMA_R
+#define COFEM_1K_TMA_R 1      // 1: stage r as well as p
+#endif
+#ifndef COFEM_1K_TMA_CPS
+#define COFEM_1K_TMA_CPS 1    // CTAs per SM of the persistent grid
+#endif
+constexpr int RT = COFEM_1K_TMA_RT, NT = L / RT, STG = (COFEM_1K_TMA_R ? 2 : 1) * L;
+__host__ __device__ constexpr size_t smem_bytes() {
+  return (size_t)RT * STG * 4 + (size_t)RT * WREG * 4 + (size_t)TPRE * sizeof(cplx<float>) + (size_t)RT * 8;
+}
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)));
+}
+__device__ __forceinline__ void expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done)
+                 : "r"(su32(b)), "r"(parity)
+                 : "memory");
+}
+}  // namespace rtma
+
+__global__ void __launch_bounds__(rtma::RT * 32, COFEM_1K_TMA_CPS) k1k_rows_inv_tma(DctArgs a, int j0, int ncols, int dir) {
+  using namespace rtma;
+  extern __shared__ __align__(16) unsigned char smraw[];   // bulk copies need 16-byte alignment
+  float* stg = reinterpret_cast<float*>(smraw);                                  // [RT][STG]: p row, r row
+  float* sm = stg + RT * STG;                                                    // [RT][WREG] exchange
+  cplx<float>* tabs = reinterpret_cast<cplx<float>*>(sm + RT * WREG);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tabs + TPRE);
+  __shared__ ColFlags ci;
+  load_colinfo(ci, a.cs, j0, ncols);
+  if (!any_active(ci, ncols)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int items = ncols * NT;
+  auto next_item = [&](int w) {   // CTA-uniform: the next item of this CTA whose column is active
+    for (; w < items; w += gridDim.x)
+      if (!ci.frozen[w / NT]) return w;
+    return items;
+  };
+  auto issue = [&](int w) {       // lane 0: this warp's row of item w -> its staging buffer
+    const DctCol<float> cn = col_of<float>(a, j0 + w / NT);
+    const int64_t rb = (int64_t)((w % NT) * RT + warp) * L;
+    const bool rr = COFEM_1K_TMA_R && dir;
+    expect_tx(&bar[warp], rr ? 2 * L * 4 : L * 4);
+    bulk(stg + warp * STG, cn.p + rb, L * 4, &bar[warp]);
+    if (rr) bulk(stg + warp * STG + L, cn.r + rb, L * 4, &bar[warp]);
+  };
+  int w = next_item(blockIdx.x);
+  if (lane == 0) {
+    bar_init(&bar[warp]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (w < items) issue(w);
+  }
+  const Tw<float> tb = load_tables<float>(tab1k<float>(a), tabs, TPRE);   // + barrier
+  uint32_t phase = 0;
+  const float4* st4p = reinterpret_cast<const float4*>(stg + warp * STG);
+  const float4* st4r = reinterpret_cast<const float4*>(stg + warp * STG + (COFEM_1K_TMA_R ? L : 0));
+  while (w < items) {
+    const int wn = next_item(w + gridDim.x);
+    const int jj = w / NT, tile = w % NT, row0 = tile * RT;
+    const DctCol<float> c = col_of<float>(a, j0 + jj);
+    const int64_t rb = (int64_t)(row0 + warp) * L;
+    wait(&bar[warp], phase);
+    phase ^= 1u;
+    float4 pv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pv[i] = st4p[lane + 32 * i];
+    if (dir) {
+      const float bb = (float)ci.b[jj];
+      const float4* __restrict__ dv = reinterpret_cast<const float4*>(c.dinv + rb);
+      float4* __restrict__ pr = reinterpret_cast<float4*>(c.p + rb);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {    // a6: p = M^-1 r + b p
+        const float4 rv = COFEM_1K_TMA_R ? st4r[lane + 32 * i] : reinterpret_cast<const float4*>(c.r + rb)[lane + 32 * i];
+        const float4 dd = dv[lane + 32 * i];
+        pv[i].x = dd.x * rv.x + bb * pv[i].x; pv[i].y = dd.y * rv.y + bb * pv[i].y;
+        pv[i].z = dd.z * rv.z + bb * pv[i].z; pv[i].w = dd.w * rv.w + bb * pv[i].w;
+        pr[lane + 32 * i] = pv[i];
+      }
+    }
+    float4* r4 = reinterpret_cast<float4*>(sm + warp * WREG);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r4[lane + 32 * i] = pv[i];
+    __syncwarp();                    // the staging buffer is consumed (pv depends on every read of it)
+    if (!COFEM_1K_TMA_R && dir && wn < items) {   // r of the next row: L2 prefetch instead
+      const int64_t rbn = (int64_t)((wn % NT) * RT + warp) * L;
+      pf_line(col_of<float>(a, j0 + wn / NT).r + rbn);
+    }
+    if (wn < items && lane == 0) issue(wn);
+    const float* reg = sm + warp * WREG;
+    float A[8], B[8], C[8], E[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      int o[4];
+      canon(lane, r, o);
+      A[r] = reg[o[0]]; B[r] = reg[o[1]]; C[r] = reg[o[2]]; E[r] = reg[o[3]];
+    }
+    __syncwarp();                    // fft512 reuses the region
+    cplx<float> va[8], vb[8];
+    pre_all<float>(lane, A, B, C, E, va, vb, tb);
+    float* regw = sm + warp * WREG;
+    fft512<float, +1>(va, vb, lane, reinterpret_cast<cplx<float>*>(regw), tb);
+    const int ja = lane, jb = lane ? 64 - lane : 32;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {     // packed v-order output w[n] = v[2n] + i v[2n+1]
+      *reinterpret_cast<cplx<float>*>(regw + 2 * (ja + 64 * r)) = va[r];
+      *reinterpret_cast<cplx<float>*>(regw + 2 * (jb + 64 * r)) = vb[r];
+    }
+    bar_rt<RT>();
+    float* __restrict__ out = c.t1;   // T^T[cv][row], line length L: 32-byte segments of 8 rows
+#pragma unroll
+    for (int it = 0; it < L / (RT * 32); ++it) {
+      const int cv = it * RT * 32 + threadIdx.x;
+#pragma unroll
+      for (int h = 0; h < RT / 8; ++h) {
+        float v0[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v0[i] = sm[(8 * h + i) * WREG + cv];
+        st32B<float, 8>(out + (int64_t)cv * L + row0 + 8 * h, v0);
+      }
+    }
+    bar_rt<RT>();                    // the exchange regions are reused by the next item
+    w = wn;
   }
 }
 
@@ -1100,6 +1250,9 @@ template <typename T> static size_t smem_bytes(int ntab = TTOT) {
 
 template <typename T> static void set_attrs() {
   const int s = (int)smem_bytes<T>();
+#if COFEM_1K_INV_TMA
+  cudaFuncSetAttribute(k1k_rows_inv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rtma::smem_bytes());
+#endif
   cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(TPRE));
   cudaFuncSetAttribute(k1k_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
   cudaFuncSetAttribute(k1k_rows_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
@@ -1244,6 +1397,14 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   const dim3 blk(RT * 32);
   const bool mean = j0 == 0;        // the fp64 mean column is timed as its own class
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
+#if COFEM_1K_INV_TMA
+  if constexpr (sizeof(T) == 4) {
+    const int items = ncols * rtma::NT;   // persistent: one CTA per SM (each warp prefetches its next row)
+    int g = std::min(items, c->num_sms * COFEM_1K_TMA_CPS);
+    if (j0 > 0 && c->probe_groups > 1) g = std::min(g, (c->num_sms * 120) / 148 * COFEM_1K_TMA_CPS);
+    k1k_rows_inv_tma<<<std::max(1, g), rtma::RT * 32, rtma::smem_bytes(), st>>>(a, j0, ncols, dir ? 1 : 0);
+  } else
+#endif
   k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(TPRE)), blk, smem_bytes<T>(TPRE), st>>>(
       a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
