@@ -547,9 +547,12 @@ def main():
     dom_bytes, work_frac = active_bytes(dom, w, K_loc, D, groups, frozen)
     achieved = dom_bytes / (busy_ms / 1000.0) / 1e9
     traffic = None
+    pipes = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+        tdoc = json.load(open(tp))
+        traffic = tdoc.get(args.workload, {}).get(dom)
+        pipes = tdoc.get(args.workload + "_pipes", {}).get(dom)
     share = {c: round(prof[c][0] / prof_ms, 4) for c in classes if prof[c][1] > 0}
     busy_share = {c: round(busy[c] / prof_ms, 4) for c in classes if prof[c][1] > 0}
     # whole-step view (the classes run concurrently on the DCT path): every class's algorithmic
@@ -573,6 +576,10 @@ def main():
                             "(probe classes; the fp64 mean column is not counted)"},
             "share_of_step": share, "busy_share_of_step": busy_share, "timed_in": "separate profiled pass of %d EM iteration(s), events per launch" %
             args.prof_steps}
+    if pipes:
+        # what bounds a kernel that is not HBM-bound (dct_cols: the L1TEX / shared-memory pipe), from the
+        # committed steady-state ncu capture of the same kernel (like `traffic`), % of peak while active
+        roof["ncu_pipes"] = dict(pipes, source="profiles/ncu_traffic.json (steady-state ncu --set full capture)")
     if dom == "dense_cluster":
         # the whole CG loop in one 8-CTA cluster, state in shared memory (op_dense_cluster.cu): the
         # bound is FP32 issue and the cluster barriers, not memory.  FP32 SIMT peak = SMs x 128 lanes
