@@ -64,3 +64,18 @@ def test_executed_applies_counts_frozen_columns():
     applied in iterations 0..F (the apply of F finds it frozen), one never frozen in all U."""
     assert bench.executed_applies([[-1, 3, 0]], 10) == 10 + 4 + 1
     assert bench.executed_applies([[-1, -1], [9, 12]], 10) == 20 + 10 + 10
+
+
+def test_every_profiled_class_with_work_has_bytes():
+    """The dominant-kernel pick only considers classes with algorithmic bytes: every kernel class
+    that carries the E-step's work on some path (incl. the cluster CG loop of small dense problems)
+    must have them, or a path whose only heavy class lacks them would have no roofline."""
+    dense = types.SimpleNamespace(D=400, U=10, kind="dense", N=100, rows=0, cols=0)
+    dct = types.SimpleNamespace(D=1 << 20, U=10, kind="dct2_masked", N=1 << 18, rows=1024, cols=1024)
+    conv = _w()
+    for cls, w in [("dense_phi_p", dense), ("dense_phiT_w", dense), ("dense_cluster", dense),
+                   ("pcg_update", dense), ("pcg_direction", dense), ("dct_rows_inv", dct), ("dct_cols", dct),
+                   ("dct_rows_fwd", dct), ("conv_apply", conv)]:
+        assert bench.algorithmic_bytes(cls, w, 4) > 0, cls
+    # the cluster loop reads Phi and the state once per E-step: more columns, more bytes
+    assert bench.algorithmic_bytes("dense_cluster", dense, 8) > bench.algorithmic_bytes("dense_cluster", dense, 4)
