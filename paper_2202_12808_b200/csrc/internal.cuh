@@ -3,7 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/cofem.h"
@@ -314,6 +316,20 @@ cofem_status comm_halo(Ctx* c, const void* send_left, const void* send_right, vo
 // after a per-column reduction written to c->colsum: sum over ranks, then apply it (mode:
 // 0 = rho0 (init), 1 = gamma -> freeze rule / step length, 2 = rho' -> b)
 cofem_status sharded_finish(Ctx* c, int m, int mode, int iter);
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to the function, not to a context: only ever
+// raise it, so that a context set up later with a smaller need (max_probes, N, D) does not break the
+// launches of an earlier one
+inline cudaError_t raise_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> cur;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cur[fn];
+  if (bytes <= c) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) c = bytes;
+  return e;
+}
 
 // vector kernels (cofem.cu)
 cofem_status launch_dir(Ctx* c, int m);

@@ -237,11 +237,11 @@ cofem_status dense_setup(Ctx* c, const float* y_dev) {
   c->part_stride = std::max(c->part_stride, k2grid);
   size_t s1 = k1_smem(c->Kcap, tp), s2 = k2_smem(c->Kcap, tp);
   if (c->probe64) {
-    cudaFuncSetAttribute(k_dense_phiP<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-    cudaFuncSetAttribute(k_dense_phiTW<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+    raise_smem_attr((const void*)k_dense_phiP<double>, s1);
+    raise_smem_attr((const void*)k_dense_phiTW<double>, s2);
   } else {
-    cudaFuncSetAttribute(k_dense_phiP<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-    cudaFuncSetAttribute(k_dense_phiTW<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+    raise_smem_attr((const void*)k_dense_phiP<float>, s1);
+    raise_smem_attr((const void*)k_dense_phiTW<float>, s2);
   }
   cofem_status st = dense_tc_setup(c);
   if (st == COFEM_OK && dense_cluster_eligible(c)) st = dense_cluster_setup(c);

@@ -363,9 +363,8 @@ cofem_status dense_cluster_setup(Ctx* c) {
     cudaFuncSetAttribute(dcl::k_dense_cluster_cg<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(dcl::k_dense_cluster_cg<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
-  cudaError_t e = c->probe64
-      ? cudaFuncSetAttribute(dcl::k_dense_cluster_cg<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)
-      : cudaFuncSetAttribute(dcl::k_dense_cluster_cg<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaError_t e = c->probe64 ? raise_smem_attr((const void*)dcl::k_dense_cluster_cg<double>, sm)
+                              : raise_smem_attr((const void*)dcl::k_dense_cluster_cg<float>, sm);
   if (e != cudaSuccess) { c->err = std::string("dense cluster setup: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
   c->dense_cluster = true;
   return COFEM_OK;

@@ -802,12 +802,12 @@ cofem_status dense_tc_setup(Ctx* c) {
             make_map(&t->wll, t->Wl, t->Npad, c->Kcap, t->Npad, BK, t->bn);
   if (!ok) { c->err = "cuTensorMapEncodeTiled failed"; return COFEM_ERR_CUDA; }
   const int sm = (int)smem_of(t->pl);
-  cudaFuncSetAttribute(k_tc_phiP<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiP<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiP<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiTW<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiTW<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-  cudaFuncSetAttribute(k_tc_phiTW<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  raise_smem_attr((const void*)k_tc_phiP<0>, sm);
+  raise_smem_attr((const void*)k_tc_phiP<1>, sm);
+  raise_smem_attr((const void*)k_tc_phiP<2>, sm);
+  raise_smem_attr((const void*)k_tc_phiTW<0>, sm);
+  raise_smem_attr((const void*)k_tc_phiTW<1>, sm);
+  raise_smem_attr((const void*)k_tc_phiTW<2>, sm);
   c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
   return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }

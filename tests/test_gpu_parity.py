@@ -638,3 +638,19 @@ def test_dense_cluster_cg_loop(w):
     a2, mu2, s2 = gpu_em(ctx_of(w, max_probes=w.K, apply_path=2), w, w.T, w.K, 5)
     assert rel(1 / a, 1 / a2) <= 1e-3 and rel(mu, mu2) <= 1e-4, (rel(1 / a, 1 / a2), rel(mu, mu2))
     assert ctx.report()["frozen_at"] is not None
+
+
+@pytest.mark.parametrize("path", [0, 1, 2], ids=["cluster", "simt", "tcgen05"])
+def test_context_created_later_with_smaller_smem_does_not_break_earlier(path):
+    """Dynamic shared-memory limits are per kernel function, not per context: a context set up after
+    another with a smaller max_probes must not lower the limit the first one's launches need
+    (raise_smem_attr).  Direct launches (use_graph off): a captured graph fixes its launch
+    configuration at instantiation and would not notice."""
+    w = synth.preset("C1")
+    ones = np.ones(w.D)
+    big = ctx_of(w, max_probes=64, apply_path=path, use_graph=False)
+    mu1, s1 = gpu_estep(big, w, ones, w.K, 3, 0)
+    small = ctx_of(w, max_probes=2, apply_path=path, use_graph=False)
+    gpu_estep(small, w, ones, 2, 3, 0)
+    mu2, s2 = gpu_estep(big, w, ones, w.K, 3, 0)
+    assert np.array_equal(mu1, mu2) and np.array_equal(s1, s2)
