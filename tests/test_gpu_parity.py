@@ -519,7 +519,7 @@ def test_c4_shape_convention1_estep1_closed_form():
     check("s", s, es, 1e-4, 1e-3)
 
 
-@pytest.mark.parametrize("w", [SMALL[1], SMALL[2], SMALL[5], SMALL[7],
+@pytest.mark.parametrize("w", [SMALL[0], SMALL[1], SMALL[2], SMALL[5], SMALL[7],
                                synth.dct(1024, 1024, 262144, 400, K=3, U=30, T=3, seed=3, name="dct1024_fast_U30")],
                          ids=lambda w: w.name)
 def test_warm_start_em_matches_oracle(w):
