@@ -443,9 +443,10 @@ def test_c4_full_size_bitwise_deterministic():
 def test_probe_parallel_library_mode_world1():
     """dist_mode 1 (probe-parallel inside the library: owner split, NCCL all-reduce of s and
     broadcast of mu) on a 1-rank communicator: the collectives are identities, so cofem_em must be
-    bitwise equal to the single-GPU run, on the generic DCT path and the 1024^2 fast path."""
+    bitwise equal to the single-GPU run, on the generic DCT path, the 1024^2 fast path and the dense
+    cluster CG loop (C1)."""
     from paper_2202_12808_b200 import get_unique_id
-    for w in [SMALL[2], synth.dct(1024, 1024, 262144, 400, K=4, U=8, T=1, seed=1)]:
+    for w in [SMALL[2], synth.dct(1024, 1024, 262144, 400, K=4, U=8, T=1, seed=1), SMALL[0]]:
         ref = gpu_em(ctx_of(w, cg_iters=w.U), w, 2, w.K, 3)
         pp = ctx_of(w, cg_iters=w.U, rank=0, world=1, nccl_id=get_unique_id(), dist_mode=1)
         got = gpu_em(pp, w, 2, w.K, 3)
