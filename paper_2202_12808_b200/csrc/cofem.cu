@@ -823,6 +823,9 @@ static cofem_status cg_loop_split(Ctx* c, int K, double invK, SplitApply apply) 
       cudaStream_t gst = g ? c->gstream[g] : c->stream;
       unsigned* tk = g ? c->counters + 3 * MAXM + gj[g] : c->counters + MAXM;   // per-group tickets
       if ((st = apply(c, gj[g], gj[g + 1], it, it > 0, gst)) != COFEM_OK) return st;
+#ifdef COFEM_EXP_NO_UPD   // timing experiment build only (results invalid): the probe update skipped
+      continue;
+#endif
       if (c->probe64) update_range<double>(c, K, invK, gj[g], gj[g + 1], tk, gst, KC_UPDATE, g ? c->gs[g] : nullptr);
       else update_range<float>(c, K, invK, gj[g], gj[g + 1], tk, gst, KC_UPDATE, g ? c->gs[g] : nullptr);
     }

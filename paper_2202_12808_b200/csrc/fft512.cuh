@@ -41,7 +41,38 @@ __host__ __device__ constexpr int ia(int k) { return k; }
 __host__ __device__ constexpr int ib(int k) { return M + k; }
 #endif
 #endif
+// Computed Makhoul factors (fp32 per-pass kernels): Ahat_k = u_k - i v_k, Bhat_k = e^{-i pi/4}(u_k + i v_k)
+// with u_k = (sc/2) e^{-i theta k}, v_k = (sc/2) e^{-5 i theta k}, theta = pi/2L; a lane's k are
+// k0 + 64 r (k0 = ja or jb), so u_k = u_{k0} e^{-i pi r/32} and v_k = v_{k0} e^{-5 i pi r/32}: four
+// per-lane bases [u_ja | v_ja | u_jb | v_jb][lane] replace the 2 x 512-entry tables in shared memory.
+// The fp32 table holds them after the full layout (at TTOT); the kernels copy w2 | w3 | bases.
+#if defined(COFEM_1K_TAB6)
+#undef COFEM_1K_CTAB
+#define COFEM_1K_CTAB 0
+#endif
+#ifndef COFEM_1K_CTAB
+#define COFEM_1K_CTAB 0
+#endif
+constexpr int NBAS = 4 * 32;                 // per-lane bases (complex entries)
+constexpr int TBAS = TW3 + 512;              // their offset in the compact shared-memory image
+constexpr int TCT = TBAS + NBAS;             // entries of the compact image
+// COFEM_1K_CTAB: bit PASS set = pass PASS (0 rows_inv, 1 cols, 2 rows_fwd) computes the factors (fp32)
+template <typename T> __host__ __device__ constexpr bool ctab() { return COFEM_1K_CTAB != 0 && sizeof(T) == 4; }
+template <typename T, int PASS> __host__ __device__ constexpr bool ctp() {
+  return ((COFEM_1K_CTAB >> PASS) & 1) != 0 && sizeof(T) == 4;
+}
+template <typename T, int PASS> __host__ __device__ constexpr int ntab() {
+  return ctp<T, PASS>() ? TCT : PASS == 0 ? TPRE : TTOT;
+}
 template <typename T> struct Tw { const cplx<T>* base; };
+
+// Compact image for the computed-factor kernels: g[0, TBAS) then the bases g[TTOT, TTOT + NBAS).
+template <typename T>
+__device__ __forceinline__ Tw<T> load_tables_ct(const cplx<T>* __restrict__ g, cplx<T>* sm) {
+  for (int i = threadIdx.x; i < TCT; i += blockDim.x) sm[i] = g[i < TBAS ? i : TTOT + (i - TBAS)];
+  __syncthreads();
+  return {sm};
+}
 
 template <typename T>
 __device__ __forceinline__ Tw<T> load_tables(const cplx<T>* __restrict__ g, cplx<T>* sm, int n = TTOT) {

@@ -84,12 +84,69 @@ __device__ __forceinline__ void dct2_post(int k, cplx<T> Wk, cplx<T> Wm, const T
 }
 #endif
 
-// Packed spectra of the DCT-III of a line held canonically in A, B, C, E.
+#ifndef COFEM_1K_TAB6
+// Computed factors (COFEM_1K_CTAB, fft512.cuh): Ahat, Bhat of k = k0 + 64 r from the lane's bases
+// u = u_{k0}, v = v_{k0}; the rotations e^{-i pi r/32}, e^{-5 i pi r/32} are compile-time constants.
 template <typename T>
+__device__ __forceinline__ void ab_comp(cplx<T> u, cplx<T> v, int r, cplx<T>& A, cplx<T>& B) {
+  constexpr double c1[8] = {1.0, 0.99518472667219692873, 0.98078528040323043058, 0.95694033573220882438,
+                            0.92387953251128673848, 0.88192126434835504956, 0.83146961230254523567, 0.77301045336273699338};
+  constexpr double s1[8] = {0.0, 0.09801714032956060363, 0.19509032201612824808, 0.29028467725446233105,
+                            0.38268343236508978178, 0.47139673682599764204, 0.55557023301960217765, 0.63439328416364548779};
+  constexpr double c5[8] = {1.0, 0.88192126434835504956, 0.55557023301960228867, 0.09801714032956077016,
+                            -0.38268343236508972627, -0.77301045336273699338, -0.98078528040323043058, -0.95694033573220893540};
+  constexpr double s5[8] = {0.0, 0.47139673682599764204, 0.83146961230254523567, 0.99518472667219681771,
+                            0.92387953251128673848, 0.63439328416364548779, 0.19509032201612860891, -0.29028467725446210901};
+  cplx<T> U = u, V = v;
+  if (r) {   // U = u e^{-i pi r/32}, V = v e^{-5 i pi r/32}
+    const T c = (T)c1[r], s = (T)s1[r], cc = (T)c5[r], ss = (T)s5[r];
+    U = {u.x * c + u.y * s, u.y * c - u.x * s};
+    V = {v.x * cc + v.y * ss, v.y * cc - v.x * ss};
+  }
+  const T h = (T)0.70710678118654752440;
+  A = {U.x + V.y, U.y - V.x};                              // U - i V
+  const T tx = U.x - V.y, ty = U.y + V.x;                  // U + i V
+  B = {h * (tx + ty), h * (ty - tx)};                      // e^{-i pi/4} (U + i V)
+}
+template <typename T>
+__device__ __forceinline__ cplx<T> dct3_pre_ab(cplx<T> A, cplx<T> B, T Xk, T XLk, T XkM, T XMk) {
+  return {Xk * A.x - XLk * A.y + XkM * B.x - XMk * B.y, -Xk * A.y - XLk * A.x - XkM * B.y - XMk * B.x};
+}
+template <typename T>
+__device__ __forceinline__ void dct2_post_ab(cplx<T> A, cplx<T> B, cplx<T> Wk, cplx<T> Wm, T& lo, T& hi) {
+  const T h = (T)0.70710678118654752440;
+  const T u = h * (Wm.x + Wm.y), v = h * (Wm.x - Wm.y);
+  lo = Wk.x * A.x - Wk.y * A.y + u * B.x - v * B.y;
+  hi = Wk.x * B.x - Wk.y * B.y + v * A.x + u * A.y;
+}
+#endif
+
+// Packed spectra of the DCT-III of a line held canonically in A, B, C, E.
+// CT: Makhoul factors computed from the per-lane bases (fft512.cuh) instead of read from the tables.
+template <typename T, bool CT = false>
 __device__ __forceinline__ void pre_all(int lane, const T (&A)[8], const T (&B)[8], const T (&C)[8], const T (&E)[8],
                                         cplx<T> (&va)[8], cplx<T> (&vb)[8], const Tw<T>& tb) {
   const int ja = lane, jb = lane ? 64 - lane : 32;
   const bool l0 = lane == 0;
+#ifndef COFEM_1K_TAB6
+  if constexpr (CT) {
+    const cplx<T> ua = tb.base[TBAS + lane], wa = tb.base[TBAS + 32 + lane];
+    const cplx<T> ub = tb.base[TBAS + 64 + lane], wb = tb.base[TBAS + 96 + lane];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const T aMk = l0 ? (r ? A[(8 - r) & 7] : C[0]) : B[7 - r];
+      const T aLk = l0 ? (r ? C[(8 - r) & 7] : (T)0) : E[7 - r];
+      cplx<T> Af, Bf;
+      ab_comp<T>(ua, wa, r, Af, Bf);
+      va[r] = dct3_pre_ab<T>(Af, Bf, (l0 && r == 0) ? A[0] * (T)1.41421356237309504880 : A[r], aLk, C[r], aMk);
+      const T bMk = l0 ? B[7 - r] : A[7 - r];
+      const T bLk = l0 ? E[7 - r] : C[7 - r];
+      ab_comp<T>(ub, wb, r, Af, Bf);
+      vb[r] = dct3_pre_ab<T>(Af, Bf, B[r], bLk, E[r], bMk);
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     // slot a, k = ja + 64 r: X[M-k], X[L-k]
@@ -108,11 +165,29 @@ __device__ __forceinline__ void pre_all(int lane, const T (&A)[8], const T (&B)[
 }
 
 // DCT-II outputs of a line from its FFT (va, vb) into canonical A, B, C, E.
-template <typename T>
+template <typename T, bool CT = false>
 __device__ __forceinline__ void post_all(int lane, const cplx<T> (&va)[8], const cplx<T> (&vb)[8], T (&A)[8], T (&B)[8],
                                          T (&C)[8], T (&E)[8], const Tw<T>& tb) {
   const int ja = lane, jb = lane ? 64 - lane : 32;
   const bool l0 = lane == 0;
+#ifndef COFEM_1K_TAB6
+  if constexpr (CT) {
+    const cplx<T> ua = tb.base[TBAS + lane], wa0 = tb.base[TBAS + 32 + lane];
+    const cplx<T> ub = tb.base[TBAS + 64 + lane], wb0 = tb.base[TBAS + 96 + lane];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      cplx<T> Af, Bf;
+      const cplx<T> wa = l0 ? va[(8 - r) & 7] : vb[7 - r];
+      ab_comp<T>(ua, wa0, r, Af, Bf);
+      dct2_post_ab<T>(Af, Bf, va[r], wa, A[r], C[r]);
+      if (l0 && r == 0) A[0] *= (T)0.70710678118654752440;     // k = 0: s0 / s = 1 / sqrt 2
+      const cplx<T> wb = l0 ? vb[7 - r] : va[7 - r];
+      ab_comp<T>(ub, wb0, r, Af, Bf);
+      dct2_post_ab<T>(Af, Bf, vb[r], wb, B[r], E[r]);
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int r = 0; r < 8; ++r) {
     const cplx<T> wa = l0 ? va[(8 - r) & 7] : vb[7 - r];
@@ -189,6 +264,13 @@ template <typename T> __device__ __forceinline__ const cplx<T>* tab1k(const DctA
   if constexpr (sizeof(T) == 8) return (const cplx<T>*)a.tab1k64; else return (const cplx<T>*)a.tab1k32;
 }
 
+// The per-pass kernels' shared-memory tables: the compact image (FFT twiddles + Makhoul bases) where
+// the factors are computed (fp32, COFEM_1K_CTAB), else the [0, n) prefix of the full layout.
+template <typename T, int PASS> __device__ __forceinline__ Tw<T> load_tab_pass(const DctArgs& a, cplx<T>* sm) {
+  if constexpr (ctp<T, PASS>()) return load_tables_ct<T>(tab1k<T>(a), sm);
+  else return load_tables<T>(tab1k<T>(a), sm, ntab<T, PASS>());
+}
+
 // ---------------------------------------------------------------- pass A
 // Shared memory: [RT warps][WREG] (FFT exchange / output tile row) then the twiddle tables.
 // Persistent kernels: work item w = (column j0 + w / NTILE, tile w % NTILE), grid-strided.
@@ -219,7 +301,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_INV
     if (dir) pf_line(cn.r + rn);
   }
   // pass A needs the FFT twiddles and the DCT-III pre tables only: the [0, TPRE) prefix (12.8 KB in fp32)
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG), TPRE);   // + barrier
+  const Tw<T> tb = load_tab_pass<T, 0>(a, reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
@@ -316,7 +398,7 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
     }
   }
   cplx<T> va[8], vb[8];
-  pre_all<T>(lane, A, B, C, E, va, vb, tb);
+  pre_all<T, ctp<T, 0>() && !CG>(lane, A, B, C, E, va, vb, tb);
   T* reg = sm + warp * WREG;
   fft512<T, +1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   const int ja = lane, jb = lane ? 64 - lane : 32;
@@ -501,7 +583,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_COL
   if (!any_active(ci, ncols)) return;
   if (blockIdx.x < ncols * NT && !ci.frozen[blockIdx.x / NT])     // the first item's line, before the tables
     pf_line(col_of<T>(a, j0 + blockIdx.x / NT).t1 + (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L);
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  const Tw<T> tb = load_tab_pass<T, 1>(a, reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
     if (ci.frozen[jj]) continue;
@@ -529,7 +611,7 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
     A[r] = ldx<CG>(ln + o[0]); B[r] = ldx<CG>(ln + o[1]); C[r] = ldx<CG>(ln + o[2]); E[r] = ldx<CG>(ln + o[3]);
   }
   cplx<T> va[8], vb[8];
-  pre_all<T>(lane, A, B, C, E, va, vb, tb);
+  pre_all<T, ctp<T, 1>() && !CG>(lane, A, B, C, E, va, vb, tb);
   T* reg = sm + warp * WREG;
   fft512<T, +1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
 #pragma unroll
@@ -540,7 +622,7 @@ __device__ __forceinline__ void cols_item(const DctArgs& a, int j, int tile, T* 
     if (!((mb >> (17 + 2 * r)) & 1u)) vb[r].y = (T)0;
   }
   fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
-  post_all<T>(lane, va, vb, A, B, C, E, tb);
+  post_all<T, ctp<T, 1>() && !CG>(lane, va, vb, A, B, C, E, tb);
 #pragma unroll
   for (int r = 0; r < 8; ++r) {     // natural-order column values -> tile row (the exchange region is free)
     int o[4];
@@ -710,7 +792,14 @@ template <typename T, bool CG = false>
 __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int tile, T* sm, const Tw<T>& tb);
 
 template <typename T>
+#ifndef COFEM_1K_FWD_MINB
+#define COFEM_1K_FWD_MINB 0   // 0: no min-blocks bound (nvcc then takes 80 registers, 3 CTAs per SM)
+#endif
+#if COFEM_1K_FWD_MINB > 0
+__global__ void __launch_bounds__(Geo<T>::RT * 32, sizeof(T) == 4 ? COFEM_1K_FWD_MINB : 1) k1k_rows_fwd(DctArgs a, int j0, int ncols) {
+#else
 __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j0, int ncols) {
+#endif
   constexpr int RT = Geo<T>::RT, NT = Work<T>::NTILE;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
@@ -722,7 +811,7 @@ __global__ void __launch_bounds__(Geo<T>::RT * 32) k1k_rows_fwd(DctArgs a, int j
     const int64_t rn = (int64_t)((blockIdx.x % NT) * RT + (threadIdx.x >> 5)) * L;
     pf_line(cn.t2 + rn); pf_line(cn.p + rn);
   }
-  const Tw<T> tb = load_tables<T>(tab1k<T>(a), reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
+  const Tw<T> tb = load_tab_pass<T, 2>(a, reinterpret_cast<cplx<T>*>(sm + RT * WREG));   // + barrier
   const int warp = threadIdx.x >> 5;
   for (int w = blockIdx.x; w < ncols * NT; w += gridDim.x) {
     const int jj = w / NT;
@@ -780,7 +869,7 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
   }
   fft512<T, -1>(va, vb, lane, reinterpret_cast<cplx<T>*>(reg), tb);
   T A[8], B[8], C[8], E[8];
-  post_all<T>(lane, va, vb, A, B, C, E, tb);
+  post_all<T, ctp<T, 2>() && !CG>(lane, va, vb, A, B, C, E, tb);
   double g = 0.0;
   if constexpr (sizeof(T) == 4) {
     // fp32: canonical values -> the warp's exchange region -> 16-byte vectors (lane l: elements
@@ -1244,8 +1333,8 @@ __global__ void k1k_mask_lanes(const uint8_t* __restrict__ maskT, uint32_t* __re
   maskL[idx] = w;
 }
 
-template <typename T> static size_t smem_bytes(int ntab = TTOT) {
-  return (size_t)Geo<T>::RT * WREG * sizeof(T) + (size_t)ntab * sizeof(cplx<T>);
+template <typename T> static size_t smem_bytes(int n = (ntab<T, 1>())) {
+  return (size_t)Geo<T>::RT * WREG * sizeof(T) + (size_t)n * sizeof(cplx<T>);
 }
 
 template <typename T> static void set_attrs() {
@@ -1253,9 +1342,9 @@ template <typename T> static void set_attrs() {
 #if COFEM_1K_INV_TMA
   cudaFuncSetAttribute(k1k_rows_inv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rtma::smem_bytes());
 #endif
-  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(TPRE));
+  cudaFuncSetAttribute(k1k_rows_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(ntab<T, 0>()));
   cudaFuncSetAttribute(k1k_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k1k_rows_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k1k_rows_fwd<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<T>(ntab<T, 2>()));
 }
 
 }  // namespace d1k
@@ -1274,7 +1363,7 @@ template <typename T> static std::vector<cplx<T>> build_tables() {
   using namespace d1k;
   typedef std::complex<double> C;
   const double PI = 3.14159265358979323846;
-  std::vector<cplx<T>> h(TTOT);
+  std::vector<cplx<T>> h(TTOT + (ctab<T>() ? NBAS : 0));
   auto put = [&](int i, C z) { h[i] = cplx<T>{(T)z.real(), (T)z.imag()}; };
   auto e = [](double ang) { return C(cos(ang), sin(ang)); };
   for (int r = 0; r < 8; ++r)
@@ -1299,6 +1388,16 @@ template <typename T> static std::vector<cplx<T>> build_tables() {
     put(TAB2 + ib(k), sc * q2 * (1.0 + I * hh) / 2.0);       // Bhat_k
 #endif
   }
+#ifndef COFEM_1K_TAB6
+  if (ctab<T>())     // per-lane bases u_k0 = (sc/2) e^{-i pi k0/2L}, v_k0 = (sc/2) e^{-5 i pi k0/2L}, k0 = ja | jb
+    for (int lane = 0; lane < 32; ++lane) {
+      const int ja = lane, jb = lane ? 64 - lane : 32;
+      put(TTOT + lane, sc / 2.0 * e(-PI * ja / (2.0 * L)));
+      put(TTOT + 32 + lane, sc / 2.0 * e(-5.0 * PI * ja / (2.0 * L)));
+      put(TTOT + 64 + lane, sc / 2.0 * e(-PI * jb / (2.0 * L)));
+      put(TTOT + 96 + lane, sc / 2.0 * e(-5.0 * PI * jb / (2.0 * L)));
+    }
+#endif
   return h;
 }
 
@@ -1405,7 +1504,7 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
     k1k_rows_inv_tma<<<std::max(1, g), rtma::RT * 32, rtma::smem_bytes(), st>>>(a, j0, ncols, dir ? 1 : 0);
   } else
 #endif
-  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(TPRE)), blk, smem_bytes<T>(TPRE), st>>>(
+  k1k_rows_inv<T><<<grid_of((const void*)k1k_rows_inv<T>, smem_bytes<T>(ntab<T, 0>())), blk, smem_bytes<T>(ntab<T, 0>()), st>>>(
       a, j0, ncols, dir ? 1 : 0);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_INV, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_COLS, st);
@@ -1421,7 +1520,8 @@ static cofem_status dct1k_apply_t(Ctx* c, int j0, int j1, int iter, bool dir, cu
   k1k_cols<T><<<grid_of((const void*)k1k_cols<T>, sm), blk, sm, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_COLS, st);
   launch_begin(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
-  k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>, sm), blk, sm, st>>>(a, j0, ncols);
+  const size_t smf = smem_bytes<T>(ntab<T, 2>());
+  k1k_rows_fwd<T><<<grid_of((const void*)k1k_rows_fwd<T>, smf), blk, smf, st>>>(a, j0, ncols);
   launch_end(c, mean ? KC_MEAN : KC_DCT_ROWS_FWD, st);
   return check_launch(c, "dct1k apply") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
