@@ -349,6 +349,19 @@ __device__ __forceinline__ void rows_inv_item(const DctArgs& a, int j, int tile,
         float4 rv[4], dd[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) { rv[i] = ldx<CG>(rr + lane + 32 * (4 * h + i)); dd[i] = dv[lane + 32 * (4 * h + i)]; }
+#ifdef COFEM_EXP_FUSE_EMU   // timing experiment only: the extra traffic of a fused update (q read, r write)
+        {
+          const float4* __restrict__ qq4 = reinterpret_cast<const float4*>(c.q + rb);
+          float4* rw = const_cast<float4*>(rr);
+          const float z0 = (float)(a.beta * 0.0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 qv = qq4[lane + 32 * (4 * h + i)];
+            rv[i].x -= z0 * qv.x; rv[i].y -= z0 * qv.y; rv[i].z -= z0 * qv.z; rv[i].w -= z0 * qv.w;
+            rw[lane + 32 * (4 * h + i)] = rv[i];
+          }
+        }
+#endif
 #pragma unroll
         for (int i = 0; i < 4; ++i) {    // a6: p = M^-1 r + b p
           pv[i].x = dd[i].x * rv[i].x + bb * pv[i].x; pv[i].y = dd[i].y * rv[i].y + bb * pv[i].y;
@@ -886,11 +899,32 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
     const float4* __restrict__ al = reinterpret_cast<const float4*>(alpha_of<T>(a, j) + rb);
     float4* __restrict__ qq = reinterpret_cast<float4*>(c.q + rb);
     const float beta = (float)a.beta;
+#ifdef COFEM_EXP_FUSE_EMU   // timing experiment only: rho, delta1, delta2 of single-reduction CG in pass C
+    double e1 = 0.0, e2 = 0.0, e3 = 0.0;
+    const float4* __restrict__ rr4 = reinterpret_cast<const float4*>(c.r + rb);
+    const float4* __restrict__ dd4 = reinterpret_cast<const float4*>(c.dinv + rb);
+#endif
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float4 pv[4], av[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) { pv[i] = ldx<CG>(pp + lane + 32 * (4 * h + i)); av[i] = al[lane + 32 * (4 * h + i)]; }
+#ifdef COFEM_EXP_FUSE_EMU
+      float4 rv[4], dv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { rv[i] = rr4[lane + 32 * (4 * h + i)]; dv[i] = dd4[lane + 32 * (4 * h + i)]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 x = r4[lane + 32 * (4 * h + i)];
+        const float xs[4] = {x.x, x.y, x.z, x.w}, rs[4] = {rv[i].x, rv[i].y, rv[i].z, rv[i].w};
+        const float ds[4] = {dv[i].x, dv[i].y, dv[i].z, dv[i].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float zr = ds[e] * rs[e], zq = ds[e] * xs[e];
+          e1 += (double)rs[e] * (double)zr; e2 += (double)zq * (double)rs[e]; e3 += (double)zq * (double)xs[e];
+        }
+      }
+#endif
 #pragma unroll
       for (int i = 0; i < 4; ++i) {   // a3: q = beta Phi^T Phi p + alpha o p; a4: gamma partial
         const float4 x = r4[lane + 32 * (4 * h + i)];
@@ -903,6 +937,10 @@ __device__ __forceinline__ double rows_fwd_item(const DctArgs& a, int j, int til
       }
     }
     __syncwarp();                    // the next item's FFT reuses the region
+#ifdef COFEM_EXP_FUSE_EMU
+    e1 = warp_sum(e1); e2 = warp_sum(e2); e3 = warp_sum(e3);
+    g += 1e-300 * (e1 + e2 + e3);
+#endif
     return warp_sum(g);
   }
   const T* __restrict__ pp = c.p + rb;
