@@ -106,8 +106,10 @@ typedef struct {
    * stencil); 2 = as 0 without the cluster CG loop (small dense problems on the per-iteration
    * tensor-core kernels). */
   int32_t apply_path;
-  /* 1024 x 1024 DCT path: probe columns run as this many concurrent groups on their own streams
-   * (DESIGN.md §7.1); 0 = auto (2).  Range 0..4. */
+  /* Concurrent probe-column groups, 0 = auto.  1024 x 1024 DCT path: that many groups on their own
+   * streams (auto 2, range 0..4).  Dense cluster CG loop: that many thread-block
+   * clusters in one launch, each solving a contiguous share of the probes (cluster 0 also the mean;
+   * DESIGN.md §7.2.1; auto 4, at most K and 4).  Ignored elsewhere. */
   int32_t probe_groups;
   /* 1 (default): each E-step is captured once into a CUDA graph and replayed; 0: launched directly. */
   int32_t use_graph;

@@ -11,7 +11,9 @@
 //                             over the NC partials in fixed order and stores them into EVERY CTA's W
 //   gamma_j, rho'_j         : per-CTA partials, every CTA sums the NC partials in fixed order and
 //                             takes the same step lengths / freeze decisions (R5) on its own copy
-// Four cluster barriers per CG iteration, no global memory traffic inside the loop.
+// Four cluster barriers per CG iteration, no global memory traffic inside the loop.  The probe
+// columns may be split over several clusters of one launch (dcl_groups; cluster 0 also solves the
+// mean system), each writing its own s partial; the partials are summed in cluster order.
 //
 // Arithmetic mirrors the SIMT kernels (op_dense.cu) and k_update / k_dir (cofem.cu): probe columns
 // in probe precision TP with fp32 Phi, the mean column in fp64 (fp32 Phi promoted exactly), gamma,
@@ -46,9 +48,13 @@ constexpr int NC = COFEM_DCL_NC;            // CTAs per cluster (8: the portable
 constexpr int THREADS = COFEM_DCL_THREADS;
 constexpr int KG = COFEM_DCL_KG;            // probe columns per thread work unit (register accumulators)
 
+constexpr int MAXCL = 4;                    // clusters per launch (probe-column groups)
+
 struct Args {
   const float* phi; int64_t ld;
   int N, D, Dc, DcP, K, U;
+  int ncl, Kmax;                    // clusters: cluster g solves probes [K g / ncl, K (g+1) / ncl) (+ the mean if g = 0)
+  double* sg[MAXCL];                // cluster g's s partial (sg[0] = s); summed in cluster order afterwards
   double beta, invK;
   const double* alpha; const double* dinv64; const void* dinvp;
   double* x0; const double* r0; const double* p0;
@@ -119,8 +125,13 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int N = a.N, K = a.K, m = K + 1, Dc = a.Dc, DcP = a.DcP, KP = kpad(K), G = KP / KG;
-  const Layout L = layout(N, Dc, DcP, K, sizeof(TP));
+  // probe-column group of this cluster: local column j (0 = mean, on cluster 0 only) is global
+  // column jg(j); with one cluster this is the whole E-step
+  const int cid = blockIdx.x / NC, klo = (int)((int64_t)a.K * cid / a.ncl), khi = (int)((int64_t)a.K * (cid + 1) / a.ncl);
+  const bool has_mean = cid == 0;
+  auto jg = [&](int j) { return j == 0 ? 0 : klo + j; };
+  const int N = a.N, K = khi - klo, m = K + 1, Dc = a.Dc, DcP = a.DcP, KP = kpad(K), G = KP / KG;
+  const Layout L = layout(N, Dc, DcP, a.Kmax, sizeof(TP));
   float* phs = reinterpret_cast<float*>(smraw + L.phi);     // [N][DcP]
   TP* Ps = reinterpret_cast<TP*>(smraw + L.Pp);             // [Dc][KP]
   TP* Rs = reinterpret_cast<TP*>(smraw + L.Rp);
@@ -157,10 +168,10 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     const int dl = i / KP, k = i % KP;
     const bool v = dl < Dl && k < K;
     const int d = d0 + dl;
-    Ps[i] = v ? Pg[(int64_t)k * a.Dp + d] : (TP)0;
-    Rs[i] = v ? Rg[(int64_t)k * a.Dp + d] : (TP)0;
+    Ps[i] = v ? Pg[(int64_t)(klo + k) * a.Dp + d] : (TP)0;
+    Rs[i] = v ? Rg[(int64_t)(klo + k) * a.Dp + d] : (TP)0;
     Qs[i] = (TP)0;
-    sgn[i] = v ? (uint8_t)((a.bits[(int64_t)k * a.wpc + (d >> 5)] >> (d & 31)) & 1u) : (uint8_t)0;
+    sgn[i] = v ? (uint8_t)((a.bits[(int64_t)(klo + k) * a.wpc + (d >> 5)] >> (d & 31)) & 1u) : (uint8_t)0;
   }
   for (int i = tid; i < N * KP; i += THREADS) { wpart[i] = (TP)0; wfull[i] = (TP)0; }
   for (int dl = tid; dl < Dc; dl += THREADS) {
@@ -168,9 +179,12 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     const int d = d0 + dl;
     dvp[dl] = v ? dvg[d] : (TP)0;
     xs[dl] = v ? a.x0[d] : 0.0; rs[dl] = v ? a.r0[d] : 0.0; ps[dl] = v ? a.p0[d] : 0.0; qs[dl] = 0.0;
-    dv[dl] = v ? a.dinv64[d] : 0.0; als[dl] = v ? a.alpha[d] : 0.0; sacc[dl] = v ? a.s[d] : 0.0;
+    dv[dl] = v ? a.dinv64[d] : 0.0; als[dl] = v ? a.alpha[d] : 0.0; sacc[dl] = v && has_mean ? a.s[d] : 0.0;
   }
-  for (int j = tid; j < m; j += THREADS) cs[j] = a.cs[j];
+  for (int j = tid; j < m; j += THREADS) {
+    cs[j] = a.cs[jg(j)];
+    if (j == 0 && !has_mean) cs[0].frozen = 1;     // the mean system is cluster 0's
+  }
   const int Nr = (N + NC - 1) / NC, n_lo = min(N, rank * Nr), n_hi = min(N, n_lo + Nr);
   cl.sync();
 
@@ -181,7 +195,7 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     for (int j = tid; j < m; j += THREADS) act |= !cs[j].frozen;
     if (!__syncthreads_or(act)) break;
     // ---- 1. W partial = Phi_c P_c (probe precision) and Phi_c p0 (fp64)
-    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : N * (G + 1)); u += THREADS) {
+    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : N * (G + (has_mean ? 1 : 0))); u += THREADS) {
       const int n = u % N, g = u / N;
       const float* ph = phs + n * DcP;
       if (g < G) {
@@ -205,8 +219,9 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     }
     cl.sync();
     // ---- 2. rows [n_lo, n_hi): sum the NC partials in rank order, store into every CTA's W
-    for (int i = tid; i < (COFEM_DCL_EXP >= 2 ? 0 : (n_hi - n_lo) * (K + 1)); i += THREADS) {
-      const int n = n_lo + i / (K + 1), k = i % (K + 1);
+    const int kw = K + (has_mean ? 1 : 0);          // W columns: the probes (+ the mean)
+    for (int i = tid; i < (COFEM_DCL_EXP >= 2 ? 0 : (n_hi - n_lo) * kw); i += THREADS) {
+      const int n = n_lo + i / kw, k = i % kw;
       if (k < K) {
         TP x[NC];
 #pragma unroll
@@ -230,7 +245,7 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     cl.sync();
     // ---- 3. Q = beta Phi_c^T W + alpha o P (a3), q0 likewise in fp64; gamma partials (a4)
     const TP betat = (TP)a.beta;
-    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : Dl * (G + 1)); u += THREADS) {
+    for (int u = tid; u < (COFEM_DCL_EXP >= 1 ? 0 : Dl * (G + (has_mean ? 1 : 0))); u += THREADS) {
       const int dl = u % Dl, g = u / Dl;
       if (g < G) {
         TP acc[KG];
@@ -257,7 +272,7 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     __syncthreads();
     for (int j = warp; j < m; j += THREADS / 32) {   // one warp per column: lane-strided, then the tree
       double g = 0.0;
-      if (j == 0) for (int dl = lane; dl < Dl; dl += 32) g += ps[dl] * qs[dl];
+      if (j == 0) { if (has_mean) for (int dl = lane; dl < Dl; dl += 32) g += ps[dl] * qs[dl]; }
       else for (int dl = lane; dl < Dl; dl += 32) g += (double)Ps[dl * KP + j - 1] * (double)Qs[dl * KP + j - 1];
       g = warp_sum(g);
       if (lane == 0) gpart[j] = g;
@@ -338,10 +353,24 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
     __syncthreads();
   }
   // ---- results: mu slice, s slice; the column states (identical in every CTA) from rank 0
-  for (int dl = tid; dl < Dl; dl += THREADS) { a.x0[d0 + dl] = xs[dl]; a.s[d0 + dl] = sacc[dl]; }
+  for (int dl = tid; dl < Dl; dl += THREADS) {
+    if (has_mean) a.x0[d0 + dl] = xs[dl];
+    a.sg[cid][d0 + dl] = sacc[dl];
+  }
   if (rank == 0)
-    for (int j = tid; j < m; j += THREADS) a.cs[j] = cs[j];
+    for (int j = tid; j < m; j += THREADS)
+      if (j > 0 || has_mean) a.cs[jg(j)] = cs[j];
   cl.sync();                         // no CTA leaves while others may still read its shared memory
+}
+
+__global__ void k_sum_parts(int64_t D, int ncl, double* __restrict__ s, const double* __restrict__ s1,
+                            const double* __restrict__ s2, const double* __restrict__ s3) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
+    double v = s[d] + s1[d];
+    if (ncl > 2) v += s2[d];
+    if (ncl > 3) v += s3[d];
+    s[d] = v;
+  }
 }
 
 }  // namespace dcl
@@ -349,6 +378,20 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
 static size_t dcl_smem(const Ctx* c, int K) {
   const int Dc = (int)((c->D + dcl::NC - 1) / dcl::NC);
   return dcl::layout((int)c->N, Dc, Dc | 1, K, c->probe64 ? 8 : 4).total;
+}
+
+// Clusters per E-step: the probe columns split over ncl concurrent clusters (each on its own NC
+// SMs, each with its own copy of Phi's slices; the columns are independent systems, R3), so each
+// cluster's per-iteration loops (products, update, per-column dots) cover a quarter of the columns
+// while the barrier and reduction latency stays the same; options.probe_groups, else COFEM_DCL_GROUPS.
+#ifndef COFEM_DCL_GROUPS
+#define COFEM_DCL_GROUPS 4   // C1 E-step (fixed alpha): 1 cluster 1.36 ms, 2 1.13, 3 1.00, 4 1.00
+#endif
+static int dcl_groups(const Ctx* c, int K) {
+  int g = c->opt.probe_groups > 0 ? c->opt.probe_groups : COFEM_DCL_GROUPS;
+  g = std::max(1, std::min(g, std::min(dcl::MAXCL, K)));
+  while (g > 1 && !c->gs[g - 1]) --g;
+  return g;
 }
 
 bool dense_cluster_eligible(const Ctx* c) {
@@ -367,6 +410,11 @@ cofem_status dense_cluster_setup(Ctx* c) {
                               : raise_smem_attr((const void*)dcl::k_dense_cluster_cg<float>, sm);
   if (e != cudaSuccess) { c->err = std::string("dense cluster setup: ") + cudaGetErrorString(e); return COFEM_ERR_CUDA; }
   c->dense_cluster = true;
+  for (int g = 1; g < dcl::MAXCL && g < Ctx::MAXG; ++g)      // the clusters' s partials (dcl_groups)
+    if (!c->gs[g]) {
+      if (cudaMalloc(&c->gs[g], c->Dp * sizeof(double)) != cudaSuccess) { c->gs[g] = nullptr; cudaGetLastError(); break; }
+      cudaMemset(c->gs[g], 0, c->Dp * sizeof(double));          // the padding [D, Dp) stays 0
+    }
   return COFEM_OK;
 }
 
@@ -379,10 +427,15 @@ cofem_status dense_cluster_cg(Ctx* c, int K, double invK) {
   a.alpha = c->alpha; a.dinv64 = c->dinv64; a.dinvp = c->dinvp;
   a.x0 = c->x0; a.r0 = c->r0; a.p0 = c->p0; a.R = c->R; a.P = c->P;
   a.s = c->s; a.bits = c->bits; a.Dp = c->Dp; a.wpc = c->Dp / 32; a.cs = c->cs;
-  const size_t sm = dcl::layout(a.N, a.Dc, a.DcP, K, c->probe64 ? 8 : 4).total;
+  a.ncl = dcl_groups(c, K);
+  a.Kmax = (K + a.ncl - 1) / a.ncl;
+  for (int g = 0; g < dcl::MAXCL; ++g) a.sg[g] = g == 0 ? c->s : (g < a.ncl ? c->gs[g] : nullptr);
+  const size_t sm = dcl::layout(a.N, a.Dc, a.DcP, a.Kmax, c->probe64 ? 8 : 4).total;
   launch_begin(c, KC_DENSE_CLUSTER);
-  if (c->probe64) dcl::k_dense_cluster_cg<double><<<dcl::NC, dcl::THREADS, sm, c->stream>>>(a);
-  else dcl::k_dense_cluster_cg<float><<<dcl::NC, dcl::THREADS, sm, c->stream>>>(a);
+  if (c->probe64) dcl::k_dense_cluster_cg<double><<<dcl::NC * a.ncl, dcl::THREADS, sm, c->stream>>>(a);
+  else dcl::k_dense_cluster_cg<float><<<dcl::NC * a.ncl, dcl::THREADS, sm, c->stream>>>(a);
+  if (a.ncl > 1)                      // s = ((s_0 + s_1) + s_2) + s_3 in cluster order (deterministic)
+    dcl::k_sum_parts<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, a.ncl, a.sg[0], a.sg[1], a.sg[2], a.sg[3]);
   launch_end(c, KC_DENSE_CLUSTER);
   return check_launch(c, "k_dense_cluster_cg") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }

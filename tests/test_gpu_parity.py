@@ -641,6 +641,30 @@ def test_dense_cluster_cg_loop(w):
     assert ctx.report()["frozen_at"] is not None
 
 
+@pytest.mark.parametrize("w", [synth.preset("C1"), synth.dense(64, 1000, 12, K=33, U=80, T=2, seed=9),
+                               synth.dense(37, 203, 4, K=3, U=40, T=2, seed=8)], ids=lambda w: w.name)
+def test_dense_cluster_groups(w):
+    """The probe columns split over 1..4 thread-block clusters of one launch (probe_groups;
+    op_dense_cluster.cu dcl_groups; more clusters than probes falls back to K): the mean system is
+    cluster 0's whatever the split, so mu is bitwise the same; s differs only by the order of the
+    clusters' partial sums (cluster order, deterministic: repeated runs are bitwise equal), and
+    every split meets the north_star bar against the oracle.  Also on an EM (alpha, mu)."""
+    omu, os_, _ = estep(op_of(w), w.y, w.beta, np.ones(w.D), w.K, 3, 1, w.U)
+    m1, s1 = gpu_estep(ctx_of(w, max_probes=w.K, probe_groups=1), w, np.ones(w.D), w.K, 3, 1)
+    bar = max(1e-4, 2 * rel(s1, os_))
+    em1 = gpu_em(ctx_of(w, max_probes=w.K, probe_groups=1), w, w.T, w.K, 5)
+    for g in (2, 3, 4):
+        ctx = ctx_of(w, max_probes=w.K, probe_groups=g)
+        mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
+        mu2, s2 = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
+        assert np.array_equal(mu, m1), g
+        assert np.array_equal(mu, mu2) and np.array_equal(s, s2), g
+        assert rel(s, s1) <= 1e-12 and float(np.abs(s - s1).max() / np.abs(s1).max()) <= 1e-12, (g, rel(s, s1))
+        assert rel(mu, omu) <= 1e-4 and rel(s, os_) <= bar, (g, rel(mu, omu), rel(s, os_), bar)
+        a, emu, es = gpu_em(ctx, w, w.T, w.K, 5)
+        assert rel(1 / a, 1 / em1[0]) <= 1e-6 and rel(emu, em1[1]) <= 1e-6, (g, rel(1 / a, 1 / em1[0]))
+
+
 @pytest.mark.parametrize("path", [0, 1, 2], ids=["cluster", "simt", "tcgen05"])
 def test_context_created_later_with_smaller_smem_does_not_break_earlier(path):
     """Dynamic shared-memory limits are per kernel function, not per context: a context set up after
