@@ -100,7 +100,7 @@ typedef struct {
    * 0 (default): fixed U iterations (BASELINE north_star, R5).  Must be in [0, 1). */
   double cg_rtol;
   /* Operator path (tests, comparisons): 0 = auto, the fastest eligible kernels (dense: the whole
-   * CG loop in one thread-block cluster when Phi fits its shared memory -- config 1 --, else
+   * CG loop in thread-block clusters (one launch) when Phi fits a cluster's shared memory -- config 1 --, else
    * tcgen05 3xTF32 for fp32 probes; DCT2 1024 x 1024: the warp-per-line FFT path; CIRCCONV:
    * overlap-save FFT); 1 = the general kernels (dense FP32 SIMT, generic DCT passes, direct 127-tap
    * stencil); 2 = as 0 without the cluster CG loop (small dense problems on the per-iteration
