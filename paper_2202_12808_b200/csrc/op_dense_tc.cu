@@ -171,6 +171,13 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
                "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                : "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
@@ -215,12 +222,25 @@ __device__ __forceinline__ float tf32_hi(float x) {
 // 1: bn <= 64, three N = bn MMAs per K = 8, 4 buffers of 64 columns (the MMA of pair p waits for
 // the promotion of pair p - 4: never on the critical path); 2: bn <= 128, unfused, 2 x 128.
 // Pipeline depth: 6 stages of <= 33 KB (bn <= 64) or 4 of <= 49 KB (bn <= 128).
-__host__ __device__ constexpr int stages_of(int mode) { return mode == 2 ? 4 : 6; }
-__host__ __device__ constexpr int nacc_of(int mode) { return mode == 1 ? 4 : 2; }
+// 3: bn <= 32 (C2), three N = bn MMAs, 4 accumulator buffers of only 32 columns, so TMEM holds
+// SIX A buffers (three pairs): the splitters run two pairs ahead of the MMAs instead of one
+// (the split chain MMA(p) -> split(p + NP) -> MMA(p + NP) is what bounds these kernels).
+#ifndef COFEM_TC_M3_STAGES
+#define COFEM_TC_M3_STAGES 8 // 6: 17.97 ms at PLAG 3
+#endif
+#ifndef COFEM_TC_M3_PLAG
+#define COFEM_TC_M3_PLAG 2   // C2 E-step: 2 17.90 ms, 3 18.07, 4 18.04 (mode 1: 19.10)
+#endif
+__host__ __device__ constexpr int stages_of(int mode) { return mode == 2 ? 4 : mode == 3 ? COFEM_TC_M3_STAGES : 6; }
+__host__ __device__ constexpr int nacc_of(int mode) { return mode == 1 || mode == 3 ? 4 : 2; }
+__host__ __device__ constexpr int accw_of(int mode) { return mode == 3 ? 32 : mode == 1 ? 64 : 128; }
+__host__ __device__ constexpr int nabuf_of(int mode) { return mode == 3 ? 6 : 4; }        // TMEM A buffers
+__host__ __device__ constexpr int tma_of(int mode) { return mode == 3 ? 128 : TM_A; }     // their base column
+__host__ __device__ constexpr int plag_of(int mode) { return mode == 3 ? COFEM_TC_M3_PLAG : PLAG; }
 
 // Accumulator columns promoted (and written by the epilogue) per splitter group: the bn <= 64
 // logical columns split evenly over the 4 groups (128 / 4 in mode 2).
-__host__ __device__ constexpr int cpg_of(int mode) { return mode == 2 ? 32 : 16; }
+__host__ __device__ constexpr int cpg_of(int mode) { return mode == 2 ? 32 : mode == 3 ? 8 : 16; }
 
 // Shared-memory plan (dynamic, 1024-aligned):
 // STAGES x [A: MT tiles x 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64 (1 KB)]
@@ -287,8 +307,12 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
                          const CUtensorMap* mBl, int row0, int k0, int nk, const double* __restrict__ mean_w,
                          double (&acc0)[1], float (&sum)[1][cpg_of(MODE)]) {
   constexpr int NACC = nacc_of(MODE), S = stages_of(MODE);      // compile-time: no integer division on the MMA thread's path
-  using TP = TmemPlan<1, NACC>;
-  constexpr int CPG = cpg_of(MODE);
+  constexpr int CPG = cpg_of(MODE), ACCW = accw_of(MODE), NABUF = nabuf_of(MODE), NP = NABUF / 2, PL = plag_of(MODE);
+  struct TP {      // TMEM plan of this mode: NACC accumulators of ACCW columns, NABUF A buffers (hi 32 | lo 32)
+    static __device__ __forceinline__ uint32_t acc(int ab, int) { return ab * ACCW; }
+    static __device__ __forceinline__ uint32_t abuf(int b, int) { return tma_of(MODE) + b * 64; }
+  };
+  static_assert(NACC * ACCW <= tma_of(MODE) && tma_of(MODE) + NABUF * 64 <= TMEM_COLS, "TMEM budget");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
   const int np = (nk + 1) >> 1;                     // K-step pairs (= promotion chunks)
@@ -345,7 +369,7 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
           if (kt >= nk) break;
           const int s = kt % S;
           const uint32_t bh = su32(sm + pl.bhi_off(s)), bl = su32(sm + pl.blo_off(s));
-          const uint32_t ahi = tmem + TP::abuf(kt & 3, 0), alo = ahi + 32;
+          const uint32_t ahi = tmem + TP::abuf(kt % NABUF, 0), alo = ahi + 32;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {        // K = 8 per tf32 MMA; B advances 32 B in the swizzle atom
             const uint64_t dbh = desc_k_sw128(bh + kk * 32);
@@ -381,6 +405,14 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       if (q == 0 && lane == 0) TC_TRACE(4 * c + g, 7)
       fence_after();
 #pragma unroll
+      if constexpr (CPG == 8) {                         // mode 3: 8 columns per group
+        if (g * CPG < pl.bn) {
+          float v[8];
+          tmem_ld8(lane_addr + TP::acc(ab, 0) + g * CPG, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sum[0][i] += v[i];
+        }
+      } else
       for (int cc = 0; cc < CPG; cc += 16) {
         if (g * CPG + cc >= pl.bn) continue;           // columns past bn carry nothing
 #ifdef COFEM_TC_EXP_NOPROMO
@@ -404,16 +436,16 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
     const int nk2 = 2 * np;                           // an odd nk leaves the second half of the last pair empty
     for (int kt = g; kt < nk2; kt += NGROUP) {
       // promote the chunks PLAG pairs behind this step (their MMAs need no split work of ours anymore)
-      while (cdone < np && 2 * (cdone + PLAG) <= kt) promote(cdone++);
+      while (cdone < np && 2 * (cdone + PL) <= kt) promote(cdone++);
       const int p = kt >> 1;
       if (kt < nk) {
         const int s = kt % S;
-        if (p >= 2) mbar_wait(&bs.pair_done[(p - 2) & 3], ((p - 2) >> 2) & 1, SPLIT_SLEEP);   // A buffer free
+        if (p >= NP) mbar_wait(&bs.pair_done[(p - NP) & 3], ((p - NP) >> 2) & 1, SPLIT_SLEEP);   // A buffer free
         if (q == 0 && lane == 0) TC_TRACE(kt, 5)
         mbar_wait(&bs.full[s], (kt / S) & 1, SPLIT_SLEEP);
         if (q == 0 && lane == 0) TC_TRACE(kt, 4)
         const unsigned char* a = sm + pl.a_off(s, 0);
-        const uint32_t buf = TP::abuf(kt & 3, 0);
+        const uint32_t buf = TP::abuf(kt % NABUF, 0);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           float x[8];
@@ -768,7 +800,10 @@ cofem_status dense_tc_setup(Ctx* c) {
 #ifdef COFEM_TC_FUSE
   t->mode = t->bn > 64 ? 2 : 0;                   // timing comparison build (tools/build_variant.sh)
 #else
-  t->mode = t->bn > 64 ? 2 : 1;
+#ifndef COFEM_TC_MODE3
+#define COFEM_TC_MODE3 1      // bn <= 32: mode 3 (three pairs of TMEM A buffers); 0 = mode 1 (A/B switch)
+#endif
+  t->mode = t->bn > 64 ? 2 : (COFEM_TC_MODE3 && t->bn <= 32 ? 3 : 1);
 #endif
   t->pl = plan_for(t->bn, t->mt, t->mode);
   if (smem_of(t->pl) > 227 * 1024) { c->err = "dense tc: shared-memory plan too large"; return COFEM_ERR_INVALID; }
@@ -805,9 +840,11 @@ cofem_status dense_tc_setup(Ctx* c) {
   raise_smem_attr((const void*)k_tc_phiP<0>, sm);
   raise_smem_attr((const void*)k_tc_phiP<1>, sm);
   raise_smem_attr((const void*)k_tc_phiP<2>, sm);
+  raise_smem_attr((const void*)k_tc_phiP<3>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<0>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<1>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<2>, sm);
+  raise_smem_attr((const void*)k_tc_phiTW<3>, sm);
   c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
   return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
@@ -827,6 +864,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   const dim3 g1((unsigned)((c->N + rows - 1) / rows), t->splits);
   if (t->mode == 0) k_tc_phiP<0><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else if (t->mode == 1) k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  else if (t->mode == 3) k_tc_phiP<3><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
                                                        c->sharded ? nullptr : t->Wl, t->w0);
@@ -849,6 +887,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   const unsigned g2 = (unsigned)((c->D + rows - 1) / rows);
   if (t->mode == 0) k_tc_phiTW<0><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else if (t->mode == 1) k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  else if (t->mode == 3) k_tc_phiTW<3><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
