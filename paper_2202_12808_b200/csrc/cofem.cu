@@ -108,6 +108,8 @@ struct VecArgs {
   int warm;         // k_init: the mean column starts from x0 (= mu of the previous E-step; q0 = A x0)
   int nofinish;     // k_update: no rho' reduction (single-reduction CG, R23: rho' came with gamma)
   double* s_part; unsigned* tile_cnt;
+  int spersist;     // k_update chunks: s_part[chunk] accumulates over the whole E-step (k_sum_chunks adds
+                    // them to s at its end) instead of the per-iteration ticketed chunk sum
 };
 
 // Probe-stream parameters of the current E-step, read from device memory so that one
@@ -393,7 +395,16 @@ __global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM
         if (lane == 0) sh.red[warp][k + u + 1] += acc;
       }
     }
-    if (nch == 1) {
+    if (nch > 1 && a.spersist) {      // this (tile, chunk) item owns s_part[chunk] on the tile: plain RMW
+      if (any) {
+        double sv[8];
+        double* sp = a.s_part + (int64_t)chunk * a.Dp + d0;
+        ld8(sp, sv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sv[e] += sacc[e];
+        st8(sp, sv);
+      }
+    } else if (nch == 1) {
       if (any) {
         double sv[8];
         ld8(a.s + d0, sv);
@@ -434,6 +445,16 @@ __global__ void __launch_bounds__(VEC_THREADS, UNR == 2 ? COFEM_UPD_MINB : COFEM
     c.rho = v;
     cs[j] = c;
   });
+}
+
+// End of an E-step whose k_update accumulated s per column chunk (VecArgs::spersist): s += sum of
+// the chunk accumulators in chunk order (deterministic), which are zeroed for the next E-step.
+__global__ void k_sum_chunks(int64_t Dp, int nch, double* __restrict__ s, double* __restrict__ s_part) {
+  for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < Dp; d += (int64_t)gridDim.x * blockDim.x) {
+    double v = s[d];
+    for (int c = 0; c < nch; ++c) { v += s_part[(int64_t)c * Dp + d]; s_part[(int64_t)c * Dp + d] = 0.0; }
+    s[d] = v;
+  }
 }
 
 // a6: P_j = M^-1 R_j + b_j P_j  (separate kernel for dense / conv; fused into DCT pass A).
@@ -674,6 +695,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.uchunks = c->upd_chunks; a.s_part = c->s_part; a.tile_cnt = c->tile_cnt; a.mean_grid = c->vec_grid;
   a.warm = c->warm_now ? 1 : 0;
   a.nofinish = c->sr ? 1 : 0;
+  a.spersist = 0;
   return a;
 }
 
@@ -918,6 +940,11 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   if (c->fast1k) return cg_loop_split(c, K, invK, dct1k_apply);
   if (c->fast_conv && c->sharded) return cg_loop_conv_sharded(c, K, invK);
   if (c->fast_conv) return cg_loop_split(c, K, invK, conv_fft_apply);
+  // small D with chunked probe updates: per-chunk s accumulators for the whole E-step
+#ifndef COFEM_UPD_SPERSIST
+#define COFEM_UPD_SPERSIST 1   // A/B build switch: 0 = the per-iteration ticketed chunk sum
+#endif
+  const int spersist = COFEM_UPD_SPERSIST && c->upd_chunks > 1 ? 1 : 0;   // s is rank-local in the sharded modes too
   for (int it = 0; it < c->opt.cg_iters; ++it) {
     cofem_status st;
     if (c->kind == COFEM_OP_DCT2_MASKED) {
@@ -928,11 +955,24 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
     }
     if (st != COFEM_OK) return st;
     launch_begin(c, KC_UPDATE);
-    if (c->probe64) k_update<double, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, invK));
-    else k_update<float, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, invK));
+    if (c->probe64) {
+      VecArgs<double> va = vec_args<double>(c, K, invK);
+      va.spersist = spersist;
+      k_update<double, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(va);
+    } else {
+      VecArgs<float> va = vec_args<float>(c, K, invK);
+      va.spersist = spersist;
+      k_update<float, 1><<<c->upd_grid, VEC_THREADS, 0, c->stream>>>(va);
+    }
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_update")) return COFEM_ERR_CUDA;
     if (c->sharded && !c->sr && (st = sharded_finish(c, m, 2, it)) != COFEM_OK) return st;
+  }
+  if (spersist) {
+    launch_begin(c, KC_UPDATE);
+    k_sum_chunks<<<std::max(1, c->vec_grid), VEC_THREADS, 0, c->stream>>>(c->Dp, c->upd_chunks, c->s, c->s_part);
+    launch_end(c, KC_UPDATE);
+    if (check_launch(c, "k_sum_chunks")) return COFEM_ERR_CUDA;
   }
   return COFEM_OK;
 }
