@@ -108,6 +108,7 @@ struct VecArgs {
   int warm;         // k_init: the mean column starts from x0 (= mu of the previous E-step; q0 = A x0)
   int nofinish;     // k_update: no rho' reduction (single-reduction CG, R23: rho' came with gamma)
   double* s_part; unsigned* tile_cnt;
+  float *Ph, *Pl;   // k_dir (tensor-core dense path): also write the tf32 hi / lo halves of the new P
   int spersist;     // k_update chunks: s_part[chunk] accumulates over the whole E-step (k_sum_chunks adds
                     // them to s at its end) instead of the per-iteration ticketed chunk sum
 };
@@ -480,6 +481,18 @@ __global__ void __launch_bounds__(VEC_THREADS) k_dir(VecArgs<TP> a) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) p[e] = dv[e] * r[e] + bt * p[e];
       st8(Pk, p);
+      if constexpr (sizeof(TP) == 4) {
+        if (a.Ph) {   // the next apply's B operand halves (k_tc_split_p's rule: hi = rna tf32, lo = p - hi)
+          float h[8], l[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            uint32_t u;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"((float)p[e]));
+            h[e] = __uint_as_float(u); l[e] = (float)p[e] - h[e];
+          }
+          st8(a.Ph + (int64_t)(j - 1) * a.Dp + d0, h); st8(a.Pl + (int64_t)(j - 1) * a.Dp + d0, l);
+        }
+      }
     }
   }
 }
@@ -696,6 +709,7 @@ static VecArgs<TP> vec_args(Ctx* c, int K, double invK) {
   a.warm = c->warm_now ? 1 : 0;
   a.nofinish = c->sr ? 1 : 0;
   a.spersist = 0;
+  a.Ph = a.Pl = nullptr;
   return a;
 }
 
@@ -717,7 +731,17 @@ cofem_status launch_dir(Ctx* c, int m) {
   dim3 grid((unsigned)std::min<int64_t>(c->Dp / VEC_TILE, (int64_t)c->num_sms * 4), m);
   launch_begin(c, KC_DIR);
   if (c->probe64) k_dir<double><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<double>(c, K, 0));
-  else k_dir<float><<<grid, VEC_THREADS, 0, c->stream>>>(vec_args<float>(c, K, 0));
+  else {
+    VecArgs<float> va = vec_args<float>(c, K, 0);
+#ifndef COFEM_DIR_SPLIT
+#define COFEM_DIR_SPLIT 1    // A/B build switch: 0 = k_tc_split_p in every apply
+#endif
+    if (COFEM_DIR_SPLIT && c->kind == COFEM_OP_DENSE && c->dense_tc) {   // the next tensor-core apply skips its split
+      dense_tc_p_split(c, &va.Ph, &va.Pl);
+      c->p_presplit = va.Ph != nullptr;
+    }
+    k_dir<float><<<grid, VEC_THREADS, 0, c->stream>>>(va);
+  }
   launch_end(c, KC_DIR);
   return check_launch(c, "k_dir") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }

@@ -142,6 +142,7 @@ struct Ctx {
   double* colsum = nullptr;             // [4 MAXM] per-column totals of this rank (gamma; single-reduction CG:
                                         // + rho at [m, 2m), delta1 at [2m, 3m), delta2 at [3m, 4m))
   bool sr = false;                      // single-reduction CG (cg_variant 2, reading R23)
+  bool p_presplit = false;              // k_dir wrote the tf32 halves of P: the next tensor-core apply skips k_tc_split_p
   double* sr_part = nullptr;            // k_sr_dots CTA partials [3 MAXM][part_stride]
   unsigned* sr_cnt = nullptr;           // k_sr_dots last-CTA tickets [MAXM]
   int rank = 0, world = 1;
@@ -281,6 +282,7 @@ cofem_status dense_apply(Ctx* c, int m, int iter);
 bool dense_cluster_eligible(const Ctx* c);
 cofem_status dense_cluster_setup(Ctx* c);
 cofem_status dense_cluster_cg(Ctx* c, int K, double invK);
+void dense_tc_p_split(Ctx* c, float** ph, float** pl);   // the tensor-core path's P_hi / P_lo (or null)
 cofem_status dense_tc_setup(Ctx* c);
 cofem_status dense_tc_apply(Ctx* c, int m, int iter);
 void dense_tc_free(Ctx* c);

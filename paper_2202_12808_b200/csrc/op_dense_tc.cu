@@ -849,6 +849,12 @@ cofem_status dense_tc_setup(Ctx* c) {
   return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
 
+void dense_tc_p_split(Ctx* c, float** ph, float** pl) {
+  DenseTC* t = (DenseTC*)c->dense_tc;
+  *ph = t ? t->Ph : nullptr;
+  *pl = t ? t->Pl : nullptr;
+}
+
 cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   using namespace tc;
   DenseTC* t = (DenseTC*)c->dense_tc;
@@ -856,7 +862,10 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   const size_t sm = smem_of(t->pl);
   const int rows = BM * t->mt;
   launch_begin(c, KC_DENSE_PHI_P);
-  k_tc_split_p<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * c->Dp, (const float*)c->P, t->Ph, t->Pl);
+  // P_hi / P_lo: already written by the direction kernel (k_dir) when it ran just before this apply
+  if (!(c->p_presplit && iter > 0))
+    k_tc_split_p<<<c->num_sms * 4, 256, 0, c->stream>>>((int64_t)K * c->Dp, (const float*)c->P, t->Ph, t->Pl);
+  c->p_presplit = false;
   PhiPArgs a1;
   a1.pl = t->pl; a1.N = (int)c->N; a1.D = (int)c->D; a1.K = K; a1.kchunk = t->kchunk; a1.p0 = c->p0;
   a1.Wpart = t->Wpart; a1.W0part = t->W0part; a1.Npad = t->Npad;
