@@ -994,7 +994,7 @@ static cofem_status estep_body(Ctx* c, int K, int K_total) {
   }
   if (spersist) {
     launch_begin(c, KC_UPDATE);
-    k_sum_chunks<<<std::max(1, c->vec_grid), VEC_THREADS, 0, c->stream>>>(c->Dp, c->upd_chunks, c->s, c->s_part);
+    k_sum_chunks<<<c->num_sms * 4, VEC_THREADS, 0, c->stream>>>(c->Dp, c->upd_chunks, c->s, c->s_part);
     launch_end(c, KC_UPDATE);
     if (check_launch(c, "k_sum_chunks")) return COFEM_ERR_CUDA;
   }
