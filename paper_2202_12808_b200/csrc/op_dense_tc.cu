@@ -231,16 +231,21 @@ __device__ __forceinline__ float tf32_hi(float x) {
 #ifndef COFEM_TC_M3_PLAG
 #define COFEM_TC_M3_PLAG 2   // C2 E-step: 2 17.90 ms, 3 18.07, 4 18.04 (mode 1: 19.10)
 #endif
-__host__ __device__ constexpr int stages_of(int mode) { return mode == 2 ? 4 : mode == 3 ? COFEM_TC_M3_STAGES : 6; }
-__host__ __device__ constexpr int nacc_of(int mode) { return mode == 1 || mode == 3 ? 4 : 2; }
-__host__ __device__ constexpr int accw_of(int mode) { return mode == 3 ? 32 : mode == 1 ? 64 : 128; }
+// 4: bn <= 32, FUSED: one N = 2 bn = 64 MMA forms A_hi [B_hi | B_lo] and one N = bn MMA adds A_lo B_hi
+// (2 MMAs per K = 8 instead of 3, against the issuing thread's ~42 cycles per tcgen05.mma --
+// tools/tc_trace.py C2: 1009 of mode 3's 1579-cycle pair period), 4 accumulators of 64, four A
+// buffers.  Measured slower than mode 3 (C2 E-step 16.2 vs 15.5 ms): build switch only.
+__host__ __device__ constexpr int stages_of(int mode) { return mode == 2 ? 4 : (mode == 3 || mode == 4) ? COFEM_TC_M3_STAGES : 6; }
+__host__ __device__ constexpr int nacc_of(int mode) { return mode == 1 || mode == 3 || mode == 4 ? 4 : 2; }
+__host__ __device__ constexpr int accw_of(int mode) { return mode == 3 ? 32 : (mode == 1 || mode == 4) ? 64 : 128; }
 __host__ __device__ constexpr int nabuf_of(int mode) { return mode == 3 ? 6 : 4; }        // TMEM A buffers
 __host__ __device__ constexpr int tma_of(int mode) { return mode == 3 ? 128 : TM_A; }     // their base column
 __host__ __device__ constexpr int plag_of(int mode) { return mode == 3 ? COFEM_TC_M3_PLAG : PLAG; }
+__host__ __device__ constexpr bool fused_of(int mode) { return mode == 0 || mode == 4; }
 
 // Accumulator columns promoted (and written by the epilogue) per splitter group: the bn <= 64
 // logical columns split evenly over the 4 groups (128 / 4 in mode 2).
-__host__ __device__ constexpr int cpg_of(int mode) { return mode == 2 ? 32 : mode == 3 ? 8 : 16; }
+__host__ __device__ constexpr int cpg_of(int mode) { return mode == 2 ? 32 : (mode == 3 || mode == 4) ? 8 : 16; }
 
 // Shared-memory plan (dynamic, 1024-aligned):
 // STAGES x [A: MT tiles x 16 KB | Bhi bn x 128 B | Blo bn x 128 B | mean-column operand 32 x fp64 (1 KB)]
@@ -316,7 +321,7 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t tmem = bs.tmem_base;
   const int np = (nk + 1) >> 1;                     // K-step pairs (= promotion chunks)
-  constexpr bool fuse = MODE == 0;
+  constexpr bool fuse = fused_of(MODE);
   acc0[0] = 0.0;
 #pragma unroll
   for (int i = 0; i < CPG; ++i) sum[0][i] = 0.f;
@@ -405,10 +410,16 @@ __device__ void mainloop(const Plan& pl, unsigned char* sm, Bars& bs, const CUte
       if (q == 0 && lane == 0) TC_TRACE(4 * c + g, 7)
       fence_after();
 #pragma unroll
-      if constexpr (CPG == 8) {                         // mode 3: 8 columns per group
+      if constexpr (CPG == 8) {                         // modes 3 / 4: 8 columns per group
         if (g * CPG < pl.bn) {
           float v[8];
           tmem_ld8(lane_addr + TP::acc(ab, 0) + g * CPG, v);
+          if constexpr (fuse) {                         // + the hi.lo half of the N = 2 bn product
+            float u[8];
+            tmem_ld8(lane_addr + TP::acc(ab, 0) + pl.bn + g * CPG, u);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] += u[i];
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i) sum[0][i] += v[i];
         }
@@ -801,9 +812,9 @@ cofem_status dense_tc_setup(Ctx* c) {
   t->mode = t->bn > 64 ? 2 : 0;                   // timing comparison build (tools/build_variant.sh)
 #else
 #ifndef COFEM_TC_MODE3
-#define COFEM_TC_MODE3 1      // bn <= 32: mode 3 (three pairs of TMEM A buffers); 0 = mode 1 (A/B switch)
+#define COFEM_TC_MODE3 1      // bn <= 32: 1 = mode 3 (six A buffers), 2 = mode 4 (fused: C2 16.2 vs 15.5 ms, slower), 0 = mode 1
 #endif
-  t->mode = t->bn > 64 ? 2 : (COFEM_TC_MODE3 && t->bn <= 32 ? 3 : 1);
+  t->mode = t->bn > 64 ? 2 : (COFEM_TC_MODE3 && t->bn <= 32 ? (COFEM_TC_MODE3 == 2 ? 4 : 3) : 1);
 #endif
   t->pl = plan_for(t->bn, t->mt, t->mode);
   if (smem_of(t->pl) > 227 * 1024) { c->err = "dense tc: shared-memory plan too large"; return COFEM_ERR_INVALID; }
@@ -841,10 +852,12 @@ cofem_status dense_tc_setup(Ctx* c) {
   raise_smem_attr((const void*)k_tc_phiP<1>, sm);
   raise_smem_attr((const void*)k_tc_phiP<2>, sm);
   raise_smem_attr((const void*)k_tc_phiP<3>, sm);
+  raise_smem_attr((const void*)k_tc_phiP<4>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<0>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<1>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<2>, sm);
   raise_smem_attr((const void*)k_tc_phiTW<3>, sm);
+  raise_smem_attr((const void*)k_tc_phiTW<4>, sm);
   c->part_stride = std::max(c->part_stride, (int)((c->D + BM - 1) / BM));
   return check_launch(c, "dense tc setup") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }
@@ -874,6 +887,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   if (t->mode == 0) k_tc_phiP<0><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else if (t->mode == 1) k_tc_phiP<1><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else if (t->mode == 3) k_tc_phiP<3><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
+  else if (t->mode == 4) k_tc_phiP<4><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   else k_tc_phiP<2><<<g1, THREADS, sm, c->stream>>>(t->phi_k, t->phh, t->pll, a1);
   k_tc_reduce_w<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->N, t->Npad, K, t->splits, t->Wpart, t->W0part, t->Wh,
                                                        c->sharded ? nullptr : t->Wl, t->w0);
@@ -897,6 +911,7 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   if (t->mode == 0) k_tc_phiTW<0><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else if (t->mode == 1) k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else if (t->mode == 3) k_tc_phiTW<3><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
+  else if (t->mode == 4) k_tc_phiTW<4><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else k_tc_phiTW<2><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   launch_end(c, KC_DENSE_PHIT_W);
   if (check_launch(c, "k_tc_phiTW")) return COFEM_ERR_CUDA;
