@@ -257,7 +257,6 @@ struct Plan {
   __host__ __device__ int w_off(int s) const { return s * stage_bytes + mt * BM * BK * 4 + 2 * bn * 128; }
 };
 
-constexpr int MAXMT = 2;
 struct Bars {
   uint64_t full[8], split_done[4], pair_done[4], chunk_free[4];   // 4 phases apart: no parity aliasing
   uint32_t tmem_base;
