@@ -587,8 +587,9 @@ def main():
         # the whole CG loop in 8-CTA clusters, state in shared memory (op_dense_cluster.cu): the
         # bound is FP32 issue and the cluster barriers, not memory.  FP32 SIMT peak = SMs x 128 lanes
         # x 2 flop x max SM clock (B200_PROFILING unit counts); the kernel runs on 8 SMs per cluster,
-        # min(4, K) clusters (dcl_groups' default, probe_groups = 0: one probe share each)
+        # min(8, K, max(min(4, K), ceil(K / 4))) clusters (dcl_groups' default, probe_groups = 0)
         probe_ex = sum(sum(w.U if f < 0 else min(f + 1, w.U) for f in fz[1:]) for fz in frozen)
+        ncl = max(1, min(8, K_loc, max(min(4, K_loc), (K_loc + 3) // 4)))
         props = torch.cuda.get_device_properties(local)
         fmax = (clocks or {}).get("sm_max_mhz") or 1965.0
         fp32_peak = props.multi_processor_count * 128 * 2 * fmax * 1e6 / 1e12
@@ -597,8 +598,8 @@ def main():
         roof.update({"bound": "alu", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": ach / fp32_peak, "peak_source": "%d SMs x 128 FP32 lanes x 2 x %.0f MHz" %
                      (props.multi_processor_count, fmax),
-                     "frac_of_cluster_sms": ach / (fp32_peak * 8 * min(4, K_loc) / props.multi_processor_count),
-                     "cluster_sms": 8 * min(4, K_loc),
+                     "frac_of_cluster_sms": ach / (fp32_peak * 8 * ncl / props.multi_processor_count),
+                     "cluster_sms": 8 * ncl,
                      "achieved_def": "FP32 flops of the probe columns' two products (2 x 2 N D per executed "
                                      "column-iteration; the fp64 mean column not counted) / busy time"})
     if w.kind == "dense" and flush is not None:

@@ -109,7 +109,7 @@ typedef struct {
   /* Concurrent probe-column groups, 0 = auto.  1024 x 1024 DCT path: that many groups on their own
    * streams (auto 2, range 0..4).  Dense cluster CG loop: that many thread-block
    * clusters in one launch, each solving a contiguous share of the probes (cluster 0 also the mean;
-   * DESIGN.md §7.2.1; auto 4, at most K and 4).  Ignored elsewhere. */
+   * DESIGN.md §7.2.1; auto max(min(4, K), ceil(K/4)), at most K and 8).  Ignored elsewhere. */
   int32_t probe_groups;
   /* 1 (default): each E-step is captured once into a CUDA graph and replayed; 0: launched directly. */
   int32_t use_graph;

@@ -48,7 +48,7 @@ constexpr int NC = COFEM_DCL_NC;            // CTAs per cluster (8: the portable
 constexpr int THREADS = COFEM_DCL_THREADS;
 constexpr int KG = COFEM_DCL_KG;            // probe columns per thread work unit (register accumulators)
 
-constexpr int MAXCL = 4;                    // clusters per launch (probe-column groups)
+constexpr int MAXCL = 8;                    // clusters per launch (probe-column groups)
 
 struct Args {
   const float* phi; int64_t ld;
@@ -363,13 +363,12 @@ __global__ void __cluster_dims__(NC, 1, 1) __launch_bounds__(THREADS) k_dense_cl
   cl.sync();                         // no CTA leaves while others may still read its shared memory
 }
 
-__global__ void k_sum_parts(int64_t D, int ncl, double* __restrict__ s, const double* __restrict__ s1,
-                            const double* __restrict__ s2, const double* __restrict__ s3) {
+struct Parts { double* p[MAXCL]; };
+__global__ void k_sum_parts(int64_t D, int ncl, Parts sp) {
   for (int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; d < D; d += (int64_t)gridDim.x * blockDim.x) {
-    double v = s[d] + s1[d];
-    if (ncl > 2) v += s2[d];
-    if (ncl > 3) v += s3[d];
-    s[d] = v;
+    double v = sp.p[0][d];
+    for (int g = 1; g < ncl; ++g) v += sp.p[g][d];
+    sp.p[0][d] = v;
   }
 }
 
@@ -385,10 +384,12 @@ static size_t dcl_smem(const Ctx* c, int K) {
 // cluster's per-iteration loops (products, update, per-column dots) cover a quarter of the columns
 // while the barrier and reduction latency stays the same; options.probe_groups, else COFEM_DCL_GROUPS.
 #ifndef COFEM_DCL_GROUPS
-#define COFEM_DCL_GROUPS 4   // C1 E-step (fixed alpha): 1 cluster 1.36 ms, 2 1.13, 3 1.00, 4 1.00
-#endif
+#define COFEM_DCL_GROUPS 0   // 0 = auto: max(min(4, K), ceil(K / KG)) -- whole KG-column units per cluster
+#endif                       // (C1 E-step, fixed alpha: 1 cluster 1.36 ms, 2 1.13, 3 1.00, 4 0.99, 5 0.96, 7 0.96)
 static int dcl_groups(const Ctx* c, int K) {
-  int g = c->opt.probe_groups > 0 ? c->opt.probe_groups : COFEM_DCL_GROUPS;
+  int g = c->opt.probe_groups > 0 ? c->opt.probe_groups
+                                  : COFEM_DCL_GROUPS > 0 ? COFEM_DCL_GROUPS
+                                                         : std::max(std::min(4, K), (K + dcl::KG - 1) / dcl::KG);
   g = std::max(1, std::min(g, std::min(dcl::MAXCL, K)));
   while (g > 1 && !c->gs[g - 1]) --g;
   return g;
@@ -435,7 +436,11 @@ cofem_status dense_cluster_cg(Ctx* c, int K, double invK) {
   if (c->probe64) dcl::k_dense_cluster_cg<double><<<dcl::NC * a.ncl, dcl::THREADS, sm, c->stream>>>(a);
   else dcl::k_dense_cluster_cg<float><<<dcl::NC * a.ncl, dcl::THREADS, sm, c->stream>>>(a);
   if (a.ncl > 1)                      // s = ((s_0 + s_1) + s_2) + s_3 in cluster order (deterministic)
-    dcl::k_sum_parts<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, a.ncl, a.sg[0], a.sg[1], a.sg[2], a.sg[3]);
+  {
+    dcl::Parts sp;
+    for (int g = 0; g < dcl::MAXCL; ++g) sp.p[g] = a.sg[g];
+    dcl::k_sum_parts<<<c->num_sms * 2, 256, 0, c->stream>>>(c->D, a.ncl, sp);
+  }
   launch_end(c, KC_DENSE_CLUSTER);
   return check_launch(c, "k_dense_cluster_cg") == cudaSuccess ? COFEM_OK : COFEM_ERR_CUDA;
 }

@@ -644,7 +644,7 @@ def test_dense_cluster_cg_loop(w):
 @pytest.mark.parametrize("w", [synth.preset("C1"), synth.dense(64, 1000, 12, K=33, U=80, T=2, seed=9),
                                synth.dense(37, 203, 4, K=3, U=40, T=2, seed=8)], ids=lambda w: w.name)
 def test_dense_cluster_groups(w):
-    """The probe columns split over 1..4 thread-block clusters of one launch (probe_groups;
+    """The probe columns split over 1..8 thread-block clusters of one launch (probe_groups;
     op_dense_cluster.cu dcl_groups; more clusters than probes falls back to K): the mean system is
     cluster 0's whatever the split, so mu is bitwise the same; s differs only by the order of the
     clusters' partial sums (cluster order, deterministic: repeated runs are bitwise equal), and
@@ -653,7 +653,7 @@ def test_dense_cluster_groups(w):
     m1, s1 = gpu_estep(ctx_of(w, max_probes=w.K, probe_groups=1), w, np.ones(w.D), w.K, 3, 1)
     bar = max(1e-4, 2 * rel(s1, os_))
     em1 = gpu_em(ctx_of(w, max_probes=w.K, probe_groups=1), w, w.T, w.K, 5)
-    for g in (2, 3, 4):
+    for g in (2, 3, 4, 5, 8):
         ctx = ctx_of(w, max_probes=w.K, probe_groups=g)
         mu, s = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
         mu2, s2 = gpu_estep(ctx, w, np.ones(w.D), w.K, 3, 1)
