@@ -823,11 +823,16 @@ cofem_status dense_tc_setup(Ctx* c) {
   // split-K: the K1 grid (one CTA per SM) is sized to just fill whole waves (>= 8 K steps per split)
   const int ksteps = (int)((c->D + BK - 1) / BK);
   int splits = 1;
-  for (int w = 2; w <= 8; ++w) {
+  // from ONE wave up (C2: 16 M-tiles x 9 splits = 144 CTAs, E-step 15.7 -> 14.7 ms against 18 splits
+  // in two waves; fewer partials for k_tc_reduce_w too); C3 (64 M-tiles) still takes 9 splits
+  for (int w = 1; w <= 8; ++w) {
     const int sp = std::max(1, std::min(ksteps / 8, (w * c->num_sms) / mtiles));
     if (sp * mtiles >= (w * c->num_sms * 7) / 8) { splits = sp; break; }
     splits = sp;
   }
+#ifdef COFEM_TC_SPLITS
+  splits = std::max(1, std::min(ksteps, COFEM_TC_SPLITS));   // tuning build switch: force the K1 split count
+#endif
   t->kchunk = ((ksteps + splits - 1) / splits) * BK;
   t->splits = (int)((c->D + t->kchunk - 1) / t->kchunk);
   const size_t pk = (size_t)c->Kcap * c->Dp, wk = (size_t)c->Kcap * t->Npad;
