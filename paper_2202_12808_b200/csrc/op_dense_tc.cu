@@ -645,6 +645,9 @@ struct PhiTWArgs {
   const float* P; float* Q;
   ColState* cs; double* part; int stride; unsigned* counter; int iter;
   double* colsum;
+  // split-K over N (gridDim.y splits; build switch COFEM_TC_KSPLIT2): split partials [split][K][Dp] /
+  // [split][Dp]; the tile's last split (ticket) sums them in split order
+  float* Qpart; double* Q0part; unsigned* tile_cnt;
 };
 
 template <int MODE>
@@ -658,12 +661,53 @@ __global__ void __launch_bounds__(THREADS, 1) k_tc_phiTW(const __grid_constant__
   for (int i = threadIdx.x; i < NSPLIT * MAXM; i += THREADS) (&bs.red[0][0])[i] = 0.0;
   setup_cta(bs, a.pl.stages);
   const int row0 = blockIdx.x * BM * MT;
-  const int nk = (a.N + BK - 1) / BK;
+  const int nk_all = (a.N + BK - 1) / BK, ks = gridDim.y, split = blockIdx.y;
+  const int kchunk = (nk_all + ks - 1) / ks, kt0 = split * kchunk, nk = min(nk_all - kt0, kchunk);
   double acc0[MT];
   float sum[MT][cpg_of(MODE)];
-  mainloop<true, MODE>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, 0, nk, a.w0, acc0, sum);
+  mainloop<true, MODE>(a.pl, sm, bs, &mA, &mBh, &mBl, row0, kt0 * BK, nk, a.w0, acc0, sum);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m = a.K + 1;
+  if (ks > 1) {        // split-K: partials out; the tile's last split sums them in split order (deterministic)
+    if (warp >= 2) {
+      constexpr int CPG = cpg_of(MODE);
+      const int q = warp & 3, g = (warp - 2) >> 2, d = row0 + 32 * q + lane;
+      if (d < a.D) {
+#pragma unroll
+        for (int i = 0; i < CPG; ++i) {
+          const int k = g * CPG + i;
+          if (k < a.K) a.Qpart[((int64_t)split * a.K + k) * a.Dp + d] = sum[0][i];
+        }
+        if (g == 0) a.Q0part[(int64_t)split * a.Dp + d] = acc0[0];
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) bs.last = atomicAdd(a.tile_cnt + blockIdx.x, 1u) == (unsigned)ks - 1;
+    __syncthreads();
+    if (!bs.last) { teardown_cta(bs); return; }
+    __threadfence();
+    if (warp >= 2) {
+      constexpr int CPG = cpg_of(MODE);
+      const int q = warp & 3, g = (warp - 2) >> 2, d = row0 + 32 * q + lane;
+      if (d < a.D) {
+#pragma unroll
+        for (int i = 0; i < CPG; ++i) {
+          const int k = g * CPG + i;
+          if (k >= a.K) break;
+          float v = 0.f;
+          for (int sp = 0; sp < ks; ++sp) v += __ldcg(a.Qpart + ((int64_t)sp * a.K + k) * a.Dp + d);
+          sum[0][i] = v;
+        }
+        if (g == 0) {
+          double v = 0.0;
+          for (int sp = 0; sp < ks; ++sp) v += __ldcg(a.Q0part + (int64_t)sp * a.Dp + d);
+          acc0[0] = v;
+        }
+      }
+    }
+    if (threadIdx.x == 0) a.tile_cnt[blockIdx.x] = 0u;
+  }
   if (warp >= 2) {
     constexpr int CPG = cpg_of(MODE);
     const int wi = warp - 2, q = warp & 3, g = wi >> 2;
@@ -778,9 +822,10 @@ static size_t smem_of(const Plan& p) { return (size_t)p.stages * p.stage_bytes +
 
 struct DenseTC {
   CUtensorMap phi_k, phi_mn, phh, pll, whh, wll;
-  float *Ph, *Pl, *Wh, *Wl, *Wpart;
-  double *W0part, *w0;
-  int bn, mt, splits, kchunk, Npad;
+  float *Ph, *Pl, *Wh, *Wl, *Wpart, *Qpart;
+  double *W0part, *w0, *Q0part;
+  unsigned* tile_cnt;
+  int bn, mt, splits, kchunk, Npad, ksplit2;
   int mode;
   tc::Plan pl;
 };
@@ -788,7 +833,7 @@ struct DenseTC {
 void dense_tc_free(Ctx* c) {
   DenseTC* t = (DenseTC*)c->dense_tc;
   if (!t) return;
-  void* ptrs[] = {t->Ph, t->Pl, t->Wh, t->Wl, t->Wpart, t->W0part, t->w0};
+  void* ptrs[] = {t->Ph, t->Pl, t->Wh, t->Wl, t->Wpart, t->W0part, t->w0, t->Qpart, t->Q0part, t->tile_cnt};
   for (void* p : ptrs) if (p) cudaFree(p);
   delete t;
   c->dense_tc = nullptr;
@@ -840,6 +885,23 @@ cofem_status dense_tc_setup(Ctx* c) {
       cudaMalloc(&t->Wl, wk * 4) || cudaMalloc(&t->Wpart, (size_t)t->splits * wk * 4) ||
       cudaMalloc(&t->W0part, (size_t)t->splits * t->Npad * 8) || cudaMalloc(&t->w0, (size_t)t->Npad * 8)) {
     c->err = "cudaMalloc dense tensor-core workspace"; return COFEM_ERR_OOM;
+  }
+  {   // K2 split-K over N while the D tiles alone fill under half of the SMs: the splits stay in one
+      // wave, >= 8 K steps each (C2: 63 tiles x 2 = 126 CTAs, E-step 14.77 -> 13.65 ms; C3: 256 tiles,
+      // unsplit -- split-K measured slower there)
+#ifndef COFEM_TC_KSPLIT2
+#define COFEM_TC_KSPLIT2 0    // build switch: force the K2 split count (0 = the rule above)
+#endif
+    const int tiles2 = (int)((c->D + BM - 1) / BM), nk2 = (int)((c->N + BK - 1) / BK);
+    t->ksplit2 = COFEM_TC_KSPLIT2 > 0 ? COFEM_TC_KSPLIT2 : std::min(c->num_sms / std::max(tiles2, 1), nk2 / 8);
+    t->ksplit2 = std::max(1, std::min(t->ksplit2, nk2));
+    if (t->ksplit2 > 1) {
+      if (cudaMalloc(&t->Qpart, (size_t)t->ksplit2 * c->Kcap * c->Dp * 4) ||
+          cudaMalloc(&t->Q0part, (size_t)t->ksplit2 * c->Dp * 8) || cudaMalloc(&t->tile_cnt, (size_t)tiles2 * 4)) {
+        c->err = "cudaMalloc dense tensor-core split workspace"; return COFEM_ERR_OOM;
+      }
+      cudaMemset(t->tile_cnt, 0, (size_t)tiles2 * 4);
+    }
   }
   cudaMemset(t->Ph, 0, pk * 4); cudaMemset(t->Pl, 0, pk * 4);
   cudaMemset(t->Wh, 0, wk * 4); cudaMemset(t->Wl, 0, wk * 4);
@@ -910,8 +972,9 @@ cofem_status dense_tc_apply(Ctx* c, int m, int iter) {
   a2.alpha = c->alpha; a2.w0 = t->w0; a2.p0 = c->p0; a2.q0 = c->q0; a2.P = (const float*)c->P; a2.Q = (float*)c->Q;
   a2.cs = c->cs; a2.part = c->part; a2.stride = c->part_stride; a2.counter = c->counters + MAXM; a2.iter = iter;
   a2.colsum = c->sharded ? c->colsum : nullptr;
+  a2.Qpart = t->Qpart; a2.Q0part = t->Q0part; a2.tile_cnt = t->tile_cnt;
   launch_begin(c, KC_DENSE_PHIT_W);
-  const unsigned g2 = (unsigned)((c->D + rows - 1) / rows);
+  const dim3 g2((unsigned)((c->D + rows - 1) / rows), (unsigned)t->ksplit2);
   if (t->mode == 0) k_tc_phiTW<0><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else if (t->mode == 1) k_tc_phiTW<1><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
   else if (t->mode == 3) k_tc_phiTW<3><<<g2, THREADS, sm, c->stream>>>(t->phi_mn, t->whh, t->wll, a2);
